@@ -1,0 +1,1033 @@
+// pod_attn.cu -- sm_100a kernels of the POD-Attention hot path and the C ABI
+// run entry points (include/pod_attn.h).
+//
+//   prefill role : causal chunked-prefill tile; QK^T and PV on tcgen05 with
+//                  TMEM accumulators, K/V/Q staged by TMA (128B swizzle);
+//                  semantics of tiled_prefill_attention (attention.hpp:148-222)
+//                  restricted to the CTA's kv split, emitting O and LSE.
+//   decode role  : split-KV paged decode on CUDA cores, one warp per virtual
+//                  decode CTA (work_decomp.hpp:179-197),
+//                  online softmax + warp-shuffle reductions, in-CTA LSE merge
+//                  of the 4 virtual CTAs; semantics of decode_attention_splitk
+//                  (attention.hpp:240-292).
+//   merge        : LSE merge of split partials (merge_partials, attention.hpp:294-326).
+//   fused kernel : SM-aware runtime role binding (PAPER.md:387-423,
+//                  gpu_sim.hpp:114-131) over P + D CTAs, counters self-reset.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "pod_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace pod {
+
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& s) { g_last_error = s; }
+
+// ------------------------------------------------------------ smem plan --
+// Prefill role (offsets from the 1024-aligned dynamic smem base):
+constexpr uint32_t kQBytes = kMBlock * kHeadDim * 2;        // 32 KB: 2 swizzle columns of 128 x 128B
+constexpr uint32_t kKvStageBytes = kKvTile * kHeadDim * 2;  // 16 KB
+constexpr uint32_t kOffQ = 0;
+constexpr uint32_t kOffK = kOffQ + kQBytes;                 // 2 stages
+constexpr uint32_t kOffV = kOffK + 2 * kKvStageBytes;       // 2 stages
+constexpr uint32_t kOffP = kOffV + 2 * kKvStageBytes;       // 128 x 64 bf16 = 16 KB
+constexpr uint32_t kOffBar = kOffP + kMBlock * kKvTile * 2;
+constexpr uint32_t kOffTmemSlot = kOffBar + 128;
+constexpr uint32_t kOffRole = kOffTmemSlot + 16;
+constexpr uint32_t kSmemBytes = kOffBar + 256;              // 114944 B -> 2 CTAs / SM
+static_assert(kSmemBytes * 2 + 2048 <= 233472, "two CTAs must fit one SM");
+constexpr uint32_t kTmemCols = 256;                         // S0 | S1 | O(128)
+constexpr uint32_t kTmemS0 = 0, kTmemO = 128;
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct RunParams {
+    const void* q_decode;
+    const void* k_pool;
+    const void* v_pool;
+    const int32_t* page_indptr;
+    const int32_t* page_indices;
+    float* o_prefill;
+    float* lse_prefill;
+    float* o_decode;
+    float* lse_decode;
+    float* ppart_o;
+    float* ppart_lse;
+    float* dpart_o;
+    float* dpart_lse;
+    const PrefillCta* pctas;
+    const DecodeCta* dctas;
+    SchedCounters* ctr;
+    int32_t* role_log;
+    int32_t num_pctas;
+    int32_t num_dctas;
+    int32_t prefill_ratio;
+    int32_t decode_ratio;
+    int32_t hq;
+    int32_t hkv;
+    int32_t group;
+    int32_t chunk;
+    int32_t offset;
+    int32_t kv_layout;
+    int32_t decode_splits;
+    int32_t pad0;
+    int64_t num_pages;
+    float sl2;  // log2(e) / scale  (scale is the reference's divisor)
+};
+
+// ============================================================ prefill ===
+template <int kFmt>
+__device__ __forceinline__ void prefill_issue_qk(uint32_t tmem_s, uint32_t sQ, uint32_t sK) {
+    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kKvTile, 0);
+#pragma unroll
+    for (int kk = 0; kk < kHeadDim / 16; ++kk) {
+        const uint32_t koff = (kk & 3) * 32u;  // 16 elements = 32 B inside the 128 B swizzle row
+        const uint64_t a = ptx::sw128_desc(sQ + (kk >> 2) * (kMBlock * 128) + koff, 16, 1024);
+        const uint64_t b = ptx::sw128_desc(sK + (kk >> 2) * (kKvTile * 128) + koff, 16, 1024);
+        ptx::umma_f16_ss(tmem_s, a, b, idesc, kk > 0 ? 1u : 0u);
+    }
+}
+
+template <int kFmt>
+__device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t sP, uint32_t sV,
+                                                 bool accumulate) {
+    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);
+#pragma unroll
+    for (int kk = 0; kk < kKvTile / 16; ++kk) {
+        const uint64_t a = ptx::sw128_desc(sP + kk * 32, 16, 1024);
+        const uint64_t b = ptx::sw128_desc(sV + kk * 2048, kKvTile * 128, 1024);
+        ptx::umma_f16_ss(tmem_o, a, b, idesc, (accumulate || kk > 0) ? 1u : 0u);
+    }
+}
+
+struct BlockRange {
+    int r0;      // first chunk row of the block
+    int nrows;   // chunk rows in the block
+    int kt0;     // first key of tile 0 (page aligned)
+    int nt;      // kv tiles
+};
+
+__device__ __forceinline__ BlockRange prefill_block(const RunParams& p, const PrefillCta& job,
+                                                    int b) {
+    const int rpb = kMBlock / p.group;
+    BlockRange br;
+    br.r0 = job.row_begin + b * rpb;
+    br.nrows = min(rpb, job.rows - b * rpb);
+    const int r_last = br.r0 + br.nrows - 1;
+    const int kv_hi = min(job.kv_end, p.offset + r_last + 1);
+    br.kt0 = (job.kv_begin / 16) * 16;
+    br.nt = kv_hi > job.kv_begin ? (kv_hi - br.kt0 + kKvTile - 1) / kKvTile : 0;
+    return br;
+}
+
+// Issue the 8 TMA boxes (4 pages x 2 swizzle columns) of one 64-key tile.
+__device__ __forceinline__ void prefill_load_kv_tile(const RunParams& p, const CUtensorMap* tm,
+                                                     uint32_t dst, uint32_t bar, int kt, int kv_head,
+                                                     int pbeg, int npages) {
+#pragma unroll
+    for (int pg = 0; pg < kKvTile / 16; ++pg) {
+        const int lp = min(kt / 16 + pg, npages - 1);
+        const int phys = __ldg(p.page_indices + pbeg + lp);
+#pragma unroll
+        for (int dh = 0; dh < 2; ++dh) {
+            const uint32_t d = dst + dh * (kKvTile * 128) + pg * 2048;
+            if (p.kv_layout == POD_KV_HND)
+                ptx::tma_load_4d(d, tm, bar, dh * 64, 0, kv_head, phys);
+            else
+                ptx::tma_load_4d(d, tm, bar, dh * 64, kv_head, 0, phys);
+        }
+    }
+}
+
+template <int kFmt>
+__device__ void prefill_cta(const RunParams& p, const CUtensorMap* tmq, const CUtensorMap* tmk,
+                            const CUtensorMap* tmv, int cta_id, uint8_t* smem) {
+    const PrefillCta job = p.pctas[cta_id];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t sbase = ptx::smem_u32(smem);
+    const uint32_t sQ = sbase + kOffQ, sK = sbase + kOffK, sV = sbase + kOffV, sP = sbase + kOffP;
+    const uint32_t bar0 = sbase + kOffBar;
+    const uint32_t b_qfull = bar0 + 0, b_qempty = bar0 + 8;
+    const uint32_t b_kfull = bar0 + 16, b_kempty = bar0 + 32;  // [2] each, 8 B apart
+    const uint32_t b_vfull = bar0 + 48, b_vempty = bar0 + 64;
+    const uint32_t b_sfull = bar0 + 80;                        // [2]
+    const uint32_t b_pv = bar0 + 96;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
+
+    const int G = p.group;
+    const int rpb = kMBlock / G;
+    const int nblocks = (job.rows + rpb - 1) / rpb;
+    const int pbeg = p.page_indptr[0];
+    const int npages = p.page_indptr[1] - pbeg;
+
+    if (tid == 0) {
+        if (sbase & 1023u) __trap();  // SW128 atoms need a 1024-aligned base
+        for (int i = 0; i < 13; ++i) ptx::mbar_init(bar0 + 8 * i, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) {
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), kTmemCols);
+        ptx::tmem_relinquish();
+    }
+    if (warp == 4 && lane == 0) {
+        ptx::prefetch_tmap(tmq);
+        ptx::prefetch_tmap(tmk);
+        ptx::prefetch_tmap(tmv);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        // ------------------------------------------------ TMA producer --
+        if (lane == 0) {
+            int g = 0, qb = 0;
+            for (int b = 0; b < nblocks; ++b) {
+                const BlockRange br = prefill_block(p, job, b);
+                if (br.nt == 0) continue;
+                if (qb > 0) ptx::mbar_wait(b_qempty, (qb - 1) & 1);
+                ptx::mbar_arrive_expect_tx(b_qfull, kQBytes);
+                ptx::tma_load_3d(sQ, tmq, b_qfull, 0, job.kv_head * G, br.r0);
+                ptx::tma_load_3d(sQ + kMBlock * 128, tmq, b_qfull, 64, job.kv_head * G, br.r0);
+                ++qb;
+                for (int t = 0; t <= br.nt; ++t) {
+                    if (t < br.nt) {  // K of tile t
+                        const int gg = g + t, st = gg & 1;
+                        if (gg >= 2) ptx::mbar_wait(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
+                        ptx::mbar_arrive_expect_tx(b_kfull + 8 * st, kKvStageBytes);
+                        prefill_load_kv_tile(p, tmk, sK + st * kKvStageBytes, b_kfull + 8 * st,
+                                             br.kt0 + t * kKvTile, job.kv_head, pbeg, npages);
+                    }
+                    if (t > 0) {  // V of tile t-1
+                        const int gg = g + t - 1, st = gg & 1;
+                        if (gg >= 2) ptx::mbar_wait(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
+                        ptx::mbar_arrive_expect_tx(b_vfull + 8 * st, kKvStageBytes);
+                        prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
+                                             br.kt0 + (t - 1) * kKvTile, job.kv_head, pbeg, npages);
+                    }
+                }
+                g += br.nt;
+            }
+        }
+    } else {
+        // ------------------------------ softmax / MMA-issue (128 threads) --
+        const int m = tid;  // TMEM lane == M row
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        int g = 0, qb = 0;
+        for (int b = 0; b < nblocks; ++b) {
+            const BlockRange br = prefill_block(p, job, b);
+            const int my_r = br.r0 + m / G;
+            const int my_g = m % G;
+            const bool row_ok = (m / G) < br.nrows;
+            const int vis = p.offset + my_r;  // last visible key (inclusive)
+            const int qhead = job.kv_head * G + my_g;
+            float* orow;
+            float* lrow;
+            if (job.n_splits == 1) {
+                orow = p.o_prefill + (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim;
+                lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
+            } else {
+                const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
+                orow = p.ppart_o + row * kHeadDim;
+                lrow = p.ppart_lse + row;
+            }
+            if (br.nt == 0) {
+                if (row_ok) {
+                    for (int c = 0; c < kHeadDim; c += 4)
+                        *reinterpret_cast<float4*>(orow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                    *lrow = -INFINITY;
+                }
+                continue;
+            }
+            if (tid == 0) {
+                ptx::mbar_wait(b_qfull, qb & 1);
+                const int st = g & 1;
+                ptx::mbar_wait(b_kfull + 8 * st, (g >> 1) & 1);
+                ptx::tc_fence_after();
+                prefill_issue_qk<kFmt>(tmem + kTmemS0 + st * kKvTile, sQ, sK + st * kKvStageBytes);
+                ptx::umma_commit(b_sfull + 8 * st);
+                ptx::umma_commit(b_kempty + 8 * st);
+                if (br.nt == 1) ptx::umma_commit(b_qempty);
+            }
+            float m_run = -INFINITY, l_run = 0.f;
+            for (int t = 0; t < br.nt; ++t) {
+                const int gg = g + t, st = gg & 1;
+                if (tid == 0 && t + 1 < br.nt) {
+                    const int g1 = gg + 1, s1 = g1 & 1;
+                    ptx::mbar_wait(b_kfull + 8 * s1, (g1 >> 1) & 1);
+                    ptx::tc_fence_after();
+                    prefill_issue_qk<kFmt>(tmem + kTmemS0 + s1 * kKvTile, sQ, sK + s1 * kKvStageBytes);
+                    ptx::umma_commit(b_sfull + 8 * s1);
+                    ptx::umma_commit(b_kempty + 8 * s1);
+                    if (t + 2 == br.nt) ptx::umma_commit(b_qempty);
+                }
+                // S tile -> registers
+                ptx::mbar_wait(b_sfull + 8 * st, (gg >> 1) & 1);
+                ptx::tc_fence_after();
+                float s[kKvTile];
+                ptx::tmem_ld32(lane_base + kTmemS0 + st * kKvTile, *reinterpret_cast<float(*)[32]>(&s[0]));
+                ptx::tmem_ld32(lane_base + kTmemS0 + st * kKvTile + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+                ptx::tmem_wait_ld();
+                const int kb = br.kt0 + t * kKvTile;
+                // valid keys: [lo, hi) within this tile for this row
+                const int lo = max(job.kv_begin - kb, 0);
+                const int hi = row_ok ? min(min(job.kv_end, vis + 1) - kb, kKvTile) : 0;
+                float tmax = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < kKvTile; ++c) {
+                    const bool ok = (c >= lo) && (c < hi);
+                    s[c] = ok ? s[c] * p.sl2 : -INFINITY;
+                    tmax = fmaxf(tmax, s[c]);
+                }
+                const float m_new = fmaxf(m_run, tmax);
+                // lazy rescale (only when the max grows by > 2^8): exact algebra,
+                // the stale reference max bounds p by 256.
+                const bool need = m_new > m_run + 8.f;
+                const float m_use = need ? m_new : m_run;
+                const float factor = need ? ptx::ex2(m_run - m_new) : 1.f;
+                l_run *= factor;
+                m_run = m_use;
+                uint32_t pk[kKvTile / 2];
+                float lsum = 0.f;
+                if (m_use == -INFINITY) {
+#pragma unroll
+                    for (int c = 0; c < kKvTile / 2; ++c) pk[c] = 0u;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < kKvTile; c += 2) {
+                        const float p0 = ptx::ex2(s[c] - m_use);
+                        const float p1 = ptx::ex2(s[c + 1] - m_use);
+                        lsum += p0 + p1;
+                        if constexpr (kFmt == 1) {
+                            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+                            pk[c / 2] = *reinterpret_cast<uint32_t*>(&h);
+                        } else {
+                            __half2 h = __floats2half2_rn(p0, p1);
+                            pk[c / 2] = *reinterpret_cast<uint32_t*>(&h);
+                        }
+                    }
+                }
+                l_run += lsum;
+                // PV of the previous tile must be complete before O or P are touched.
+                if (t > 0) {
+                    ptx::mbar_wait(b_pv, (gg - 1) & 1);
+                    ptx::tc_fence_after();
+                    if (__any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+                        for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+                            float o[32];
+                            ptx::tmem_ld32(lane_base + kTmemO + ch * 32, o);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) o[c] *= factor;
+                            ptx::tmem_st32(lane_base + kTmemO + ch * 32, o);
+                        }
+                        ptx::tmem_wait_st();
+                    }
+                }
+                // P row -> smem, SW128 K-major: 16 B chunk c of row m at chunk c ^ (m & 7).
+                {
+                    uint8_t* prow = smem + kOffP + m * 128;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        *reinterpret_cast<uint4*>(prow + ((c ^ (m & 7)) << 4)) =
+                            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                    }
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::tc_fence_before();
+                ptx::named_bar_sync(1, 128);
+                if (tid == 0) {
+                    ptx::tc_fence_after();
+                    ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
+                    prefill_issue_pv<kFmt>(tmem + kTmemO, sP, sV + st * kKvStageBytes, t > 0);
+                    ptx::umma_commit(b_pv);
+                    ptx::umma_commit(b_vempty + 8 * st);
+                }
+            }
+            // ------------------------------------------------- epilogue --
+            ptx::mbar_wait(b_pv, (g + br.nt - 1) & 1);
+            ptx::tc_fence_after();
+            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll 1
+            for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+                float o[32];
+                ptx::tmem_ld32(lane_base + kTmemO + ch * 32, o);
+                ptx::tmem_wait_ld();
+                if (row_ok) {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4)
+                        *reinterpret_cast<float4*>(orow + ch * 32 + c) =
+                            make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv);
+                }
+            }
+            if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
+            ptx::tc_fence_before();
+            g += br.nt;
+            ++qb;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, kTmemCols);
+    }
+}
+
+// ============================================================= decode ===
+template <int kFmt>
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if constexpr (kFmt == 1) {
+            f[2 * i] = __uint_as_float(w[i] << 16);
+            f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+        } else {
+            const float2 x = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+            f[2 * i] = x.x;
+            f[2 * i + 1] = x.y;
+        }
+    }
+}
+
+// One physical decode CTA: 4 warps = 4 virtual decode CTAs over
+// split_ranges(kv_end - kv_begin, 4).  Lane l owns key slot (l >> 4) of each key
+// pair and d-elements [8 (l & 15), +8).
+template <int G, int kFmt>
+__device__ void decode_cta(const RunParams& p, int cta_id, uint8_t* smem) {
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    if (warp >= kDecodeWarps) return;
+    const DecodeCta job = p.dctas[cta_id];
+    const int len = job.kv_end - job.kv_begin;
+    const int base = len / kDecodeWarps, rem = len % kDecodeWarps;
+    const int wb = job.kv_begin + warp * base + min(warp, rem);
+    const int we = wb + base + (warp < rem ? 1 : 0);
+    const int half = lane >> 4, c8 = (lane & 15) * 8;
+    const int h = job.kv_head;
+
+    using elem_t = uint16_t;
+    const elem_t* q = static_cast<const elem_t*>(p.q_decode) +
+                      (static_cast<size_t>(job.request) * p.hq + h * G) * kHeadDim + c8;
+    float qf[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const uint4 v = *reinterpret_cast<const uint4*>(q + g * kHeadDim);
+        unpack8<kFmt>(v, qf[g]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) qf[g][e] *= p.sl2;
+    }
+    float m[G], l[G], o[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        m[g] = -INFINITY;
+        l[g] = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[g][e] = 0.f;
+    }
+
+    const elem_t* kp = static_cast<const elem_t*>(p.k_pool);
+    const elem_t* vp = static_cast<const elem_t*>(p.v_pool);
+    const size_t key_stride = p.kv_layout == POD_KV_HND ? kHeadDim : static_cast<size_t>(p.hkv) * kHeadDim;
+    const int32_t* pidx = p.page_indices + p.page_indptr[job.page_row];
+    if (we > wb) {
+        const int pg0 = wb >> 4, pg1 = (we - 1) >> 4;
+        int cached_base = -1000000;
+        int cached = 0;
+        for (int pg = pg0; pg <= pg1; ++pg) {
+            if (pg - cached_base >= 32 || pg < cached_base) {
+                cached_base = pg;
+                cached = (pg + lane <= pg1) ? __ldg(pidx + pg + lane) : 0;
+            }
+            const int phys = __shfl_sync(0xffffffffu, cached, pg - cached_base);
+            size_t off;
+            if (p.kv_layout == POD_KV_HND)
+                off = (static_cast<size_t>(phys) * p.hkv + h) * 16 * kHeadDim;
+            else
+                off = (static_cast<size_t>(phys) * 16 * p.hkv + h) * kHeadDim;
+            const elem_t* kpg = kp + off + c8;
+            const elem_t* vpg = vp + off + c8;
+            uint4 kr[8], vr[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) kr[i] = ptx::ldg_nc_v4(kpg + (2 * i + half) * key_stride);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vr[i] = ptx::ldg_nc_v4(vpg + (2 * i + half) * key_stride);
+            float s[8][G];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float kf[8];
+                unpack8<kFmt>(kr[i], kf);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc = fmaf(qf[g][e], kf[e], acc);
+                    s[i][g] = acc;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    float a = s[i][g];
+                    a += __shfl_xor_sync(0xffffffffu, a, 1);
+                    a += __shfl_xor_sync(0xffffffffu, a, 2);
+                    a += __shfl_xor_sync(0xffffffffu, a, 4);
+                    a += __shfl_xor_sync(0xffffffffu, a, 8);
+                    s[i][g] = a;
+                }
+            const int kbase = pg * 16 + half;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int key = kbase + 2 * i;
+                if (key < wb || key >= we) {
+#pragma unroll
+                    for (int g = 0; g < G; ++g) s[i][g] = -INFINITY;
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                float mx = s[0][g];
+#pragma unroll
+                for (int i = 1; i < 8; ++i) mx = fmaxf(mx, s[i][g]);
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                const float m_new = fmaxf(m[g], mx);
+                const float f = ptx::ex2(m[g] - m_new);  // m = -inf -> 0
+                m[g] = m_new;
+                l[g] *= f;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) o[g][e] *= f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float pr = ptx::ex2(s[i][g] - m_new);
+                    s[i][g] = pr;
+                    l[g] += pr;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float vf[8];
+                unpack8<kFmt>(vr[i], vf);
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) o[g][e] = fmaf(s[i][g], vf[e], o[g][e]);
+            }
+        }
+    }
+    // combine the two key halves of the warp
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        l[g] += __shfl_xor_sync(0xffffffffu, l[g], 16);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[g][e] += __shfl_xor_sync(0xffffffffu, o[g][e], 16);
+    }
+    // in-CTA merge of the 4 virtual CTAs (LSE merge, attention.hpp:294-326)
+    constexpr int kStride = kHeadDim + 4;
+    float* red = reinterpret_cast<float*>(smem);
+    if (half == 0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float* dst = red + (warp * G + g) * kStride;
+            *reinterpret_cast<float4*>(dst + c8) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+            *reinterpret_cast<float4*>(dst + c8 + 4) = make_float4(o[g][4], o[g][5], o[g][6], o[g][7]);
+            if (lane == 0) {
+                dst[kHeadDim] = m[g];
+                dst[kHeadDim + 1] = l[g];
+            }
+        }
+    }
+    ptx::named_bar_sync(2, kDecodeWarps * 32);
+    for (int idx = tid; idx < G * kHeadDim; idx += kDecodeWarps * 32) {
+        const int g = idx / kHeadDim, d = idx % kHeadDim;
+        float mw[kDecodeWarps], M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kDecodeWarps; ++w) {
+            mw[w] = red[(w * G + g) * kStride + kHeadDim];
+            M = fmaxf(M, mw[w]);
+        }
+        float L = 0.f, acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < kDecodeWarps; ++w) {
+            const float wt = ptx::ex2(mw[w] - M);  // empty warp: m = -inf -> 0
+            L += red[(w * G + g) * kStride + kHeadDim + 1] * wt;
+            acc += red[(w * G + g) * kStride + d] * wt;
+        }
+        const int qhead = h * G + g;
+        const float out = acc / L;
+        const float lse = (M + ptx::lg2(L)) * kLn2;
+        if (job.n_splits == 1) {
+            p.o_decode[(static_cast<size_t>(job.request) * p.hq + qhead) * kHeadDim + d] = out;
+            if (d == 0) p.lse_decode[static_cast<size_t>(job.request) * p.hq + qhead] = lse;
+        } else {
+            const size_t row = (static_cast<size_t>(job.request) * p.decode_splits + job.split) * p.hq + qhead;
+            p.dpart_o[row * kHeadDim + d] = out;
+            if (d == 0) p.dpart_lse[row] = lse;
+        }
+    }
+}
+
+// ============================================================== merge ===
+// One warp per output (row, q head): O = sum_i exp(lse_i - lse_tot) O_i in
+// split order (= kv-range order), lse_tot = m + log(sum exp(lse_i - m)).
+// mode 0: prefill rows r in [0, chunk); partials [split][chunk][Hq][d].
+// mode 1: decode requests; partials [req][splits][Hq][d].
+__global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* tile_splits,
+                                                    int tile_q, int mode, int nrows) {
+    const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp_global >= nrows) return;
+    const int r = warp_global / p.hq, qh = warp_global % p.hq;
+    int n;
+    const float* po;
+    const float* pl;
+    size_t stride_o, stride_l;
+    float* out_o;
+    float* out_l;
+    if (mode == 0) {
+        n = tile_splits[r / tile_q];
+        if (n <= 1) return;
+        const size_t row = static_cast<size_t>(r) * p.hq + qh;
+        po = p.ppart_o + row * kHeadDim;
+        pl = p.ppart_lse + row;
+        stride_l = static_cast<size_t>(p.chunk) * p.hq;
+        stride_o = stride_l * kHeadDim;
+        out_o = p.o_prefill + row * kHeadDim;
+        out_l = p.lse_prefill + row;
+    } else {
+        n = p.decode_splits;  // uniform per plan (clamped to the shortest context)
+        if (n <= 1) return;
+        const size_t row = static_cast<size_t>(r) * p.decode_splits * p.hq + qh;
+        po = p.dpart_o + row * kHeadDim;
+        pl = p.dpart_lse + row;
+        stride_l = p.hq;
+        stride_o = stride_l * kHeadDim;
+        out_o = p.o_decode + (static_cast<size_t>(r) * p.hq + qh) * kHeadDim;
+        out_l = p.lse_decode + static_cast<size_t>(r) * p.hq + qh;
+    }
+    float M = -INFINITY;
+    for (int i = 0; i < n; ++i) M = fmaxf(M, pl[i * stride_l]);
+    float tot = 0.f;
+    for (int i = 0; i < n; ++i) tot += ptx::ex2((pl[i * stride_l] - M) * kLog2e);
+    const float lse_tot = M + ptx::lg2(tot) * kLn2;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < n; ++i) {
+        const float w = ptx::ex2((pl[i * stride_l] - lse_tot) * kLog2e);
+        const float4 v = *reinterpret_cast<const float4*>(po + i * stride_o + lane * 4);
+        acc.x += w * v.x;
+        acc.y += w * v.y;
+        acc.z += w * v.z;
+        acc.w += w * v.w;
+    }
+    *reinterpret_cast<float4*>(out_o + lane * 4) = acc;
+    if (lane == 0) *out_l = lse_tot;
+}
+
+// ============================================================ kernels ===
+template <int G, int kFmt>
+__global__ void __launch_bounds__(kThreads, 2)
+    pod_fused_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmq,
+                     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    int* role = reinterpret_cast<int*>(smem + kOffRole);
+    if (threadIdx.x == 0) {
+        // SM-aware CTA scheduling (gpu_sim.hpp:114-131)
+        const uint32_t sm = ptx::smid();
+        const int ratio = p.prefill_ratio + p.decode_ratio;
+        const uint32_t raw = atomicAdd(&p.ctr->sm_ctr[sm], 1u);
+        const int ticket = static_cast<int>(raw % static_cast<uint32_t>(ratio));
+        int op = ticket < p.prefill_ratio ? 0 : 1;
+        int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
+        if (id >= (op == 0 ? p.num_pctas : p.num_dctas)) {
+            op ^= 1;
+            id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
+            if (id >= (op == 0 ? p.num_pctas : p.num_dctas)) op = -1;
+        }
+        role[0] = op;
+        role[1] = id;
+        if (p.role_log) {
+            const uint32_t arrival = atomicAdd(&p.ctr->arrival, 1u);
+            int32_t* rec = p.role_log + 8 * blockIdx.x;
+            rec[0] = static_cast<int32_t>(sm);
+            rec[1] = static_cast<int32_t>(raw);
+            rec[2] = op;
+            rec[3] = id;
+            rec[4] = static_cast<int32_t>(arrival);
+            rec[5] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
+            rec[7] = static_cast<int32_t>(blockIdx.x);
+        }
+    }
+    __syncthreads();
+    const int op = role[0], id = role[1];
+    if (op == 0)
+        prefill_cta<kFmt>(p, &tmq, &tmk, &tmv, id, smem);
+    else if (op == 1)
+        decode_cta<G, kFmt>(p, id, smem);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (p.role_log) p.role_log[8 * blockIdx.x + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
+        __threadfence();
+        const uint32_t total = static_cast<uint32_t>(p.num_pctas + p.num_dctas);
+        const uint32_t prev = atomicAdd(&p.ctr->done, 1u);
+        if (prev == total - 1) {
+            // last CTA out: re-arm the counters for the next launch (graph friendly)
+            const uint32_t n = min(ptx::nsmid(), static_cast<uint32_t>(kMaxSms));
+            for (uint32_t i = 0; i < n; ++i) p.ctr->sm_ctr[i] = 0;
+            p.ctr->cta_assign[0] = 0;
+            p.ctr->cta_assign[1] = 0;
+            p.ctr->arrival = 0;
+            p.ctr->done = 0;
+            __threadfence();
+        }
+    }
+}
+
+template <int kFmt>
+__global__ void __launch_bounds__(kThreads, 2)
+    pod_prefill_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmq,
+                       const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    prefill_cta<kFmt>(p, &tmq, &tmk, &tmv, blockIdx.x, smem);
+}
+
+template <int G, int kFmt>
+__global__ void __launch_bounds__(kDecodeWarps * 32, 3) pod_decode_kernel(const __grid_constant__ RunParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    decode_cta<G, kFmt>(p, blockIdx.x, smem);
+}
+
+__global__ void gather_probe_kernel(const uint16_t* pool, int layout, int hkv, const int32_t* indptr,
+                                    const int32_t* indices, int req, int ctx, uint16_t* out) {
+    const size_t n = static_cast<size_t>(ctx) * hkv * (kHeadDim / 8);
+    for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int chunk = static_cast<int>(i % (kHeadDim / 8));
+        const int h = static_cast<int>((i / (kHeadDim / 8)) % hkv);
+        const int t = static_cast<int>(i / (kHeadDim / 8) / hkv);
+        const int phys = indices[indptr[req] + t / 16];
+        const int slot = t % 16;
+        size_t src;
+        if (layout == POD_KV_HND)
+            src = ((static_cast<size_t>(phys) * hkv + h) * 16 + slot) * kHeadDim;
+        else
+            src = ((static_cast<size_t>(phys) * 16 + slot) * hkv + h) * kHeadDim;
+        const uint4 v = *reinterpret_cast<const uint4*>(pool + src + chunk * 8);
+        *reinterpret_cast<uint4*>(out + (static_cast<size_t>(t) * hkv + h) * kHeadDim + chunk * 8) = v;
+    }
+}
+
+// ================================================================ host ===
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    });
+    return fn;
+}
+
+pod_status cuda_fail(cudaError_t e, const char* where) {
+    set_last_error(std::string(where) + ": " + cudaGetErrorString(e));
+    return POD_ERR_CUDA;
+}
+
+int64_t fused_smem_bytes() { return kSmemBytes; }
+
+struct Maps {
+    CUtensorMap q, k, v;
+};
+
+pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_pool, const void* v_pool,
+                     int64_t num_pages, Maps* m) {
+    std::memset(m, 0, sizeof(*m));
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) {
+        set_last_error("cuTensorMapEncodeTiled unavailable");
+        return POD_ERR_CUDA;
+    }
+    const CUtensorMapDataType dt = plan->batch.dtype == POD_DTYPE_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                                       : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const int hkv = plan->shape.num_kv_heads, hq = plan->shape.num_q_heads;
+    const int G = hq / hkv;
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    {
+        cuuint64_t dims[4], strides[3];
+        cuuint32_t box[4];
+        if (plan->batch.kv_layout == POD_KV_HND) {
+            dims[0] = kHeadDim; dims[1] = 16; dims[2] = hkv; dims[3] = num_pages;
+            strides[0] = kHeadDim * 2; strides[1] = 16ull * kHeadDim * 2; strides[2] = 16ull * hkv * kHeadDim * 2;
+            box[0] = 64; box[1] = 16; box[2] = 1; box[3] = 1;
+        } else {
+            dims[0] = kHeadDim; dims[1] = hkv; dims[2] = 16; dims[3] = num_pages;
+            strides[0] = kHeadDim * 2; strides[1] = static_cast<cuuint64_t>(hkv) * kHeadDim * 2;
+            strides[2] = 16ull * hkv * kHeadDim * 2;
+            box[0] = 64; box[1] = 1; box[2] = 16; box[3] = 1;
+        }
+        for (int which = 0; which < 2; ++which) {
+            CUresult r = enc(which == 0 ? &m->k : &m->v, dt, 4, const_cast<void*>(which == 0 ? k_pool : v_pool),
+                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                set_last_error("cuTensorMapEncodeTiled(kv) failed: " + std::to_string(static_cast<int>(r)));
+                return POD_ERR_CUDA;
+            }
+        }
+    }
+    if (plan->batch.has_prefill) {
+        cuuint64_t dims[3] = {kHeadDim, static_cast<cuuint64_t>(hq),
+                              static_cast<cuuint64_t>(plan->batch.prefill.chunk_size)};
+        cuuint64_t strides[2] = {kHeadDim * 2, static_cast<cuuint64_t>(hq) * kHeadDim * 2};
+        cuuint32_t box[3] = {64, static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(kMBlock / G)};
+        CUresult r = enc(&m->q, dt, 3, const_cast<void*>(q_prefill), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_last_error("cuTensorMapEncodeTiled(q) failed: " + std::to_string(static_cast<int>(r)));
+            return POD_ERR_CUDA;
+        }
+    }
+    return POD_OK;
+}
+
+RunParams make_params(const pod_plan* plan, const void* q_decode, const void* k_pool, const void* v_pool,
+                      int64_t num_pages, const int32_t* indptr, const int32_t* indices, float* o_prefill,
+                      float* lse_prefill, float* o_decode, float* lse_decode, void* workspace) {
+    RunParams p{};
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    p.q_decode = q_decode;
+    p.k_pool = k_pool;
+    p.v_pool = v_pool;
+    p.page_indptr = indptr;
+    p.page_indices = indices;
+    p.o_prefill = o_prefill;
+    p.lse_prefill = lse_prefill;
+    p.o_decode = o_decode;
+    p.lse_decode = lse_decode;
+    p.ppart_o = reinterpret_cast<float*>(ws + plan->ws.off_ppart_o);
+    p.ppart_lse = reinterpret_cast<float*>(ws + plan->ws.off_ppart_lse);
+    p.dpart_o = reinterpret_cast<float*>(ws + plan->ws.off_dpart_o);
+    p.dpart_lse = reinterpret_cast<float*>(ws + plan->ws.off_dpart_lse);
+    p.pctas = reinterpret_cast<const PrefillCta*>(ws + plan->ws.off_pctas);
+    p.dctas = reinterpret_cast<const DecodeCta*>(ws + plan->ws.off_dctas);
+    p.ctr = reinterpret_cast<SchedCounters*>(ws + plan->ws.off_counters);
+    p.role_log = plan->role_log;
+    p.num_pctas = static_cast<int32_t>(plan->pctas.size());
+    p.num_dctas = static_cast<int32_t>(plan->dctas.size());
+    p.prefill_ratio = static_cast<int32_t>(plan->prefill_ratio);
+    p.decode_ratio = static_cast<int32_t>(plan->decode_ratio);
+    p.hq = plan->shape.num_q_heads;
+    p.hkv = plan->shape.num_kv_heads;
+    p.group = p.hq / p.hkv;
+    p.chunk = plan->batch.has_prefill ? static_cast<int32_t>(plan->batch.prefill.chunk_size) : 0;
+    p.offset = plan->batch.has_prefill ? static_cast<int32_t>(plan->batch.prefill.position_offset) : 0;
+    p.kv_layout = plan->batch.kv_layout;
+    p.decode_splits = static_cast<int32_t>(plan->decode_splits);
+    p.num_pages = num_pages;
+    p.sl2 = static_cast<float>(1.4426950408889634 / plan->shape.scale);
+    return p;
+}
+
+pod_status check_supported(const pod_plan* plan) {
+    if (plan->shape.head_dim != kHeadDim) {
+        set_last_error("only head_dim 128 is compiled for sm_100a");
+        return POD_ERR_UNSUPPORTED;
+    }
+    const int G = plan->shape.num_q_heads / plan->shape.num_kv_heads;
+    if (G != 1 && G != 2 && G != 4 && G != 8) {
+        set_last_error("GQA group must be 1, 2, 4 or 8");
+        return POD_ERR_UNSUPPORTED;
+    }
+    if (plan->batch.page_size != 16) {
+        set_last_error("only page_size 16 is compiled");
+        return POD_ERR_UNSUPPORTED;
+    }
+    return POD_OK;
+}
+
+template <int G, int kFmt>
+pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const Maps& maps, cudaStream_t s) {
+    // mode 0 fused, 1 serial, 2 prefill only, 3 decode only
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(pod_fused_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(pod_prefill_kernel<kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        attr_done = true;
+    }
+    const int P = p.num_pctas, D = p.num_dctas;
+    const size_t dec_smem = static_cast<size_t>(kDecodeWarps) * G * (kHeadDim + 4) * sizeof(float);
+    if (mode == 0) {
+        if (P + D > 0)
+            pod_fused_kernel<G, kFmt><<<P + D, kThreads, kSmemBytes, s>>>(p, maps.q, maps.k, maps.v);
+    } else {
+        if ((mode == 1 || mode == 2) && P > 0)
+            pod_prefill_kernel<kFmt><<<P, kThreads, kSmemBytes, s>>>(p, maps.q, maps.k, maps.v);
+        if ((mode == 1 || mode == 3) && D > 0)
+            pod_decode_kernel<G, kFmt><<<D, kDecodeWarps * 32, dec_smem, s>>>(p);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "pod kernel launch");
+    // split merges
+    const bool do_p = (mode != 3) && plan->merge_rows_prefill > 0;
+    const bool do_d = (mode != 2) && plan->merge_rows_decode > 0;
+    const uint8_t* ws = reinterpret_cast<const uint8_t*>(p.ctr);
+    const int32_t* tile_splits = reinterpret_cast<const int32_t*>(ws - plan->ws.off_counters + plan->ws.off_tile_splits);
+    if (do_p) {
+        const int rows = p.chunk * p.hq;
+        merge_kernel<<<(rows + 7) / 8, 256, 0, s>>>(p, tile_splits, static_cast<int>(plan->cfg.prefill_tile_q), 0, rows);
+    }
+    if (do_d) {
+        const int rows = static_cast<int>(plan->decode_ctx.size()) * p.hq;
+        merge_kernel<<<(rows + 7) / 8, 256, 0, s>>>(p, tile_splits, 1, 1, rows);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "pod merge launch");
+    return POD_OK;
+}
+
+template <int kFmt>
+pod_status dispatch_g(const pod_plan* plan, int mode, const RunParams& p, const Maps& maps, cudaStream_t s) {
+    switch (p.group) {
+        case 1: return launch_all<1, kFmt>(plan, mode, p, maps, s);
+        case 2: return launch_all<2, kFmt>(plan, mode, p, maps, s);
+        case 4: return launch_all<4, kFmt>(plan, mode, p, maps, s);
+        case 8: return launch_all<8, kFmt>(plan, mode, p, maps, s);
+    }
+    return POD_ERR_UNSUPPORTED;
+}
+
+pod_status run_mode(const pod_plan* plan, int mode, const void* q_prefill, const void* q_decode,
+                    const void* k_pool, const void* v_pool, int64_t num_pages, const int32_t* indptr,
+                    const int32_t* indices, float* o_prefill, float* lse_prefill, float* o_decode,
+                    float* lse_decode, void* workspace, void* stream) {
+    if (!plan || !k_pool || !v_pool || !indptr || !indices || !workspace) return POD_ERR_INVALID_ARGUMENT;
+    pod_status st = check_supported(plan);
+    if (st != POD_OK) return st;
+    const bool need_p = plan->batch.has_prefill && mode != 3;
+    const bool need_d = !plan->decode_ctx.empty() && mode != 2;
+    if (need_p && (!q_prefill || !o_prefill || !lse_prefill)) return POD_ERR_INVALID_ARGUMENT;
+    if (need_d && (!q_decode || !o_decode || !lse_decode)) return POD_ERR_INVALID_ARGUMENT;
+    Maps maps;
+    st = make_maps(plan, q_prefill, k_pool, v_pool, num_pages, &maps);
+    if (st != POD_OK) return st;
+    RunParams p = make_params(plan, q_decode, k_pool, v_pool, num_pages, indptr, indices, o_prefill,
+                              lse_prefill, o_decode, lse_decode, workspace);
+    if (mode == 2) p.num_dctas = 0;
+    if (mode == 3) p.num_pctas = 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (plan->batch.dtype == POD_DTYPE_FP16) return dispatch_g<0>(plan, mode, p, maps, s);
+    return dispatch_g<1>(plan, mode, p, maps, s);
+}
+
+}  // namespace pod
+
+using namespace pod;
+
+extern "C" {
+
+pod_status pod_device_query(int device, pod_device* out) {
+    if (!out) return POD_ERR_INVALID_ARGUMENT;
+    int sms = 0, smem = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    e = cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    // B200 calibration: 1 compute unit = one (row, key)
+    // pair at d = 128 = 4*128 FLOP; 1 memory unit = one bf16 element; 1 time unit = 1 us.
+    const double tf = 1665.7e12, hbm = 6538.9e9;
+    out->num_sms = sms;
+    out->compute_rate_per_sm = tf / (4.0 * kHeadDim) / 1e6 / sms;
+    out->mem_bandwidth_total = hbm / 2.0 / 1e6;
+    out->mem_bandwidth_per_sm = 1.2 * out->mem_bandwidth_total / sms;
+    out->mem_interference = 0.25;
+    out->max_ctas_per_sm = 4;
+    out->shared_mem_per_sm = smem;
+    return POD_OK;
+}
+
+pod_status pod_attn_workspace_init(const pod_plan* plan, void* workspace, void* stream) {
+    if (!plan || !workspace) return POD_ERR_INVALID_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    cudaError_t e = cudaMemsetAsync(ws + plan->ws.off_counters, 0, sizeof(SchedCounters), s);
+    if (e == cudaSuccess && !plan->pctas.empty())
+        e = cudaMemcpyAsync(ws + plan->ws.off_pctas, plan->pctas.data(), plan->pctas.size() * sizeof(PrefillCta),
+                            cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && !plan->dctas.empty())
+        e = cudaMemcpyAsync(ws + plan->ws.off_dctas, plan->dctas.data(), plan->dctas.size() * sizeof(DecodeCta),
+                            cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && !plan->tile_splits.empty())
+        e = cudaMemcpyAsync(ws + plan->ws.off_tile_splits, plan->tile_splits.data(),
+                            plan->tile_splits.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "pod_attn_workspace_init");
+    return POD_OK;
+}
+
+pod_status pod_attn_run(const pod_plan* plan, const void* q_prefill, const void* q_decode, const void* k_pool,
+                        const void* v_pool, int64_t num_pages, const int32_t* page_indptr,
+                        const int32_t* page_indices, float* o_prefill, float* lse_prefill, float* o_decode,
+                        float* lse_decode, void* workspace, void* stream) {
+    return run_mode(plan, 0, q_prefill, q_decode, k_pool, v_pool, num_pages, page_indptr, page_indices, o_prefill,
+                    lse_prefill, o_decode, lse_decode, workspace, stream);
+}
+
+pod_status pod_attn_run_serial(const pod_plan* plan, const void* q_prefill, const void* q_decode,
+                               const void* k_pool, const void* v_pool, int64_t num_pages,
+                               const int32_t* page_indptr, const int32_t* page_indices, float* o_prefill,
+                               float* lse_prefill, float* o_decode, float* lse_decode, void* workspace,
+                               void* stream) {
+    return run_mode(plan, 1, q_prefill, q_decode, k_pool, v_pool, num_pages, page_indptr, page_indices, o_prefill,
+                    lse_prefill, o_decode, lse_decode, workspace, stream);
+}
+
+pod_status pod_attn_run_part(const pod_plan* plan, int which, const void* q_prefill, const void* q_decode,
+                             const void* k_pool, const void* v_pool, int64_t num_pages,
+                             const int32_t* page_indptr, const int32_t* page_indices, float* o_prefill,
+                             float* lse_prefill, float* o_decode, float* lse_decode, void* workspace,
+                             void* stream) {
+    if (which != 0 && which != 1) return POD_ERR_INVALID_ARGUMENT;
+    return run_mode(plan, which == 0 ? 2 : 3, q_prefill, q_decode, k_pool, v_pool, num_pages, page_indptr,
+                    page_indices, o_prefill, lse_prefill, o_decode, lse_decode, workspace, stream);
+}
+
+pod_status pod_attn_gather_probe(const pod_plan* plan, const void* kv_pool, int64_t num_pages,
+                                 const int32_t* page_indptr, const int32_t* page_indices, int32_t req,
+                                 int64_t ctx, uint16_t* out, void* stream) {
+    (void)num_pages;
+    if (!plan || !kv_pool || !page_indptr || !page_indices || !out || ctx < 1) return POD_ERR_INVALID_ARGUMENT;
+    if (plan->shape.head_dim != kHeadDim || plan->batch.page_size != 16) return POD_ERR_UNSUPPORTED;
+    gather_probe_kernel<<<148, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint16_t*>(kv_pool), plan->batch.kv_layout, plan->shape.num_kv_heads, page_indptr,
+        page_indices, req, static_cast<int>(ctx), out);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "gather_probe");
+    return POD_OK;
+}
+
+const char* pod_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+"""Shared checking helpers: run the CPU oracle (oracle/pyoracle.py, test
+infrastructure) on the same bf16 inputs the GPU receives and compare."""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+from typing import Dict, Iterable, Optional
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+from oracle import pyoracle as O  # noqa: E402
+
+# North-star tolerance: fp32 accumulate, bf16 inputs -> max abs error <= 2e-3
+# relative to the output scale (max |O_ref| of the compared block); LSE is a
+# natural log, compared absolutely.
+O_TOL = 2e-3
+LSE_TOL = 2e-3
+
+
+def oracle_prefill(wl, kv_heads: Optional[Iterable[int]] = None, row_range=None) -> Dict[int, tuple]:
+    """Per kv head h: (O [rows][G][d], lse [rows][G]) from the oracle port of
+    tiled_prefill_attention (attention.hpp:148-222) on a one-KV-head restriction
+    (GQA consistency, test_attention.cpp:252-270)."""
+    s = wl.batch.shape
+    G = s.group_size()
+    off = wl.batch.prefill.position_offset
+    q = wl.prefill_q().numpy()
+    r0, r1 = row_range if row_range else (0, q.shape[0])
+    out = {}
+    for h in (kv_heads if kv_heads is not None else range(s.num_kv_heads)):
+        ctx = off + r1
+        k = wl.request_cache(0, "k", head=h)[:ctx].numpy().reshape(ctx, 1, s.head_dim)
+        v = wl.request_cache(0, "v", head=h)[:ctx].numpy().reshape(ctx, 1, s.head_dim)
+        qh = np.ascontiguousarray(q[r0:r1, h * G:(h + 1) * G, :])
+        o = O.tiled_prefill(qh, k, v, off + r0, G, 1, s.scale, 64, 64)
+        lse = O.prefill_lse(qh, k, off + r0, G, 1, s.scale)
+        out[h] = (o, lse)
+    return out
+
+
+def oracle_decode(wl, requests: Optional[Iterable[int]] = None, kv_heads=None) -> Dict[tuple, tuple]:
+    """(request, kv head) -> (O [G][d], lse [G]) from decode_attention (attention.hpp:328-333)."""
+    s = wl.batch.shape
+    G = s.group_size()
+    q = wl.decode_q().numpy()
+    base = 1 if wl.batch.prefill is not None else 0
+    out = {}
+    reqs = requests if requests is not None else range(len(wl.batch.decodes))
+    for r in reqs:
+        for h in (kv_heads if kv_heads is not None else range(s.num_kv_heads)):
+            ctx = wl.kv_lens[base + r]
+            k = wl.request_cache(base + r, "k", head=h).numpy().reshape(ctx, 1, s.head_dim)
+            v = wl.request_cache(base + r, "v", head=h).numpy().reshape(ctx, 1, s.head_dim)
+            o, lse = O.decode_attention(np.ascontiguousarray(q[r, h * G:(h + 1) * G]), k, v, G, 1, s.scale)
+            out[(r, h)] = (o, lse)
+    return out
+
+
+def rel_err(got: np.ndarray, ref: np.ndarray) -> float:
+    scale = max(float(np.abs(ref).max()), 1e-30)
+    return float(np.abs(got - ref).max()) / scale
+
+
+def compare_prefill(wl, o_gpu: np.ndarray, lse_gpu: np.ndarray, kv_heads=None, row_range=None):
+    """Returns (worst O rel err, worst |dLSE|)."""
+    G = wl.batch.shape.group_size()
+    ref = oracle_prefill(wl, kv_heads, row_range)
+    r0, r1 = row_range if row_range else (0, o_gpu.shape[0])
+    eo = el = 0.0
+    for h, (o, lse) in ref.items():
+        got = o_gpu[r0:r1, h * G:(h + 1) * G, :]
+        eo = max(eo, rel_err(got, o))
+        el = max(el, float(np.abs(lse_gpu[r0:r1, h * G:(h + 1) * G] - lse).max()))
+    return eo, el
+
+
+def compare_decode(wl, o_gpu: np.ndarray, lse_gpu: np.ndarray, requests=None, kv_heads=None):
+    G = wl.batch.shape.group_size()
+    ref = oracle_decode(wl, requests, kv_heads)
+    eo = el = 0.0
+    for (r, h), (o, lse) in ref.items():
+        eo = max(eo, rel_err(o_gpu[r, h * G:(h + 1) * G], o))
+        el = max(el, float(np.abs(lse_gpu[r, h * G:(h + 1) * G] - lse).max()))
+    return eo, el
