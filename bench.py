@@ -1,0 +1,427 @@
+#!/usr/bin/env python3
+"""Hybrid-batch attention bench (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_b64] [--impl pod|reference]
+
+A "step" is one hybrid-batch attention layer: the fused POD launch (SM-aware
+prefill + decode CTAs, then the split merge) over one synthetic Llama-3-8B
+batch resident in HBM.  At N > 1 (torchrun, one rank per GPU) the layer is
+sharded by KV-head group (TP = N, each rank owns Hkv/N whole KV heads) and the
+per-rank outputs are assembled with one NCCL all-gather inside the step.
+
+Rank 0 prints ONE JSON line.  `value` is the fused layer latency in us
+(lower is better, max over ranks); the line also carries serial / prefill-alone
+/ decode-alone latencies, the speedup over serial, the combined-roofline
+fraction, e2e through the C ABI with host buffers, the roofline object for the
+fused kernel and the CPU reference baseline (oracle/_ref, test infrastructure,
+timed on a bounded sample on this host's cores).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "hybrid-batch attention µs/layer, speedup vs serial, % of combined roofline"
+
+# name -> (Hq, Hkv, chunk, offset, decode batch, decode ctx)
+CONFIGS = {
+    "c1": (32, 8, 512, 1536, 8, 2048),
+    "c2_b8": (32, 8, 1024, 15360, 8, 16384),
+    "c2_b16": (32, 8, 1024, 15360, 16, 16384),
+    "c2_b32": (32, 8, 1024, 15360, 32, 16384),
+    "c2_b64": (32, 8, 1024, 15360, 64, 16384),
+    "c4": (32, 32, 2048, 2048, 128, 4096),
+}
+DEFAULT_CONFIG = "c2_b64"
+
+
+def peaks():
+    p = {"hbm_gbs": 6538.9, "bf16_tflops": 1665.7, "bf16_tflops_sustained": 1381.4, "source": "measured"}
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        j = json.loads(f.read_text())
+        for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained"):
+            if k in j:
+                p[k] = float(j[k])
+    else:
+        p.update(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0, source="fallback")
+    return p
+
+
+def work(hq, hkv, chunk, off, b, ctx, d=128):
+    """Algorithmic work of one layer: prefill FLOPs (QK^T + PV,
+    causal, masked work excluded) and decode bytes (bf16 K+V + Q + fp32 O + LSE)."""
+    flops = 4.0 * d * hq * (chunk * off + chunk * (chunk + 1) / 2.0)
+    dbytes = b * (2.0 * ctx * hkv * d * 2) + b * hq * d * 2 + b * hq * d * 4 + b * hq * 4
+    return flops, dbytes
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        sms.sort()
+        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ----------------------------------------------------------- CPU baseline --
+def cpu_reference_sample(hq, hkv, chunk, off, b, ctx, target_s=12.0, threads=None, seed=7):
+    """Times the reference's own tiled_prefill_attention / decode_attention
+    (oracle/_ref, built from /root/reference) on a bounded, representative sample
+    of the layer and extrapolates linearly in (q-head row, key) pairs.
+    Returns (us_per_layer, threads, sample_description)."""
+    import numpy as np
+
+    from oracle import pyoracle as O
+
+    if not O.ref_available():
+        raise RuntimeError("oracle/_ref missing")
+    threads = threads or os.cpu_count() or 1
+    d = 128
+    G = hq // hkv
+    scale = math.sqrt(d)
+    rng = np.random.default_rng(seed)
+    # full-layer pairs
+    pf_pairs = hkv * G * (chunk * off + chunk * (chunk + 1) / 2.0)
+    dec_pairs = b * hkv * G * float(ctx)
+    total_pairs = pf_pairs + dec_pairs
+    # calibrate throughput with one small shard
+    kcal = rng.uniform(-1, 1, (4096, 1, d)).round(3)
+    qcal = rng.uniform(-1, 1, (G, d))
+    out = np.zeros((G, d))
+    t = O.run_shards([dict(kind=1, group=G, rows=1, offset=0, q=qcal, k=kcal, v=kcal, out=out)], d, scale, 64, 64, 1)
+    rate1 = G * 4096 / max(t, 1e-6)  # pairs/s on one core
+    budget_pairs = target_s * rate1 * 0.5  # ~target_s core-seconds
+    # sample: prefill row blocks spread over the chunk + decode shards, in proportion
+    n_shards = max(2 * threads, 8)
+    pf_share = pf_pairs / total_pairs
+    shards = []
+    keep = []
+    pf_budget = budget_pairs * pf_share
+    dec_budget = budget_pairs - pf_budget
+    sample_pairs = 0.0
+    npf = n_shards if chunk > 0 else 0
+    if npf:
+        rows_per = max(1, int(pf_budget / npf / (G * (off + chunk / 2.0))))
+        rows_per = min(rows_per, chunk)
+        for i in range(npf):
+            r0 = int((chunk - rows_per) * i / max(1, npf - 1))
+            kv = off + r0 + rows_per
+            k = rng.uniform(-1, 1, (kv, 1, d))
+            v = rng.uniform(-1, 1, (kv, 1, d))
+            q = rng.uniform(-1, 1, (rows_per, G, d))
+            o = np.zeros((rows_per, G * d))
+            shards.append(dict(kind=0, group=G, rows=rows_per, offset=off + r0, q=q, k=k, v=v, out=o))
+            keep += [k, v, q, o]
+            sample_pairs += G * sum(off + r0 + r + 1 for r in range(rows_per))
+    ndec = n_shards if b > 0 else 0
+    if ndec:
+        dctx = int(min(ctx, max(16, dec_budget / ndec / G)))
+        for i in range(ndec):
+            k = rng.uniform(-1, 1, (dctx, 1, d))
+            v = rng.uniform(-1, 1, (dctx, 1, d))
+            q = rng.uniform(-1, 1, (G, d))
+            o = np.zeros((G, d))
+            shards.append(dict(kind=1, group=G, rows=1, offset=0, q=q, k=k, v=v, out=o))
+            keep += [k, v, q, o]
+        dec_scale = ctx / dctx
+    else:
+        dctx, dec_scale = 0, 1.0
+    # time prefill and decode shards separately so each extrapolates by its own work
+    pf = [s for s in shards if s["kind"] == 0]
+    dc = [s for s in shards if s["kind"] == 1]
+    t_pf = O.run_shards(pf, d, scale, 64, 64, threads) if pf else 0.0
+    t_dc = O.run_shards(dc, d, scale, 64, 64, threads) if dc else 0.0
+    pf_sample_pairs = sample_pairs
+    dc_sample_pairs = len(dc) * G * dctx
+    us = 0.0
+    if pf:
+        us += t_pf * (pf_pairs / pf_sample_pairs) * 1e6
+    if dc:
+        us += t_dc * (dec_pairs / dc_sample_pairs) * 1e6
+    desc = (f"{len(pf)} prefill row-blocks x {pf[0]['rows'] if pf else 0} rows (1 KV head, {G} q heads) + "
+            f"{len(dc)} decode (request, KV head) shards at {dctx} keys; {t_pf + t_dc:.1f} s wall on {threads} "
+            f"threads; extrapolated linearly in (q-head row, key) pairs to the full layer")
+    return us, threads, desc, t_pf + t_dc
+
+
+# --------------------------------------------------------------- GPU arm ---
+def run_pod(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_18038_b200 as pkg
+    from paper_2410_18038_b200.hybrid import PodAttention
+    from paper_2410_18038_b200.workload import build_workload, make_batch
+
+    hq, hkv, chunk, off, b, ctx = CONFIGS[args.config]
+    if hkv % world:
+        raise SystemExit(f"Hkv={hkv} not divisible by {world} GPUs")
+    hq_r, hkv_r = hq // world, hkv // world
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    shape = pkg.ModelShape(hq_r, hkv_r, 128, math.sqrt(128))
+    batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
+    wl = build_workload(batch, device=dev, seed_q=42 + 1000 * rank, seed_kv=43 + 1000 * rank)
+    opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode)
+    op = PodAttention(batch, options=opts, device=local_rank)
+    out = op.alloc_outputs()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    tokens = chunk + b
+    gather_buf = None
+    if world > 1:
+        gather_buf = torch.empty(world * tokens * hq_r * 128, dtype=torch.float32, device=dev)
+
+    def step(mode):
+        op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=out, mode=mode)
+        if world > 1:
+            local = torch.cat([out.o_prefill.reshape(-1), out.o_decode.reshape(-1)])
+            dist.all_gather_into_tensor(gather_buf, local)
+
+    def timed(mode, steps, warmup):
+        for _ in range(warmup):
+            step(mode)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for i in range(steps):
+            flush.zero_()  # L2 flush (512 MB > 126 MB L2), outside the timed events
+            ev[i][0].record()
+            step(mode)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        ms = [a.elapsed_time(e) for a, e in ev]
+        t = sum(ms) / len(ms)
+        if world > 1:
+            x = torch.tensor([t], device=dev)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            dist.barrier()
+            t = float(x.item())
+        return t, ms
+
+    sampler = ClockSampler(local_rank)
+    with sampler:
+        t_fused, ms_fused = timed("fused", args.steps, args.warmup)
+    clocks = sampler.summary()
+    t_serial, _ = timed("serial", args.steps, args.warmup)
+    t_pf, _ = timed("prefill", args.steps, args.warmup) if chunk else (0.0, [])
+    t_dec, _ = timed("decode", args.steps, args.warmup) if b else (0.0, [])
+
+    # e2e through the C ABI with HOST buffers (pinned): H2D of the step's queries, the
+    # fused launch, D2H of the outputs (O + LSE).  The paged KV cache is device-resident state.
+    qp_h = wl.q_prefill.cpu().pin_memory() if chunk else None
+    qd_h = wl.q_decode.cpu().pin_memory() if b else None
+    host_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in
+                (out.o_prefill, out.lse_prefill, out.o_decode, out.lse_decode) if t is not None]
+    dev_out = [t for t in (out.o_prefill, out.lse_prefill, out.o_decode, out.lse_decode) if t is not None]
+    h2d = (qp_h.numel() * 2 if qp_h is not None else 0) + (qd_h.numel() * 2 if qd_h is not None else 0)
+    d2h = sum(t.numel() * 4 for t in dev_out)
+
+    def e2e_step():
+        if qp_h is not None:
+            wl.q_prefill.copy_(qp_h, non_blocking=True)
+        if qd_h is not None:
+            wl.q_decode.copy_(qd_h, non_blocking=True)
+        step("fused")
+        for hsrc, dsrc in zip(host_out, dev_out):
+            hsrc.copy_(dsrc, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    t1.record()
+    torch.cuda.synchronize()
+    t_e2e = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        x = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        t_e2e = float(x.item())
+
+    info = op.info
+    launches_per_step = 1 + (1 if info.num_merge_rows_prefill > 0 else 0) + (1 if info.num_merge_rows_decode > 0 else 0)
+    res = dict(t_fused=t_fused, ms_fused=ms_fused, t_serial=t_serial, t_pf=t_pf, t_dec=t_dec, t_e2e=t_e2e,
+               clocks=clocks, info=info, launches=launches_per_step, h2d=h2d, d2h=d2h, hq_r=hq_r, hkv_r=hkv_r)
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="pod", choices=["pod", "reference"])
+    ap.add_argument("--policy", type=int, default=0)
+    ap.add_argument("--tile-mode", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    hq, hkv, chunk, off, b, ctx = CONFIGS[args.config]
+    flops, dbytes = work(hq, hkv, chunk, off, b, ctx)
+    pk = peaks()
+    config = {"workload": f"{args.config}: Llama-3-8B-shaped layer ({hq} Q / {hkv} KV heads, d=128, bf16), "
+                          f"prefill chunk {chunk} at offset {off} (context {off + chunk}) + {b} decodes at "
+                          f"context {ctx}, paged KV (page 16, HND, random block tables)",
+              "tp": args.gpus, "parallelism": f"kv-head-group tp{args.gpus}", "l2": "flushed between steps "
+              "(512 MB write); KV working set also exceeds L2", "page_size": 16}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps = max(1, args.steps)
+        vals = []
+        t_wall = 0.0
+        for i in range(args.warmup + steps):
+            us, thr, desc, wall = cpu_reference_sample(hq, hkv, chunk, off, b, ctx,
+                                                       target_s=min(args.cpu_seconds, 6.0), seed=7 + i)
+            if i >= args.warmup:
+                vals.append(us)
+                t_wall += wall
+        v = sum(vals) / len(vals)
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "us/layer", "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": round(v / 1000.0, 3), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform[-1,1))",
+            "config": config,
+            "cpu_baseline": {"value": round(v, 1), "unit": "us/layer", "cores": thr, "kind": "reference",
+                             "sample": desc},
+            "e2e": {"value": round(v, 1), "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    r = run_pod(args, rank, world, local_rank)
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # per-rank roofline (each rank owns 1/world of the heads)
+    flops_r, dbytes_r = flops / world, dbytes / world
+    t_pf_roof = flops_r / (pk["bf16_tflops"] * 1e12) * 1e6
+    t_dec_roof = dbytes_r / (pk["hbm_gbs"] * 1e9) * 1e6
+    roof_us = max(t_pf_roof, t_dec_roof)
+    us = r["t_fused"] * 1000.0
+    bound = "hbm" if t_dec_roof >= t_pf_roof else "tensor"
+    if bound == "hbm":
+        achieved = dbytes_r / (us * 1e-6) / 1e9
+        peak, unit = pk["hbm_gbs"], "GB/s"
+    else:
+        achieved = flops_r / (us * 1e-6) / 1e12
+        peak, unit = pk["bf16_tflops"], "TFLOP/s"
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cus, thr, desc, _ = cpu_reference_sample(hq, hkv, chunk, off, b, ctx, target_s=args.cpu_seconds)
+            cpu = {"value": round(cus, 1), "unit": "us/layer", "cores": thr, "kind": "reference", "sample": desc}
+        except Exception as e:  # reported, never fatal for the GPU number
+            cpu = {"value": None, "unit": "us/layer", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    info = r["info"]
+    line = {
+        "metric": METRIC, "value": round(us, 2), "unit": "us/layer", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(r["t_fused"], 4), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (splitmix64 uniform[-1,1) -> bf16)",
+        "config": config,
+        "serial_us": round(r["t_serial"] * 1000, 2),
+        "speedup_vs_serial": round(r["t_serial"] / r["t_fused"], 3),
+        "prefill_alone_us": round(r["t_pf"] * 1000, 2), "decode_alone_us": round(r["t_dec"] * 1000, 2),
+        "fused_vs_max_alone": round(r["t_fused"] / max(r["t_pf"], r["t_dec"], 1e-9), 3),
+        "combined_roofline_us": round(roof_us, 2), "combined_roofline_frac": round(roof_us / us, 4),
+        "prefill_tensor_frac_alone": round(t_pf_roof / max(r["t_pf"] * 1000, 1e-9), 4) if chunk else None,
+        "decode_hbm_frac_alone": round(t_dec_roof / max(r["t_dec"] * 1000, 1e-9), 4) if b else None,
+        "tokens_per_s": round((chunk + b) / (us * 1e-6), 1),
+        "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
+                 "prefill_splits": info.prefill_splits, "decode_splits": info.decode_splits,
+                 "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
+                 "policy": args.policy},
+        "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": "pod_fused_kernel (+merge)", "peak_source": pk["source"]},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(r["t_e2e"] * 1000, 2), "unit": "us/layer", "h2d_bytes_per_step": r["h2d"],
+                "d2h_bytes_per_step": r["d2h"]},
+        "gpu_launches": r["launches"] * args.steps,
+        "clocks": r["clocks"],
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -116,7 +116,9 @@ typedef struct pod_task {
 enum {
     POD_POLICY_FIFTY_FIFTY = 0,  /* SmPolicy::FiftyFifty (gpu_sim.hpp:97-99)          */
     POD_POLICY_PROPORTIONAL = 1, /* SmPolicy::Proportional, gcd of PHYSICAL CTAs (:100-105) */
-    POD_POLICY_CLAMPED = 2       /* proportional, rounded to the per-SM slot count     */
+    POD_POLICY_CLAMPED = 2,      /* proportional, rounded to the per-SM slot count     */
+    POD_POLICY_COMPLEMENT = 3    /* bind from the roles resident on the SM:
+                                    prefill while < prefill_ratio prefill CTAs run there */
 };
 
 enum {
@@ -128,7 +130,7 @@ typedef struct pod_options {
     int32_t policy;          /* POD_POLICY_*                                        */
     int32_t tile_mode;       /* POD_TILE_*                                          */
     int32_t ctas_per_sm;     /* 0 = from tile selection; else 2 or 4 (make_tile_config) */
-    int32_t virtual_decode;  /* -1 = on (fused kernel), 0 = off, 1 = on             */
+    int32_t virtual_decode;  /* -1 = keep the tile config's flag, 0 = off, 1 = on    */
     int32_t split_wave_cap;  /* 0 = keep the tile config's value (2)                */
     int32_t decode_splits;   /* 0 = auto (fill the machine), else splits per (request, kv head) */
     const pod_tile_config* tile_override; /* non-NULL: use this TileConfig verbatim */
@@ -222,6 +224,10 @@ pod_status pod_attn_set_role_log(pod_plan* plan, int32_t* device_log);
 pod_status pod_attn_gather_probe(const pod_plan* plan, const void* kv_pool, int64_t num_pages,
                                  const int32_t* page_indptr, const int32_t* page_indices,
                                  int32_t req, int64_t ctx, uint16_t* out, void* stream);
+
+/* Resident CTAs per SM the driver allows for the fused / prefill-only /
+ * decode-only kernels of this plan's instantiation (cudaOccupancyMaxActiveBlocksPerMultiprocessor). */
+pod_status pod_attn_occupancy(const pod_plan* plan, int32_t* fused, int32_t* prefill, int32_t* decode);
 
 const char* pod_status_string(pod_status s);
 /* Last CUDA error string seen by this thread's most recent failing call. */

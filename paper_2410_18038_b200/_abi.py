@@ -19,7 +19,7 @@ STATUS_NAMES = {
 
 POD_KV_HND, POD_KV_NHD = 0, 1
 POD_DTYPE_BF16, POD_DTYPE_FP16 = 0, 1
-POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED = 0, 1, 2
+POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT = 0, 1, 2, 3
 POD_TILE_REFERENCE, POD_TILE_B200 = 0, 1
 
 
@@ -99,6 +99,7 @@ SYMBOLS = [
                                     _vp, _vp]),
     ("pod_attn_set_role_log", C.c_int, [_vp, _vp]),
     ("pod_attn_gather_probe", C.c_int, [_vp, _vp, C.c_int64, _vp, _vp, C.c_int32, C.c_int64, _vp, _vp]),
+    ("pod_attn_occupancy", C.c_int, [_vp, _i32p, _i32p, _i32p]),
     ("pod_status_string", C.c_char_p, [C.c_int]),
     ("pod_last_error", C.c_char_p, []),
     ("pod_attn_abi_version", C.c_int, []),

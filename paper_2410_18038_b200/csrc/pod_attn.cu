@@ -18,8 +18,10 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -41,11 +43,12 @@ constexpr uint32_t kKvStageBytes = kKvTile * kHeadDim * 2;  // 16 KB
 constexpr uint32_t kOffQ = 0;
 constexpr uint32_t kOffK = kOffQ + kQBytes;                 // 2 stages
 constexpr uint32_t kOffV = kOffK + 2 * kKvStageBytes;       // 2 stages
-constexpr uint32_t kOffP = kOffV + 2 * kKvStageBytes;       // 128 x 64 bf16 = 16 KB
-constexpr uint32_t kOffBar = kOffP + kMBlock * kKvTile * 2;
+constexpr uint32_t kOffBar = kOffV + 2 * kKvStageBytes;     // 16 mbarriers
 constexpr uint32_t kOffTmemSlot = kOffBar + 128;
+constexpr uint32_t kOffDecBar = kOffBar + 160;              // 4 warps x 3 stages of decode mbarriers
 constexpr uint32_t kOffRole = kOffTmemSlot + 16;
-constexpr uint32_t kSmemBytes = kOffBar + 256;              // 114944 B -> 2 CTAs / SM
+constexpr uint32_t kSmemBytes = kOffBar + 256;              // 98560 B -> 2 CTAs / SM
+static_assert(kOffDecBar + 12 * 8 <= kSmemBytes, "decode barriers");
 static_assert(kSmemBytes * 2 + 2048 <= 233472, "two CTAs must fit one SM");
 constexpr uint32_t kTmemCols = 256;                         // S0 | S1 | O(128)
 constexpr uint32_t kTmemS0 = 0, kTmemO = 128;
@@ -82,10 +85,27 @@ struct RunParams {
     int32_t offset;
     int32_t kv_layout;
     int32_t decode_splits;
-    int32_t pad0;
+    int32_t policy;
     int64_t num_pages;
     float sl2;  // log2(e) / scale  (scale is the reference's divisor)
 };
+
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+          "l"(*reinterpret_cast<uint64_t*>(&c)));
+    return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+    return *reinterpret_cast<float2*>(&d);
+}
 
 // ============================================================ prefill ===
 template <int kFmt>
@@ -100,15 +120,16 @@ __device__ __forceinline__ void prefill_issue_qk(uint32_t tmem_s, uint32_t sQ, u
     }
 }
 
+// O (+)= P V with P (bf16, 128 x 64) read from TMEM (2 values per 32-bit column,
+// 8 columns per K=16 step) and V (64 keys x 128 d, MN-major SW128) from smem.
 template <int kFmt>
-__device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t sP, uint32_t sV,
+__device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint32_t sV,
                                                  bool accumulate) {
     constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);
 #pragma unroll
     for (int kk = 0; kk < kKvTile / 16; ++kk) {
-        const uint64_t a = ptx::sw128_desc(sP + kk * 32, 16, 1024);
         const uint64_t b = ptx::sw128_desc(sV + kk * 2048, kKvTile * 128, 1024);
-        ptx::umma_f16_ss(tmem_o, a, b, idesc, (accumulate || kk > 0) ? 1u : 0u);
+        ptx::umma_f16_ts(tmem_o, tmem_p + kk * 8, b, idesc, (accumulate || kk > 0) ? 1u : 0u);
     }
 }
 
@@ -151,51 +172,57 @@ __device__ __forceinline__ void prefill_load_kv_tile(const RunParams& p, const C
     }
 }
 
+// Prefill role: one CTA = one CtaTask of decompose_prefill (q tile x kv head x kv
+// split), processed as M-blocks of 128 packed (row, q-head) rows.  Warp roles:
+//   warps 0-3  softmax: TMEM lane quadrant w, one M row per thread
+//   warp 4     TMA producer (Q, K and V boxes through the page table)
+//   warp 5     MMA issuer (one thread): S = Q K^T (SS), O += P V (TS, P in TMEM)
+// S tiles are double-buffered in TMEM; each softmax thread overwrites its S row
+// with its bf16 P row, so P is double-buffered for free and never touches smem.
+// All hand-offs are mbarriers (no CTA-wide barrier inside the KV loop).
+// Pipeline counters that persist across the work items a resident CTA runs:
+// mbarrier phases continue from item to item, so barriers are initialised once.
+struct PrefillState {
+    int g = 0;   // KV tiles issued so far (stage = g & 1, phase = (g >> 1) & 1)
+    int qb = 0;  // Q blocks loaded so far
+};
+
 template <int kFmt>
-__device__ void prefill_cta(const RunParams& p, const CUtensorMap* tmq, const CUtensorMap* tmk,
-                            const CUtensorMap* tmv, int cta_id, uint8_t* smem) {
+__device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const CUtensorMap* tmk,
+                             const CUtensorMap* tmv, int cta_id, uint8_t* smem, uint32_t tmem,
+                             PrefillState& ps) {
     const PrefillCta job = p.pctas[cta_id];
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const uint32_t sbase = ptx::smem_u32(smem);
-    const uint32_t sQ = sbase + kOffQ, sK = sbase + kOffK, sV = sbase + kOffV, sP = sbase + kOffP;
+    const uint32_t sQ = sbase + kOffQ, sK = sbase + kOffK, sV = sbase + kOffV;
     const uint32_t bar0 = sbase + kOffBar;
     const uint32_t b_qfull = bar0 + 0, b_qempty = bar0 + 8;
     const uint32_t b_kfull = bar0 + 16, b_kempty = bar0 + 32;  // [2] each, 8 B apart
     const uint32_t b_vfull = bar0 + 48, b_vempty = bar0 + 64;
     const uint32_t b_sfull = bar0 + 80;                        // [2]
-    const uint32_t b_pv = bar0 + 96;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
+    const uint32_t b_pfull = bar0 + 96;                        // [2], 4 arrivals (one per softmax warp)
+    const uint32_t b_pv = bar0 + 112;                          // [2]
 
     const int G = p.group;
     const int rpb = kMBlock / G;
     const int nblocks = (job.rows + rpb - 1) / rpb;
     const int pbeg = p.page_indptr[0];
     const int npages = p.page_indptr[1] - pbeg;
-
-    if (tid == 0) {
-        if (sbase & 1023u) __trap();  // SW128 atoms need a 1024-aligned base
-        for (int i = 0; i < 13; ++i) ptx::mbar_init(bar0 + 8 * i, 1);
-        ptx::fence_mbar_init();
+    // every thread advances the shared counters identically
+    int g0 = ps.g, qb0 = ps.qb;
+    for (int b = 0; b < nblocks; ++b) {
+        const int nt = prefill_block(p, job, b).nt;
+        if (nt > 0) {
+            ps.g += nt;
+            ps.qb += 1;
+        }
     }
-    if (warp == 0) {
-        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), kTmemCols);
-        ptx::tmem_relinquish();
-    }
-    if (warp == 4 && lane == 0) {
-        ptx::prefetch_tmap(tmq);
-        ptx::prefetch_tmap(tmk);
-        ptx::prefetch_tmap(tmv);
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
 
     if (warp == 4) {
         // ------------------------------------------------ TMA producer --
         if (lane == 0) {
-            int g = 0, qb = 0;
+            int g = g0, qb = qb0;
             for (int b = 0; b < nblocks; ++b) {
                 const BlockRange br = prefill_block(p, job, b);
                 if (br.nt == 0) continue;
@@ -223,11 +250,51 @@ __device__ void prefill_cta(const RunParams& p, const CUtensorMap* tmq, const CU
                 g += br.nt;
             }
         }
+    } else if (warp == 5) {
+        // -------------------------------------------------- MMA issuer --
+        if (lane == 0) {
+            int g = g0, qb = qb0;
+            for (int b = 0; b < nblocks; ++b) {
+                const BlockRange br = prefill_block(p, job, b);
+                if (br.nt == 0) continue;
+                ptx::mbar_wait(b_qfull, qb & 1);
+                for (int j = 0; j < 2 && j < br.nt; ++j) {
+                    const int gg = g + j, st = gg & 1;
+                    ptx::mbar_wait(b_kfull + 8 * st, (gg >> 1) & 1);
+                    ptx::tc_fence_after();
+                    prefill_issue_qk<kFmt>(tmem + kTmemS0 + st * kKvTile, sQ, sK + st * kKvStageBytes);
+                    ptx::umma_commit(b_sfull + 8 * st);
+                    ptx::umma_commit(b_kempty + 8 * st);
+                    if (j == br.nt - 1) ptx::umma_commit(b_qempty);
+                }
+                for (int t = 0; t < br.nt; ++t) {
+                    const int gg = g + t, st = gg & 1;
+                    ptx::mbar_wait(b_pfull + 8 * st, (gg >> 1) & 1);
+                    ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
+                    ptx::tc_fence_after();
+                    prefill_issue_pv<kFmt>(tmem + kTmemO, tmem + kTmemS0 + st * kKvTile, sV + st * kKvStageBytes,
+                                           t > 0);
+                    ptx::umma_commit(b_pv + 8 * st);
+                    ptx::umma_commit(b_vempty + 8 * st);
+                    if (t + 2 < br.nt) {
+                        const int g2 = gg + 2;
+                        ptx::mbar_wait(b_kfull + 8 * st, (g2 >> 1) & 1);
+                        ptx::tc_fence_after();
+                        prefill_issue_qk<kFmt>(tmem + kTmemS0 + st * kKvTile, sQ, sK + st * kKvStageBytes);
+                        ptx::umma_commit(b_sfull + 8 * st);
+                        ptx::umma_commit(b_kempty + 8 * st);
+                        if (t + 2 == br.nt - 1) ptx::umma_commit(b_qempty);
+                    }
+                }
+                g += br.nt;
+                ++qb;
+            }
+        }
     } else {
-        // ------------------------------ softmax / MMA-issue (128 threads) --
+        // ------------------------------------------ softmax (128 threads) --
         const int m = tid;  // TMEM lane == M row
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-        int g = 0, qb = 0;
+        int g = g0;
         for (int b = 0; b < nblocks; ++b) {
             const BlockRange br = prefill_block(p, job, b);
             const int my_r = br.r0 + m / G;
@@ -253,47 +320,30 @@ __device__ void prefill_cta(const RunParams& p, const CUtensorMap* tmq, const CU
                 }
                 continue;
             }
-            if (tid == 0) {
-                ptx::mbar_wait(b_qfull, qb & 1);
-                const int st = g & 1;
-                ptx::mbar_wait(b_kfull + 8 * st, (g >> 1) & 1);
-                ptx::tc_fence_after();
-                prefill_issue_qk<kFmt>(tmem + kTmemS0 + st * kKvTile, sQ, sK + st * kKvStageBytes);
-                ptx::umma_commit(b_sfull + 8 * st);
-                ptx::umma_commit(b_kempty + 8 * st);
-                if (br.nt == 1) ptx::umma_commit(b_qempty);
-            }
             float m_run = -INFINITY, l_run = 0.f;
             for (int t = 0; t < br.nt; ++t) {
                 const int gg = g + t, st = gg & 1;
-                if (tid == 0 && t + 1 < br.nt) {
-                    const int g1 = gg + 1, s1 = g1 & 1;
-                    ptx::mbar_wait(b_kfull + 8 * s1, (g1 >> 1) & 1);
-                    ptx::tc_fence_after();
-                    prefill_issue_qk<kFmt>(tmem + kTmemS0 + s1 * kKvTile, sQ, sK + s1 * kKvStageBytes);
-                    ptx::umma_commit(b_sfull + 8 * s1);
-                    ptx::umma_commit(b_kempty + 8 * s1);
-                    if (t + 2 == br.nt) ptx::umma_commit(b_qempty);
-                }
-                // S tile -> registers
+                const uint32_t s_addr = lane_base + kTmemS0 + st * kKvTile;
                 ptx::mbar_wait(b_sfull + 8 * st, (gg >> 1) & 1);
                 ptx::tc_fence_after();
                 float s[kKvTile];
-                ptx::tmem_ld32(lane_base + kTmemS0 + st * kKvTile, *reinterpret_cast<float(*)[32]>(&s[0]));
-                ptx::tmem_ld32(lane_base + kTmemS0 + st * kKvTile + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+                ptx::tmem_ld32(s_addr, *reinterpret_cast<float(*)[32]>(&s[0]));
+                ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
                 ptx::tmem_wait_ld();
                 const int kb = br.kt0 + t * kKvTile;
-                // valid keys: [lo, hi) within this tile for this row
+                // valid keys of this row inside the tile: [lo, hi)
                 const int lo = max(job.kv_begin - kb, 0);
                 const int hi = row_ok ? min(min(job.kv_end, vis + 1) - kb, kKvTile) : 0;
-                float tmax = -INFINITY;
+                // interior tiles (every row of the warp sees every key) skip masking
+                if (!__all_sync(0xffffffffu, lo == 0 && hi == kKvTile)) {
 #pragma unroll
-                for (int c = 0; c < kKvTile; ++c) {
-                    const bool ok = (c >= lo) && (c < hi);
-                    s[c] = ok ? s[c] * p.sl2 : -INFINITY;
-                    tmax = fmaxf(tmax, s[c]);
+                    for (int c = 0; c < kKvTile; ++c)
+                        if (c < lo || c >= hi) s[c] = -INFINITY;
                 }
-                const float m_new = fmaxf(m_run, tmax);
+                float tmax = s[0];
+#pragma unroll
+                for (int c = 1; c < kKvTile; c += 2) tmax = fmaxf(tmax, fmaxf(s[c], s[min(c + 1, kKvTile - 1)]));
+                const float m_new = fmaxf(m_run, tmax * p.sl2);
                 // lazy rescale (only when the max grows by > 2^8): exact algebra,
                 // the stale reference max bounds p by 256.
                 const bool need = m_new > m_run + 8.f;
@@ -301,30 +351,35 @@ __device__ void prefill_cta(const RunParams& p, const CUtensorMap* tmq, const CU
                 const float factor = need ? ptx::ex2(m_run - m_new) : 1.f;
                 l_run *= factor;
                 m_run = m_use;
-                uint32_t pk[kKvTile / 2];
-                float lsum = 0.f;
+                float pk[kKvTile / 2];  // packed 16-bit P pairs (bit patterns)
+                float2 lsum2 = make_float2(0.f, 0.f);
                 if (m_use == -INFINITY) {
 #pragma unroll
-                    for (int c = 0; c < kKvTile / 2; ++c) pk[c] = 0u;
+                    for (int c = 0; c < kKvTile / 2; ++c) pk[c] = 0.f;
                 } else {
+                    const float neg_m = -m_use;
 #pragma unroll
                     for (int c = 0; c < kKvTile; c += 2) {
-                        const float p0 = ptx::ex2(s[c] - m_use);
-                        const float p1 = ptx::ex2(s[c + 1] - m_use);
-                        lsum += p0 + p1;
+                        // p = 2^(s * log2(e)/scale - m): one FFMA + one MUFU per score
+                        const float p0 = ptx::ex2(fmaf(s[c], p.sl2, neg_m));
+                        const float p1 = ptx::ex2(fmaf(s[c + 1], p.sl2, neg_m));
+                        lsum2 = fadd2(lsum2, make_float2(p0, p1));
+                        uint32_t w;
                         if constexpr (kFmt == 1) {
                             __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-                            pk[c / 2] = *reinterpret_cast<uint32_t*>(&h);
+                            w = *reinterpret_cast<uint32_t*>(&h);
                         } else {
                             __half2 h = __floats2half2_rn(p0, p1);
-                            pk[c / 2] = *reinterpret_cast<uint32_t*>(&h);
+                            w = *reinterpret_cast<uint32_t*>(&h);
                         }
+                        pk[c / 2] = __uint_as_float(w);
                     }
                 }
-                l_run += lsum;
-                // PV of the previous tile must be complete before O or P are touched.
+                l_run += lsum2.x + lsum2.y;
+                // Observe PV_{t-1} (keeps the pv barrier phases in order; required
+                // before O is rescaled).
                 if (t > 0) {
-                    ptx::mbar_wait(b_pv, (gg - 1) & 1);
+                    ptx::mbar_wait(b_pv + 8 * ((gg - 1) & 1), ((gg - 1) >> 1) & 1);
                     ptx::tc_fence_after();
                     if (__any_sync(0xffffffffu, need)) {
 #pragma unroll 1
@@ -336,31 +391,20 @@ __device__ void prefill_cta(const RunParams& p, const CUtensorMap* tmq, const CU
                             for (int c = 0; c < 32; ++c) o[c] *= factor;
                             ptx::tmem_st32(lane_base + kTmemO + ch * 32, o);
                         }
-                        ptx::tmem_wait_st();
                     }
                 }
-                // P row -> smem, SW128 K-major: 16 B chunk c of row m at chunk c ^ (m & 7).
-                {
-                    uint8_t* prow = smem + kOffP + m * 128;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        *reinterpret_cast<uint4*>(prow + ((c ^ (m & 7)) << 4)) =
-                            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-                    }
-                }
-                ptx::fence_proxy_async_smem();
+                // P row -> TMEM over the consumed S row (A operand of the TS MMA)
+                ptx::tmem_st32(s_addr, *reinterpret_cast<float(*)[32]>(&pk[0]));
+                ptx::tmem_wait_st();
                 ptx::tc_fence_before();
-                ptx::named_bar_sync(1, 128);
-                if (tid == 0) {
-                    ptx::tc_fence_after();
-                    ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
-                    prefill_issue_pv<kFmt>(tmem + kTmemO, sP, sV + st * kKvStageBytes, t > 0);
-                    ptx::umma_commit(b_pv);
-                    ptx::umma_commit(b_vempty + 8 * st);
-                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(b_pfull + 8 * st);
             }
             // ------------------------------------------------- epilogue --
-            ptx::mbar_wait(b_pv, (g + br.nt - 1) & 1);
+            {
+                const int gl = g + br.nt - 1;
+                ptx::mbar_wait(b_pv + 8 * (gl & 1), (gl >> 1) & 1);
+            }
             ptx::tc_fence_after();
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll 1
@@ -378,39 +422,98 @@ __device__ void prefill_cta(const RunParams& p, const CUtensorMap* tmq, const CU
             if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
             ptx::tc_fence_before();
             g += br.nt;
-            ++qb;
         }
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, kTmemCols);
     }
 }
 
 // ============================================================= decode ===
+constexpr int kDecStages = 3;                          // pages in flight per warp
+constexpr uint32_t kDecPageBytes = 16 * kHeadDim * 2;  // one head-page of K (or V): 4 KB
+constexpr uint32_t kDecStageBytes = 2 * kDecPageBytes; // K + V
+constexpr uint32_t kDecWarpBytes = kDecStages * kDecStageBytes;
+static_assert(kDecodeWarps * kDecWarpBytes <= kOffBar, "decode rings must fit below the barrier block");
+
+// Decode inner products on the warp-level tensor path (mma.sync m16n8k16,
+// fp32 accumulate): the G query heads of a KV head are the M rows (padded to
+// 16), 8 keys are an N tile, so a 16-key page costs 16 MMAs for Q K^T and 32
+// for P V (P split into bf16 hi + lo parts, which keeps P at ~16 mantissa bits).
+// K/V pages land in shared memory through TMA with the 128-byte swizzle, read
+// back with ldmatrix (.trans for V) without bank conflicts.
 template <int kFmt>
-__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    if constexpr (kFmt == 1)
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+    else
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+template <int kFmt>
+__device__ __forceinline__ uint32_t pack2(float x, float y) {
+    if constexpr (kFmt == 1) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+        return *reinterpret_cast<uint32_t*>(&h);
+    } else {
+        __half2 h = __floats2half2_rn(x, y);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+}
+template <int kFmt>
+__device__ __forceinline__ float2 unpack2(uint32_t w) {
+    if constexpr (kFmt == 1) {
+        return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+    } else {
+        return __half22float2(*reinterpret_cast<const __half2*>(&w));
+    }
+}
+// Byte offset of (row, 16-byte chunk c in 0..15) of a 16 x 128 page stored as two
+// 128B-swizzled column halves of 2 KB (TMA SWIZZLE_128B boxes of 64 elements).
+__device__ __forceinline__ uint32_t page_off(int row, int c) {
+    return static_cast<uint32_t>((c >> 3) * 2048 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ void decode_issue_page(const RunParams& p, const CUtensorMap* tk,
+                                                  const CUtensorMap* tv, uint32_t dst, uint32_t bar,
+                                                  int h, int phys) {
+    ptx::mbar_arrive_expect_tx(bar, kDecStageBytes);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        if constexpr (kFmt == 1) {
-            f[2 * i] = __uint_as_float(w[i] << 16);
-            f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    for (int dh = 0; dh < 2; ++dh) {
+        if (p.kv_layout == POD_KV_HND) {
+            ptx::tma_load_4d(dst + dh * 2048, tk, bar, dh * 64, 0, h, phys);
+            ptx::tma_load_4d(dst + kDecPageBytes + dh * 2048, tv, bar, dh * 64, 0, h, phys);
         } else {
-            const float2 x = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
-            f[2 * i] = x.x;
-            f[2 * i + 1] = x.y;
+            ptx::tma_load_4d(dst + dh * 2048, tk, bar, dh * 64, h, 0, phys);
+            ptx::tma_load_4d(dst + kDecPageBytes + dh * 2048, tv, bar, dh * 64, h, 0, phys);
         }
     }
 }
 
 // One physical decode CTA: 4 warps = 4 virtual decode CTAs over
-// split_ranges(kv_end - kv_begin, 4).  Lane l owns key slot (l >> 4) of each key
-// pair and d-elements [8 (l & 15), +8).
+// split_ranges(kv_end - kv_begin, 4) (work_decomp.hpp:179-197, semantics of
+// decode_attention_splitk, attention.hpp:240-292).  Each warp streams its pages
+// (K and V head-pages, 4 KB each) through its own 3-stage TMA ring, keeps the
+// online-softmax statistics of head row g = lane/4 (quad shuffles), and the 4
+// partials are LSE-merged through shared memory at the end.
 template <int G, int kFmt>
-__device__ void decode_cta(const RunParams& p, int cta_id, uint8_t* smem) {
+__device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUtensorMap* tv, int cta_id,
+                            uint8_t* smem, int& dpos) {
+    static_assert(G <= 8, "decode rows: G query heads of one KV head (<= 8)");
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     if (warp >= kDecodeWarps) return;
@@ -419,138 +522,133 @@ __device__ void decode_cta(const RunParams& p, int cta_id, uint8_t* smem) {
     const int base = len / kDecodeWarps, rem = len % kDecodeWarps;
     const int wb = job.kv_begin + warp * base + min(warp, rem);
     const int we = wb + base + (warp < rem ? 1 : 0);
-    const int half = lane >> 4, c8 = (lane & 15) * 8;
     const int h = job.kv_head;
+    const int gq = lane >> 2, tq = lane & 3;  // mma fragment row (head) / column pair
+    const uint32_t sbase = ptx::smem_u32(smem);
+    const uint32_t ring = sbase + warp * kDecWarpBytes;
+    const uint32_t bars = sbase + kOffDecBar + warp * (kDecStages * 8);
 
+    // A fragments of Q (rows = heads, zero above G): per 16-d k-step, cols 2t..2t+1 and +8
     using elem_t = uint16_t;
-    const elem_t* q = static_cast<const elem_t*>(p.q_decode) +
-                      (static_cast<size_t>(job.request) * p.hq + h * G) * kHeadDim + c8;
-    float qf[G][8];
+    uint32_t qa[8][2];
+    {
+        const elem_t* q = static_cast<const elem_t*>(p.q_decode) +
+                          (static_cast<size_t>(job.request) * p.hq + h * G + gq) * kHeadDim;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const uint4 v = *reinterpret_cast<const uint4*>(q + g * kHeadDim);
-        unpack8<kFmt>(v, qf[g]);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) qf[g][e] *= p.sl2;
-    }
-    float m[G], l[G], o[G][8];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        m[g] = -INFINITY;
-        l[g] = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[g][e] = 0.f;
-    }
-
-    const elem_t* kp = static_cast<const elem_t*>(p.k_pool);
-    const elem_t* vp = static_cast<const elem_t*>(p.v_pool);
-    const size_t key_stride = p.kv_layout == POD_KV_HND ? kHeadDim : static_cast<size_t>(p.hkv) * kHeadDim;
-    const int32_t* pidx = p.page_indices + p.page_indptr[job.page_row];
-    if (we > wb) {
-        const int pg0 = wb >> 4, pg1 = (we - 1) >> 4;
-        int cached_base = -1000000;
-        int cached = 0;
-        for (int pg = pg0; pg <= pg1; ++pg) {
-            if (pg - cached_base >= 32 || pg < cached_base) {
-                cached_base = pg;
-                cached = (pg + lane <= pg1) ? __ldg(pidx + pg + lane) : 0;
-            }
-            const int phys = __shfl_sync(0xffffffffu, cached, pg - cached_base);
-            size_t off;
-            if (p.kv_layout == POD_KV_HND)
-                off = (static_cast<size_t>(phys) * p.hkv + h) * 16 * kHeadDim;
-            else
-                off = (static_cast<size_t>(phys) * 16 * p.hkv + h) * kHeadDim;
-            const elem_t* kpg = kp + off + c8;
-            const elem_t* vpg = vp + off + c8;
-            uint4 kr[8], vr[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) kr[i] = ptx::ldg_nc_v4(kpg + (2 * i + half) * key_stride);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) vr[i] = ptx::ldg_nc_v4(vpg + (2 * i + half) * key_stride);
-            float s[8][G];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                float kf[8];
-                unpack8<kFmt>(kr[i], kf);
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    float acc = 0.f;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) acc = fmaf(qf[g][e], kf[e], acc);
-                    s[i][g] = acc;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    float a = s[i][g];
-                    a += __shfl_xor_sync(0xffffffffu, a, 1);
-                    a += __shfl_xor_sync(0xffffffffu, a, 2);
-                    a += __shfl_xor_sync(0xffffffffu, a, 4);
-                    a += __shfl_xor_sync(0xffffffffu, a, 8);
-                    s[i][g] = a;
-                }
-            const int kbase = pg * 16 + half;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int key = kbase + 2 * i;
-                if (key < wb || key >= we) {
-#pragma unroll
-                    for (int g = 0; g < G; ++g) s[i][g] = -INFINITY;
-                }
-            }
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                float mx = s[0][g];
-#pragma unroll
-                for (int i = 1; i < 8; ++i) mx = fmaxf(mx, s[i][g]);
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-                const float m_new = fmaxf(m[g], mx);
-                const float f = ptx::ex2(m[g] - m_new);  // m = -inf -> 0
-                m[g] = m_new;
-                l[g] *= f;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) o[g][e] *= f;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float pr = ptx::ex2(s[i][g] - m_new);
-                    s[i][g] = pr;
-                    l[g] += pr;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                float vf[8];
-                unpack8<kFmt>(vr[i], vf);
-#pragma unroll
-                for (int g = 0; g < G; ++g)
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) o[g][e] = fmaf(s[i][g], vf[e], o[g][e]);
-            }
+        for (int ks = 0; ks < 8; ++ks) {
+            qa[ks][0] = gq < G ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 2 * tq) : 0u;
+            qa[ks][1] = gq < G ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 8 + 2 * tq) : 0u;
         }
     }
-    // combine the two key halves of the warp
+    float m = -INFINITY, l = 0.f;  // row gq statistics (log2 domain); l is this lane's partial
+    float o[16][4];                // O fragments: 16 n-tiles of 8 d (rows >= 8 stay zero)
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        l[g] += __shfl_xor_sync(0xffffffffu, l[g], 16);
+    for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+
+    const int32_t* pidx = p.page_indices + p.page_indptr[job.page_row];
+    const int pg0 = wb >> 4;
+    const int npg = we > wb ? ((we - 1) >> 4) - pg0 + 1 : 0;
+    // page-table cache: lane j holds the physical id of page (cache_base + j)
+    int cache_base = 0;
+    int cached = (lane < npg) ? __ldg(pidx + pg0 + lane) : 0;
+    // ring slot of this warp's n-th page overall: n % kDecStages, phase (n / kDecStages) & 1
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[g][e] += __shfl_xor_sync(0xffffffffu, o[g][e], 16);
+    for (int j = 0; j < kDecStages; ++j) {
+        const int phys = __shfl_sync(0xffffffffu, cached, j);
+        const int st = (dpos + j) % kDecStages;
+        if (lane == 0 && j < npg) decode_issue_page(p, tk, tv, ring + st * kDecStageBytes, bars + 8 * st, h, phys);
     }
-    // in-CTA merge of the 4 virtual CTAs (LSE merge, attention.hpp:294-326)
+    __syncwarp();
+    // ldmatrix row/chunk roles of this lane
+    const int lm = lane >> 3, lr = lane & 7;
+    for (int i = 0; i < npg; ++i) {
+        const int n = dpos + i;
+        const int st = n % kDecStages;
+        ptx::mbar_wait(bars + 8 * st, (n / kDecStages) & 1);
+        const uint32_t kst = ring + st * kDecStageBytes;
+        const uint32_t vst = kst + kDecPageBytes;
+        // ---- S = Q K^T for the page's 16 keys (2 n-tiles of 8)
+        float sc[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+            const int key = nt * 8 + lr;
+#pragma unroll
+            for (int kp = 0; kp < 4; ++kp) {  // two k-steps per ldmatrix.x4
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(kst + page_off(key, 4 * kp + lm), b0, b1, b2, b3);
+                mma16816<kFmt>(sc[nt], qa[2 * kp][0], qa[2 * kp][1], b0, b1);
+                mma16816<kFmt>(sc[nt], qa[2 * kp + 1][0], qa[2 * kp + 1][1], b2, b3);
+            }
+        }
+        // scores of row gq: keys 8 nt + 2 tq + {0,1}
+        float x[4] = {sc[0][0] * p.sl2, sc[0][1] * p.sl2, sc[1][0] * p.sl2, sc[1][1] * p.sl2};
+        const int kfirst = (pg0 + i) * 16;
+        if (kfirst < wb || kfirst + 16 > we) {  // boundary page: keys outside [wb, we)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int key = kfirst + (e >> 1) * 8 + 2 * tq + (e & 1);
+                if (key < wb || key >= we) x[e] = -INFINITY;
+            }
+        }
+        float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m, mx);
+        const float f = ptx::ex2(m - m_new);  // m = -inf -> 0
+        m = m_new;
+        float pr[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pr[e] = ptx::ex2(x[e] - m_new);
+        l = l * f + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
+        if (!__all_sync(0xffffffffu, f == 1.f)) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                o[j][0] *= f;
+                o[j][1] *= f;
+            }
+        }
+        // P as the A operand: hi = round(p), lo = round(p - hi)
+        const uint32_t ph0 = pack2<kFmt>(pr[0], pr[1]), ph1 = pack2<kFmt>(pr[2], pr[3]);
+        const float2 h0 = unpack2<kFmt>(ph0), h1 = unpack2<kFmt>(ph1);
+        const uint32_t pl0 = pack2<kFmt>(pr[0] - h0.x, pr[1] - h0.y), pl1 = pack2<kFmt>(pr[2] - h1.x, pr[3] - h1.y);
+        // ---- O += P V: 16 n-tiles of 8 d, V fragments via ldmatrix.trans
+#pragma unroll
+        for (int dp = 0; dp < 8; ++dp) {  // two d-tiles per ldmatrix.x4
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(vst + page_off((lm & 1) * 8 + lr, 2 * dp + (lm >> 1)), b0, b1, b2, b3);
+            mma16816<kFmt>(o[2 * dp], ph0, ph1, b0, b1);
+            mma16816<kFmt>(o[2 * dp], pl0, pl1, b0, b1);
+            mma16816<kFmt>(o[2 * dp + 1], ph0, ph1, b2, b3);
+            mma16816<kFmt>(o[2 * dp + 1], pl0, pl1, b2, b3);
+        }
+        // ---- refill this stage with page i + kDecStages
+        const int nxt = i + kDecStages;
+        if (nxt < npg) {
+            if (nxt - cache_base >= 32) {
+                cache_base += 32;
+                cached = (cache_base + lane < npg) ? __ldg(pidx + pg0 + cache_base + lane) : 0;
+            }
+            const int phys = __shfl_sync(0xffffffffu, cached, nxt - cache_base);
+            __syncwarp();
+            if (lane == 0) decode_issue_page(p, tk, tv, ring + st * kDecStageBytes, bars + 8 * st, h, phys);
+        }
+    }
+    dpos += npg;
+    l += __shfl_xor_sync(0xffffffffu, l, 1);
+    l += __shfl_xor_sync(0xffffffffu, l, 2);
+    // in-CTA merge of the 4 virtual CTAs (LSE merge, attention.hpp:294-326);
+    // reuses warp 0's ring (every warp is past its last TMA wait).
     constexpr int kStride = kHeadDim + 4;
     float* red = reinterpret_cast<float*>(smem);
-    if (half == 0) {
+    ptx::named_bar_sync(2, kDecodeWarps * 32);
+    if (gq < G) {
+        float* dst = red + (warp * G + gq) * kStride;
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            float* dst = red + (warp * G + g) * kStride;
-            *reinterpret_cast<float4*>(dst + c8) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
-            *reinterpret_cast<float4*>(dst + c8 + 4) = make_float4(o[g][4], o[g][5], o[g][6], o[g][7]);
-            if (lane == 0) {
-                dst[kHeadDim] = m[g];
-                dst[kHeadDim + 1] = l[g];
-            }
+        for (int j = 0; j < 16; ++j) *reinterpret_cast<float2*>(dst + 8 * j + 2 * tq) = make_float2(o[j][0], o[j][1]);
+        if (tq == 0) {
+            dst[kHeadDim] = m;
+            dst[kHeadDim + 1] = l;
         }
     }
     ptx::named_bar_sync(2, kDecodeWarps * 32);
@@ -640,55 +738,130 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
 }
 
 // ============================================================ kernels ===
+// Picks the next work item for this resident CTA: SM-aware runtime role binding
+// (gpu_sim.hpp:114-131).  Returns op (0 prefill, 1 decode,
+// -1 both pools exhausted) and the claimed dense per-op id.
+__device__ __forceinline__ int2 claim_item(const RunParams& p, uint32_t sm, int32_t* log_slot_out) {
+    const int ratio = p.prefill_ratio + p.decode_ratio;
+    const uint32_t raw = atomicAdd(&p.ctr->sm_ctr[sm], 1u);
+    int op;
+    if (p.policy == POD_POLICY_COMPLEMENT) {
+        // bind from what is resident on this SM: prefill while fewer than
+        // prefill_ratio prefill items run here, decode otherwise
+        const uint32_t resident = atomicAdd(&p.ctr->running_prefill[sm], 1u);
+        op = resident < static_cast<uint32_t>(p.prefill_ratio) ? 0 : 1;
+        if (op == 1) atomicSub(&p.ctr->running_prefill[sm], 1u);
+    } else {
+        const int ticket = static_cast<int>(raw % static_cast<uint32_t>(ratio));
+        op = ticket < p.prefill_ratio ? 0 : 1;
+    }
+    int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
+    if (id >= (op == 0 ? p.num_pctas : p.num_dctas)) {
+        if (p.policy == POD_POLICY_COMPLEMENT && op == 0) atomicSub(&p.ctr->running_prefill[sm], 1u);
+        op ^= 1;
+        id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
+        if (id >= (op == 0 ? p.num_pctas : p.num_dctas))
+            op = -1;
+        else if (p.policy == POD_POLICY_COMPLEMENT && op == 0)
+            atomicAdd(&p.ctr->running_prefill[sm], 1u);
+    }
+    *log_slot_out = -1;
+    if (p.role_log && op >= 0) {
+        const uint32_t slot = atomicAdd(&p.ctr->arrival, 1u);
+        int32_t* rec = p.role_log + 8 * slot;
+        rec[0] = static_cast<int32_t>(sm);
+        rec[1] = static_cast<int32_t>(raw);
+        rec[2] = op;
+        rec[3] = id;
+        rec[4] = static_cast<int32_t>(slot);
+        rec[5] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
+        rec[7] = static_cast<int32_t>(blockIdx.x);
+        *log_slot_out = static_cast<int32_t>(slot);
+    }
+    return make_int2(op, id);
+}
+
+// The POD kernel: a persistent grid of 2 CTAs per SM (every CTA holds 256 TMEM
+// columns, two fill the SM's 512).  Each CTA repeatedly binds a role for its
+// next work item -- a prefill CtaTask or a decode (request, kv head, split)
+// parent with 4 virtual warps -- until both pools are drained.  Launched with
+// num_dctas = 0 (or num_pctas = 0) it is the standalone prefill (decode) kernel
+// of the serial comparator.  Persistence matters on sm_100: kernels that use
+// tcgen05 get one new CTA dispatched only into an idle SM, so a classic
+// CTA-per-task grid would lose the second slot after the first wave.
 template <int G, int kFmt>
 __global__ void __launch_bounds__(kThreads, 2)
     pod_fused_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmq,
-                     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
+                     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                     const __grid_constant__ CUtensorMap tdk, const __grid_constant__ CUtensorMap tdv) {
     extern __shared__ __align__(1024) uint8_t smem[];
     int* role = reinterpret_cast<int*>(smem + kOffRole);
-    if (threadIdx.x == 0) {
-        // SM-aware CTA scheduling (gpu_sim.hpp:114-131)
-        const uint32_t sm = ptx::smid();
-        const int ratio = p.prefill_ratio + p.decode_ratio;
-        const uint32_t raw = atomicAdd(&p.ctr->sm_ctr[sm], 1u);
-        const int ticket = static_cast<int>(raw % static_cast<uint32_t>(ratio));
-        int op = ticket < p.prefill_ratio ? 0 : 1;
-        int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
-        if (id >= (op == 0 ? p.num_pctas : p.num_dctas)) {
-            op ^= 1;
-            id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
-            if (id >= (op == 0 ? p.num_pctas : p.num_dctas)) op = -1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sbase = ptx::smem_u32(smem);
+    if (tid == 0) {
+        if (sbase & 1023u) __trap();  // SW128 atoms need a 1024-aligned base
+        for (int i = 0; i < 16; ++i) ptx::mbar_init(sbase + kOffBar + 8 * i, (i == 12 || i == 13) ? kPrefillWarps : 1);
+        for (int i = 0; i < kDecodeWarps * kDecStages; ++i) ptx::mbar_init(sbase + kOffDecBar + 8 * i, 1);
+        ptx::fence_mbar_init();
+    }
+    // Every CTA allocates and relinquishes: on sm_100 a second CTA of a tcgen05
+    // kernel is only co-scheduled on an SM once the resident one has given up
+    // its TMEM allocation permit (decode-only launches included).
+    if (warp == 0) {
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), kTmemCols);
+        ptx::tmem_relinquish();
+    }
+    if (warp == 4 && lane == 0) {
+        if (p.num_pctas > 0) ptx::prefetch_tmap(&tmq);
+        ptx::prefetch_tmap(&tmk);
+        ptx::prefetch_tmap(&tmv);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sm = ptx::smid();
+    PrefillState ps;
+    int dpos = 0;
+    while (true) {
+        if (tid == 0) {
+            int32_t slot;
+            const int2 w = claim_item(p, sm, &slot);
+            role[0] = w.x;
+            role[1] = w.y;
+            role[2] = slot;
         }
-        role[0] = op;
-        role[1] = id;
-        if (p.role_log) {
-            const uint32_t arrival = atomicAdd(&p.ctr->arrival, 1u);
-            int32_t* rec = p.role_log + 8 * blockIdx.x;
-            rec[0] = static_cast<int32_t>(sm);
-            rec[1] = static_cast<int32_t>(raw);
-            rec[2] = op;
-            rec[3] = id;
-            rec[4] = static_cast<int32_t>(arrival);
-            rec[5] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
-            rec[7] = static_cast<int32_t>(blockIdx.x);
+        __syncthreads();
+        const int op = role[0], id = role[1], slot = role[2];
+        __syncthreads();  // role[] is rewritten by the next claim
+        if (op < 0) break;
+        if (op == 0)
+            prefill_item<kFmt>(p, &tmq, &tmk, &tmv, id, smem, tmem, ps);
+        else
+            decode_item<G, kFmt>(p, &tmk, &tmv, id, smem, dpos);
+        ptx::tc_fence_before();
+        __syncthreads();
+        ptx::tc_fence_after();
+        if (tid == 0) {
+            if (p.policy == POD_POLICY_COMPLEMENT && op == 0) atomicSub(&p.ctr->running_prefill[sm], 1u);
+            if (slot >= 0) p.role_log[8 * slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
         }
     }
-    __syncthreads();
-    const int op = role[0], id = role[1];
-    if (op == 0)
-        prefill_cta<kFmt>(p, &tmq, &tmk, &tmv, id, smem);
-    else if (op == 1)
-        decode_cta<G, kFmt>(p, id, smem);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (p.role_log) p.role_log[8 * blockIdx.x + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, kTmemCols);
+    }
+    if (tid == 0) {
         __threadfence();
-        const uint32_t total = static_cast<uint32_t>(p.num_pctas + p.num_dctas);
         const uint32_t prev = atomicAdd(&p.ctr->done, 1u);
-        if (prev == total - 1) {
+        if (prev == gridDim.x - 1) {
             // last CTA out: re-arm the counters for the next launch (graph friendly)
             const uint32_t n = min(ptx::nsmid(), static_cast<uint32_t>(kMaxSms));
-            for (uint32_t i = 0; i < n; ++i) p.ctr->sm_ctr[i] = 0;
+            for (uint32_t i = 0; i < n; ++i) {
+                p.ctr->sm_ctr[i] = 0;
+                p.ctr->running_prefill[i] = 0;
+            }
             p.ctr->cta_assign[0] = 0;
             p.ctr->cta_assign[1] = 0;
             p.ctr->arrival = 0;
@@ -696,20 +869,6 @@ __global__ void __launch_bounds__(kThreads, 2)
             __threadfence();
         }
     }
-}
-
-template <int kFmt>
-__global__ void __launch_bounds__(kThreads, 2)
-    pod_prefill_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmq,
-                       const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    prefill_cta<kFmt>(p, &tmq, &tmk, &tmv, blockIdx.x, smem);
-}
-
-template <int G, int kFmt>
-__global__ void __launch_bounds__(kDecodeWarps * 32, 3) pod_decode_kernel(const __grid_constant__ RunParams p) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    decode_cta<G, kFmt>(p, blockIdx.x, smem);
 }
 
 __global__ void gather_probe_kernel(const uint16_t* pool, int layout, int hkv, const int32_t* indptr,
@@ -758,7 +917,8 @@ pod_status cuda_fail(cudaError_t e, const char* where) {
 int64_t fused_smem_bytes() { return kSmemBytes; }
 
 struct Maps {
-    CUtensorMap q, k, v;
+    CUtensorMap q, k, v;  // prefill role: SW128 boxes of 64 d x 16 tokens, Q boxes of 64 d x 128 rows
+    CUtensorMap dk, dv;   // decode role: one whole head-page (128 d x 16 tokens), no swizzle
 };
 
 pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_pool, const void* v_pool,
@@ -793,6 +953,14 @@ pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) {
                 set_last_error("cuTensorMapEncodeTiled(kv) failed: " + std::to_string(static_cast<int>(r)));
+                return POD_ERR_CUDA;
+            }
+            cuuint32_t dbox[4] = {kHeadDim, box[1], box[2], 1};
+            r = enc(which == 0 ? &m->dk : &m->dv, dt, 4, const_cast<void*>(which == 0 ? k_pool : v_pool), dims,
+                    strides, dbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                set_last_error("cuTensorMapEncodeTiled(decode kv) failed: " + std::to_string(static_cast<int>(r)));
                 return POD_ERR_CUDA;
             }
         }
@@ -846,6 +1014,7 @@ RunParams make_params(const pod_plan* plan, const void* q_decode, const void* k_
     p.offset = plan->batch.has_prefill ? static_cast<int32_t>(plan->batch.prefill.position_offset) : 0;
     p.kv_layout = plan->batch.kv_layout;
     p.decode_splits = static_cast<int32_t>(plan->decode_splits);
+    p.policy = plan->opts.policy;
     p.num_pages = num_pages;
     p.sl2 = static_cast<float>(1.4426950408889634 / plan->shape.scale);
     return p;
@@ -874,19 +1043,28 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
     static bool attr_done = false;
     if (!attr_done) {
         cudaFuncSetAttribute(pod_fused_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        cudaFuncSetAttribute(pod_prefill_kernel<kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         attr_done = true;
     }
-    const int P = p.num_pctas, D = p.num_dctas;
-    const size_t dec_smem = static_cast<size_t>(kDecodeWarps) * G * (kHeadDim + 4) * sizeof(float);
+    const int slots = 2 * plan->dev.num_sms;  // resident CTAs of the persistent grid
+    auto launch = [&](const RunParams& q) {
+        const int items = q.num_pctas + q.num_dctas;
+        if (items > 0)
+            pod_fused_kernel<G, kFmt><<<std::min(items, slots), kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v,
+                                                                                         maps.dk, maps.dv);
+    };
     if (mode == 0) {
-        if (P + D > 0)
-            pod_fused_kernel<G, kFmt><<<P + D, kThreads, kSmemBytes, s>>>(p, maps.q, maps.k, maps.v);
+        launch(p);
     } else {
-        if ((mode == 1 || mode == 2) && P > 0)
-            pod_prefill_kernel<kFmt><<<P, kThreads, kSmemBytes, s>>>(p, maps.q, maps.k, maps.v);
-        if ((mode == 1 || mode == 3) && D > 0)
-            pod_decode_kernel<G, kFmt><<<D, kDecodeWarps * 32, dec_smem, s>>>(p);
+        if (mode == 1 || mode == 2) {
+            RunParams q = p;
+            q.num_dctas = 0;
+            launch(q);
+        }
+        if (mode == 1 || mode == 3) {
+            RunParams q = p;
+            q.num_pctas = 0;
+            launch(q);
+        }
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "pod kernel launch");
@@ -1029,5 +1207,20 @@ pod_status pod_attn_gather_probe(const pod_plan* plan, const void* kv_pool, int6
 }
 
 const char* pod_last_error(void) { return g_last_error.c_str(); }
+
+pod_status pod_attn_occupancy(const pod_plan* plan, int32_t* fused, int32_t* prefill, int32_t* decode) {
+    if (!plan || !fused || !prefill || !decode) return POD_ERR_INVALID_ARGUMENT;
+    const int G = plan->shape.num_q_heads / plan->shape.num_kv_heads;
+    if (G != 4) return POD_ERR_UNSUPPORTED;
+    int a = 0;
+    cudaFuncSetAttribute(pod_fused_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, pod_fused_kernel<4, 1>, kThreads, kSmemBytes);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    // one persistent kernel serves all three launch kinds
+    *fused = a;
+    *prefill = a;
+    *decode = a;
+    return POD_OK;
+}
 
 }  // extern "C"

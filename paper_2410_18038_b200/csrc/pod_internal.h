@@ -16,7 +16,7 @@ constexpr int kMBlock = 128;        // tcgen05 M: packed (row, q-head) rows per 
 constexpr int kKvTile = 64;         // prefill keys per tcgen05 N tile (4 pages of 16)
 constexpr int kDecodeWarps = 4;     // virtual decode CTAs per physical CTA
 constexpr int kPrefillWarps = 4;    // softmax warps (one TMEM lane quadrant each)
-constexpr int kThreads = 160;       // 4 compute warps + 1 TMA-producer warp
+constexpr int kThreads = 192;       // 4 softmax warps + 1 TMA-producer warp + 1 MMA warp
 constexpr int kMaxSms = 1024;       // sm counter slots (sized for %nsmid, not %smid density)
 
 // One physical prefill CTA = one CtaTask of decompose_prefill (work_decomp.hpp:204-247):
@@ -51,6 +51,7 @@ struct SchedCounters {
     uint32_t cta_assign[2];
     uint32_t done;
     uint32_t arrival;
+    uint32_t running_prefill[kMaxSms];  // POD_POLICY_COMPLEMENT: prefill CTAs resident per SM
 };
 
 struct WorkspaceLayout {

@@ -305,6 +305,10 @@ void scheduler_ratio(pod_plan& p) {
         p.prefill_ratio = g > 0 ? P / g : (P > 0 ? 1 : 0);
         p.decode_ratio = g > 0 ? D / g : (D > 0 ? 1 : 0);
         if (p.prefill_ratio == 0 && p.decode_ratio == 0) p.prefill_ratio = 1;
+    } else if (p.opts.policy == POD_POLICY_COMPLEMENT) {
+        // one prefill CTA per SM (2 slots): the other slot streams decode
+        p.prefill_ratio = P > 0 ? 1 : 0;
+        p.decode_ratio = 1;
     } else {
         // proportional share rounded to the per-SM slot count, never starving an op
         const int slots = std::max(2, p.cfg.ctas_per_sm);
@@ -377,9 +381,10 @@ void build(pod_plan& p) {
                 estimate_prefill_serial(p) >= estimate_decode_serial(p) && p.batch.has_prefill;
             p.cfg = make_tile_config(prefill_dominant ? 2 : 4);
         }
-        if (p.opts.virtual_decode != 0) p.cfg.virtual_decode = 1;
     }
+    // -1 keeps the config's flag (reference configs: off; B200 config: on)
     if (p.opts.virtual_decode == 0) p.cfg.virtual_decode = 0;
+    if (p.opts.virtual_decode == 1) p.cfg.virtual_decode = 1;
     if (p.opts.split_wave_cap > 0) p.cfg.split_wave_cap = p.opts.split_wave_cap;
     if (p.batch.has_prefill) decompose_prefill(p);
     if (!p.decode_ctx.empty()) decompose_decode(p);

@@ -300,7 +300,7 @@ def make_tile_config(ctas_per_sm: int) -> TileConfig:
 
 def select_tile_config(batch: HybridBatchSpec, gpu: GpuSpec) -> TileConfig:
     """select_tile_config (work_decomp.hpp:139-145)."""
-    p = Plan(batch, gpu, PlanOptions(tile_mode=_abi.POD_TILE_REFERENCE, virtual_decode=0))
+    p = Plan(batch, gpu, PlanOptions(tile_mode=_abi.POD_TILE_REFERENCE, virtual_decode=-1))
     cfg = p.tile_config()
     p.close()
     return cfg
@@ -308,7 +308,7 @@ def select_tile_config(batch: HybridBatchSpec, gpu: GpuSpec) -> TileConfig:
 
 def decompose_hybrid(batch: HybridBatchSpec, gpu: GpuSpec, config: Optional[TileConfig] = None) -> WorkDecomposition:
     """decompose_hybrid (work_decomp.hpp:249-261)."""
-    p = Plan(batch, gpu, PlanOptions(tile_mode=_abi.POD_TILE_REFERENCE, virtual_decode=0, tile_override=config))
+    p = Plan(batch, gpu, PlanOptions(tile_mode=_abi.POD_TILE_REFERENCE, virtual_decode=-1, tile_override=config))
     wd = p.tasks()
     p.close()
     return wd

@@ -1,0 +1,80 @@
+"""Runs one configuration in a given mode for ncu captures / role-log timelines.
+
+  python tools/profile_run.py --config c2_b64 --mode fused --iters 3 [--roles out.json]
+"""
+import argparse
+import json
+import math
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+import paper_2410_18038_b200 as pkg  # noqa: E402
+from bench import CONFIGS  # noqa: E402
+from paper_2410_18038_b200.hybrid import PodAttention  # noqa: E402
+from paper_2410_18038_b200.workload import build_workload, make_batch  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2_b64")
+    ap.add_argument("--mode", default="fused")
+    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--policy", type=int, default=0)
+    ap.add_argument("--tile-mode", type=int, default=1)
+    ap.add_argument("--decode-splits", type=int, default=0)
+    ap.add_argument("--roles", default="")
+    a = ap.parse_args()
+    hq, hkv, chunk, off, b, ctx = CONFIGS[a.config]
+    shape = pkg.ModelShape(hq, hkv, 128, math.sqrt(128))
+    batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
+    wl = build_workload(batch, device="cuda")
+    op = PodAttention(batch, options=pkg.PlanOptions(policy=a.policy, tile_mode=a.tile_mode,
+                                                     decode_splits=a.decode_splits))
+    log = op.enable_role_log() if a.roles else None
+    out = op.alloc_outputs()
+    for _ in range(a.iters):
+        op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=out,
+               mode=a.mode)
+    torch.cuda.synchronize()
+    if log is not None:
+        rec = log.view(-1, 8).cpu().tolist()
+        t0 = min(r[5] for r in rec)
+        rows = [{"sm": r[0], "ticket": r[1], "op": r[2], "id": r[3], "arrival": r[4],
+                 "start_us": (r[5] - t0) / 1000.0, "end_us": ((r[6] - t0) % (1 << 31)) / 1000.0} for r in rec]
+        Path(a.roles).write_text(json.dumps(rows))
+        for opk, name in ((0, "prefill"), (1, "decode")):
+            rs = [r for r in rows if r["op"] == opk]
+            if rs:
+                dur = sorted(r["end_us"] - r["start_us"] for r in rs)
+                print(f"{name}: n={len(rs)} start[min,max]=({min(r['start_us'] for r in rs):.1f},"
+                      f"{max(r['start_us'] for r in rs):.1f}) end_max={max(r['end_us'] for r in rs):.1f} "
+                      f"dur[p10,p50,p90]=({dur[len(dur)//10]:.1f},{dur[len(dur)//2]:.1f},{dur[9*len(dur)//10]:.1f})")
+        # concurrency per SM
+        import collections
+        bysm = collections.defaultdict(list)
+        for r in rows:
+            bysm[r["sm"]].append(r)
+        mx = collections.Counter()
+        for smv, rs in bysm.items():
+            ev = sorted([(r["start_us"], 1) for r in rs] + [(r["end_us"], -1) for r in rs])
+            cur = best = 0
+            for _, dlt in ev:
+                cur += dlt
+                best = max(best, cur)
+            mx[best] += 1
+        print("max concurrent CTAs per SM histogram:", dict(mx))
+    import ctypes as C
+    from paper_2410_18038_b200._abi import lib
+    a, b, c = C.c_int32(), C.c_int32(), C.c_int32()
+    st = lib().pod_attn_occupancy(op.plan.handle, C.byref(a), C.byref(b), C.byref(c))
+    print("occupancy (fused, prefill, decode):", st, a.value, b.value, c.value)
+    print("ok")
+
+
+if __name__ == "__main__":
+    main()
