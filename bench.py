@@ -205,31 +205,29 @@ def run_pod(args, rank, world, local_rank):
 
     import paper_2410_18038_b200 as pkg
     from paper_2410_18038_b200.hybrid import PodAttention
+    from paper_2410_18038_b200.tp import gather_outputs, shard_heads
     from paper_2410_18038_b200.workload import build_workload, make_batch
 
     hq, hkv, chunk, off, b, ctx = CONFIGS[args.config]
     if hkv % world:
         raise SystemExit(f"Hkv={hkv} not divisible by {world} GPUs")
-    hq_r, hkv_r = hq // world, hkv // world
+    shard = shard_heads(pkg.ModelShape(hq, hkv, 128, math.sqrt(128)), rank, world)
+    hq_r, hkv_r = shard.shape.num_q_heads, shard.shape.num_kv_heads
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    shape = pkg.ModelShape(hq_r, hkv_r, 128, math.sqrt(128))
+    shape = shard.shape
     batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
     wl = build_workload(batch, device=dev, seed_q=42 + 1000 * rank, seed_kv=43 + 1000 * rank)
     opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode)
     op = PodAttention(batch, options=opts, device=local_rank)
     out = op.alloc_outputs()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    tokens = chunk + b
-    gather_buf = None
-    if world > 1:
-        gather_buf = torch.empty(world * tokens * hq_r * 128, dtype=torch.float32, device=dev)
 
     def step(mode):
         op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=out, mode=mode)
-        if world > 1:
+        if world > 1:  # assemble the layer output: one all-gather of [tokens][Hq/T][d] over NVLink
             local = torch.cat([out.o_prefill.reshape(-1), out.o_decode.reshape(-1)])
-            dist.all_gather_into_tensor(gather_buf, local)
+            gather_outputs(local, world)
 
     def timed(mode, steps, warmup):
         for _ in range(warmup):

@@ -45,3 +45,20 @@ def slice_heads(x: torch.Tensor, shard: HeadShard, kv: bool) -> torch.Tensor:
 def assemble(gathered: torch.Tensor, world: int, tokens: int, hq_rank: int, d: int) -> torch.Tensor:
     """[world * tokens * hq_rank * d] (rank-major all-gather buffer) -> [tokens][world*hq_rank][d]."""
     return gathered.view(world, tokens, hq_rank, d).permute(1, 0, 2, 3).reshape(tokens, world * hq_rank, d)
+
+
+def gather_outputs(local: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """All-gathers each rank's flattened [tokens][Hq/T][d] output into a rank-major
+    buffer (one NCCL all-gather over NVLink on GPUs; gloo for CPU tests)."""
+    import torch.distributed as dist
+
+    if world == 1:
+        return local.reshape(-1)
+    flat = local.reshape(-1).contiguous()
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)
+        dist.all_gather_into_tensor(out, flat, group=group)
+        return out
+    parts = [torch.empty_like(flat) for _ in range(world)]
+    dist.all_gather(parts, flat, group=group)
+    return torch.cat(parts)

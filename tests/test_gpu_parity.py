@@ -1,0 +1,272 @@
+"""GPU parity: the sm_100a POD kernels vs the CPU oracle on identical bf16 inputs.
+
+Tolerance (north star): fp32 accumulate, bf16 inputs -> max |O_gpu - O_ref| <=
+2e-3 * max |O_ref| per compared block; |LSE_gpu - LSE_ref| <= 2e-3 (natural log).
+Integer work (page-table gather, scheduler claims) is checked bit-exactly.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2410_18038_b200 as pkg
+from oracle import pyoracle as O
+from paper_2410_18038_b200._abi import (POD_DTYPE_FP16, POD_KV_NHD, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT,
+                                        POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_TILE_B200,
+                                        POD_TILE_REFERENCE)
+from paper_2410_18038_b200.workload import build_workload, make_batch
+from tests.common import LSE_TOL, O_TOL, compare_decode, compare_prefill
+
+pytestmark = pytest.mark.gpu
+
+SCALE = math.sqrt(128)
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _run(batch, mode="fused", options=None, q_scale=1.0, dtype=torch.bfloat16, wl=None):
+    from paper_2410_18038_b200.hybrid import PodAttention
+
+    wl = wl or build_workload(batch, device="cuda", q_scale=q_scale, dtype=dtype)
+    op = PodAttention(batch, options=options)
+    out = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, mode=mode)
+    torch.cuda.synchronize()
+    return wl, op, out
+
+
+def _check(wl, out, kv_heads=None, requests=None, row_range=None):
+    b = wl.batch
+    if b.prefill is not None:
+        eo, el = compare_prefill(wl, out.o_prefill.cpu().numpy(), out.lse_prefill.cpu().numpy(), kv_heads, row_range)
+        assert eo <= O_TOL and el <= LSE_TOL, ("prefill", eo, el)
+    if b.decodes:
+        eo, el = compare_decode(wl, out.o_decode.cpu().numpy(), out.lse_decode.cpu().numpy(), requests, kv_heads)
+        assert eo <= O_TOL and el <= LSE_TOL, ("decode", eo, el)
+
+
+CASES = {
+    # name: (hq, hkv, chunk, offset, decode contexts)
+    "decode_only": (32, 8, 0, 0, [300, 77, 1024, 16, 1, 17]),
+    "prefill_only": (32, 8, 96, 160, []),
+    "hybrid_gqa4": (32, 8, 96, 160, [300, 77, 1024]),
+    "mha": (8, 8, 130, 0, [257, 64]),
+    "gqa2": (16, 8, 70, 33, [129, 5]),
+    "gqa8": (32, 4, 40, 500, [700, 31]),
+    "chunk1_offset0": (32, 8, 1, 0, [2]),
+    "page_edges": (32, 8, 17, 15, [15, 16, 33, 48]),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("mode", ["fused", "serial"])
+def test_matches_oracle(name, mode):
+    _need_gpu()
+    hq, hkv, chunk, off, dec = CASES[name]
+    batch = make_batch(pkg.ModelShape(hq, hkv, 128, SCALE), chunk=chunk, offset=off, decode_ctx=dec)
+    wl, _, out = _run(batch, mode)
+    _check(wl, out)
+
+
+@pytest.mark.parametrize("policy", [POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED,
+                                    POD_POLICY_COMPLEMENT])
+def test_policies_and_reference_tiles(policy):
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=200, offset=37, decode_ctx=[500, 33, 90])
+    for tile_mode in (POD_TILE_B200, POD_TILE_REFERENCE):
+        wl, _, out = _run(batch, options=pkg.PlanOptions(policy=policy, tile_mode=tile_mode))
+        _check(wl, out)
+
+
+def test_peaky_queries():
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=64, offset=900, decode_ctx=[1000, 333])
+    wl, _, out = _run(batch, q_scale=8.0)
+    _check(wl, out)
+
+
+def test_fp16_inputs():
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=64, offset=100, decode_ctx=[200, 45])
+    batch.dtype = POD_DTYPE_FP16
+    wl, _, out = _run(batch, dtype=torch.float16)
+    # the oracle regenerates bf16-rounded values; compare against fp16-rounded ones instead
+    s = batch.shape
+    G = s.group_size()
+    q = wl.q_prefill.double().cpu().numpy()
+    k_all = wl.k_pool.double().cpu().numpy()
+    v_all = wl.v_pool.double().cpu().numpy()
+    ip, ix = wl.page_indptr.cpu().numpy(), wl.page_indices.cpu().numpy()
+
+    def cache(pool, req, ctx):
+        rows = [pool[ix[ip[req] + t // 16], :, t % 16, :] for t in range(ctx)]
+        return np.stack(rows)  # [ctx][hkv][d]
+
+    k0, v0 = cache(k_all, 0, wl.kv_lens[0]), cache(v_all, 0, wl.kv_lens[0])
+    ref = O.tiled_prefill(q, k0, v0, 100, s.num_q_heads, s.num_kv_heads, SCALE, 64, 64)
+    got = out.o_prefill.cpu().numpy()
+    assert np.abs(got - ref).max() <= O_TOL * np.abs(ref).max()
+    qd = wl.q_decode.double().cpu().numpy()
+    for r in range(2):
+        kr, vr = cache(k_all, 1 + r, wl.kv_lens[1 + r]), cache(v_all, 1 + r, wl.kv_lens[1 + r])
+        o, _ = O.decode_attention(qd[r], kr, vr, s.num_q_heads, s.num_kv_heads, SCALE)
+        assert np.abs(out.o_decode[r].cpu().numpy() - o).max() <= O_TOL * np.abs(o).max()
+
+
+def test_nhd_layout():
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=50, offset=70, decode_ctx=[90, 17])
+    wl = build_workload(batch, device="cuda")
+    batch.kv_layout = POD_KV_NHD
+    wl.k_pool = wl.k_pool.permute(0, 2, 1, 3).contiguous()
+    wl.v_pool = wl.v_pool.permute(0, 2, 1, 3).contiguous()
+    _, _, out = _run(batch, wl=wl)
+    _check(wl, out)
+
+
+def test_causality_is_bitwise():
+    _need_gpu()
+    off, chunk, r = 300, 64, 20
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=chunk, offset=off, decode_ctx=[100])
+    wl, op, out1 = _run(batch)
+    before = out1.o_prefill[: r + 1].clone()
+    ix = wl.page_indices.cpu().tolist()
+    for t in range(off + r + 1, off + chunk):  # keys no row <= r can see
+        wl.k_pool[ix[t // 16], :, t % 16, :] += 17.0
+        wl.v_pool[ix[t // 16], :, t % 16, :] -= 5.0
+    out2 = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+    torch.cuda.synchronize()
+    assert torch.equal(out2.o_prefill[: r + 1], before)
+    assert not torch.equal(out2.o_prefill[r + 1:], out1.o_prefill[r + 1:])
+
+
+def test_split_invariance():
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=128, offset=1000, decode_ctx=[3000, 1500])
+    wl = build_workload(batch, device="cuda")
+    outs = []
+    for ds in (1, 2, 3, 5):
+        for cap in (1, 2, 4):
+            _, _, out = _run(batch, options=pkg.PlanOptions(decode_splits=ds, split_wave_cap=cap), wl=wl)
+            outs.append(out)
+            _check(wl, out, kv_heads=[0, 5])
+    base = outs[0]
+    for o in outs[1:]:
+        d = (o.o_decode - base.o_decode).abs().max().item() / base.o_decode.abs().max().item()
+        p = (o.o_prefill - base.o_prefill).abs().max().item() / base.o_prefill.abs().max().item()
+        assert d <= O_TOL and p <= O_TOL
+
+
+def test_deterministic_and_fused_equals_serial_bitwise():
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=256, offset=700, decode_ctx=[900] * 6)
+    wl, op, a = _run(batch)
+    b = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+    c = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, mode="serial")
+    torch.cuda.synchronize()
+    for x in (b, c):
+        assert torch.equal(a.o_prefill, x.o_prefill) and torch.equal(a.lse_prefill, x.lse_prefill)
+        assert torch.equal(a.o_decode, x.o_decode) and torch.equal(a.lse_decode, x.lse_decode)
+
+
+def test_cuda_graph_replay():
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=96, offset=100, decode_ctx=[400, 80])
+    wl = build_workload(batch, device="cuda")
+    op = PodAttention(batch)
+    out = op.alloc_outputs()
+    ref = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=out, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=out,
+                   stream=s)
+    for _ in range(3):
+        out.o_prefill.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out.o_prefill, ref.o_prefill) and torch.equal(out.o_decode, ref.o_decode)
+
+
+def test_gather_probe_bit_exact():
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=40, offset=9, decode_ctx=[1, 31, 64])
+    wl, op, _ = _run(batch)
+    pool = wl.k_pool.view(torch.int16)
+    for req, ctx in enumerate(wl.kv_lens):
+        got = op.gather_probe(pool, wl.page_indptr, wl.page_indices, req, ctx).cpu()
+        ref = O.gather_pages(pool.cpu().numpy().view(np.uint16), 0, wl.page_indptr.cpu().numpy(),
+                             wl.page_indices.cpu().numpy(), req, ctx)
+        assert np.array_equal(got.numpy().view(np.uint16), _bf16_bits(ref))
+
+
+def _bf16_bits(x: np.ndarray) -> np.ndarray:
+    return (x.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+
+
+@pytest.mark.parametrize("policy", [POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_COMPLEMENT])
+def test_role_log_scheduler_contract(policy):
+    """Every prefill id in [0, P) and decode id in [0, D) is claimed exactly once,
+    and (ticket policies) every role not forced by an exhausted pool follows the
+    SM's ticket pattern of sm_aware_assign (gpu_sim.hpp:114-131)."""
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=512, offset=1536, decode_ctx=[2048] * 8)
+    wl = build_workload(batch, device="cuda")
+    op = PodAttention(batch, options=pkg.PlanOptions(policy=policy))
+    log = op.enable_role_log()
+    op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+    torch.cuda.synchronize()
+    rec = log.view(-1, 8).cpu().numpy()
+    P, D = op.info.num_prefill_ctas, op.info.num_decode_ctas
+    assert sorted(rec[rec[:, 2] == 0, 3].tolist()) == list(range(P))
+    assert sorted(rec[rec[:, 2] == 1, 3].tolist()) == list(range(D))
+    if policy != POD_POLICY_COMPLEMENT:
+        pr, dr = op.info.prefill_ratio, op.info.decode_ratio
+        order = np.argsort(rec[:, 4])  # claim order
+        claimed = [0, 0]
+        for i in order:
+            op_i, ticket = rec[i, 2], rec[i, 1] % (pr + dr)
+            want = 0 if ticket < pr else 1
+            if op_i != want:  # switched: the wanted pool must have been exhausted by then
+                assert claimed[want] == (P if want == 0 else D)
+            claimed[op_i] += 1
+
+
+def test_fault_injection_is_detected():
+    """A wrong block-table entry must make the parity check fail (the checks bite)."""
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), decode_ctx=[256, 256])
+    wl = build_workload(batch, device="cuda")
+    ix = wl.page_indices.clone()
+    ix[[0, 20]] = ix[[20, 0]]  # swap a page of request 0 with one of request 1
+    bad = type(wl)(**{**wl.__dict__, "page_indices": ix})
+    _, _, out = _run(batch, wl=bad)
+    eo, _ = compare_decode(wl, out.o_decode.cpu().numpy(), out.lse_decode.cpu().numpy())
+    assert eo > O_TOL
+
+
+def test_full_size_c2_b64_sampled():
+    """BASELINE config 2 at full size (1K chunk at 16K + 64 decodes at 16K), checked
+    on sampled rows / heads / requests."""
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=1024, offset=15360, decode_ctx=[16384] * 64)
+    wl, _, out = _run(batch)
+    o_p, l_p = out.o_prefill.cpu().numpy(), out.lse_prefill.cpu().numpy()
+    for rows in ((0, 4), (1020, 1024)):
+        eo, el = compare_prefill(wl, o_p, l_p, kv_heads=[3], row_range=rows)
+        assert eo <= O_TOL and el <= LSE_TOL
+    eo, el = compare_decode(wl, out.o_decode.cpu().numpy(), out.lse_decode.cpu().numpy(), requests=[0, 63],
+                            kv_heads=[0, 7])
+    assert eo <= O_TOL and el <= LSE_TOL
+    assert torch.isfinite(out.o_prefill).all() and torch.isfinite(out.o_decode).all()
