@@ -66,55 +66,60 @@ def work(hq, hkv, chunk, off, b, ctx, d=128):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled every 2 ms (NVML) while the timed
+    phases run; falls back to nvidia-smi polling when NVML is unavailable."""
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = None
 
     def __enter__(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self._stop = threading.Event()
+
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for n, bit in bits.items():
+                            if r & bit:
+                                self.reasons.add(n)
+                    except Exception:
+                        pass
+                    self._stop.wait(0.002)
+
+            self._thread = threading.Thread(target=loop, daemon=True)
+            self._thread.start()
         except Exception:
-            self.proc = None
+            self._stop = None
         return self
 
     def __exit__(self, *a):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except Exception:
-                self.proc.kill()
-                out = ""
-            self.lines = [l for l in out.splitlines() if l.strip()]
+        if self._stop is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
 
     def summary(self):
-        sms, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
-            f = [x.strip() for x in l.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sms.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sms:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
-        sms.sort()
-        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
 
 
 # ----------------------------------------------------------- CPU baseline --
@@ -218,7 +223,8 @@ def run_pod(args, rank, world, local_rank):
     shape = shard.shape
     batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
     wl = build_workload(batch, device=dev, seed_q=42 + 1000 * rank, seed_kv=43 + 1000 * rank)
-    opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode)
+    opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode, precision=args.precision,
+                           decode_splits=args.decode_splits)
     op = PodAttention(batch, options=opts, device=local_rank)
     out = op.alloc_outputs()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -254,10 +260,10 @@ def run_pod(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     with sampler:
         t_fused, ms_fused = timed("fused", args.steps, args.warmup)
+        t_serial, _ = timed("serial", args.steps, args.warmup)
+        t_pf, _ = timed("prefill", args.steps, args.warmup) if chunk else (0.0, [])
+        t_dec, _ = timed("decode", args.steps, args.warmup) if b else (0.0, [])
     clocks = sampler.summary()
-    t_serial, _ = timed("serial", args.steps, args.warmup)
-    t_pf, _ = timed("prefill", args.steps, args.warmup) if chunk else (0.0, [])
-    t_dec, _ = timed("decode", args.steps, args.warmup) if b else (0.0, [])
 
     # e2e through the C ABI with HOST buffers (pinned): H2D of the step's queries, the
     # fused launch, D2H of the outputs (O + LSE).  The paged KV cache is device-resident state.
@@ -310,8 +316,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="pod", choices=["pod", "reference"])
-    ap.add_argument("--policy", type=int, default=0)
+    ap.add_argument("--policy", type=int, default=3)
     ap.add_argument("--tile-mode", type=int, default=1)
+    ap.add_argument("--precision", type=int, default=0, help="0: prefill P as bf16 hi+lo (default), 1: single bf16")
+    ap.add_argument("--decode-splits", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -406,7 +414,7 @@ def main():
         "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
                  "prefill_splits": info.prefill_splits, "decode_splits": info.decode_splits,
                  "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
-                 "policy": args.policy},
+                 "policy": args.policy, "prefill_p": "bf16 hi+lo" if args.precision == 0 else "bf16"},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": None,
                      "kernel": "pod_fused_kernel (+merge)", "peak_source": pk["source"]},

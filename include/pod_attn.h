@@ -117,8 +117,11 @@ enum {
     POD_POLICY_FIFTY_FIFTY = 0,  /* SmPolicy::FiftyFifty (gpu_sim.hpp:97-99)          */
     POD_POLICY_PROPORTIONAL = 1, /* SmPolicy::Proportional, gcd of PHYSICAL CTAs (:100-105) */
     POD_POLICY_CLAMPED = 2,      /* proportional, rounded to the per-SM slot count     */
-    POD_POLICY_COMPLEMENT = 3    /* bind from the roles resident on the SM:
+    POD_POLICY_COMPLEMENT = 3,   /* bind from the roles resident on the SM:
                                     prefill while < prefill_ratio prefill CTAs run there */
+    POD_POLICY_SLOTS = 4         /* 2 CTAs/SM, fixed 1:1: the first CTA resident on an SM
+                                    is the prefill slot (all 512 TMEM columns, two-block
+                                    ping-pong engine), the second streams decode */
 };
 
 enum {
@@ -134,7 +137,13 @@ typedef struct pod_options {
     int32_t split_wave_cap;  /* 0 = keep the tile config's value (2)                */
     int32_t decode_splits;   /* 0 = auto (fill the machine), else splits per (request, kv head) */
     const pod_tile_config* tile_override; /* non-NULL: use this TileConfig verbatim */
+    int32_t precision;       /* POD_PRECISION_* for the prefill P operand            */
 } pod_options;
+
+enum {
+    POD_PRECISION_SPLIT = 0, /* P = bf16 hi + bf16 lo (two PV MMAs): ~16-bit P, default */
+    POD_PRECISION_FAST = 1   /* P rounded to one bf16 (FlashAttention-style)            */
+};
 
 /* What the plan decided, for benches and tests. */
 typedef struct pod_plan_info {

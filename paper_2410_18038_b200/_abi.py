@@ -19,8 +19,10 @@ STATUS_NAMES = {
 
 POD_KV_HND, POD_KV_NHD = 0, 1
 POD_DTYPE_BF16, POD_DTYPE_FP16 = 0, 1
-POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT = 0, 1, 2, 3
+POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT, POD_POLICY_SLOTS = \
+    0, 1, 2, 3, 4
 POD_TILE_REFERENCE, POD_TILE_B200 = 0, 1
+POD_PRECISION_SPLIT, POD_PRECISION_FAST = 0, 1
 
 
 class pod_shape(C.Structure):
@@ -64,7 +66,8 @@ class pod_task(C.Structure):
 class pod_options(C.Structure):
     _fields_ = [("policy", C.c_int32), ("tile_mode", C.c_int32), ("ctas_per_sm", C.c_int32),
                 ("virtual_decode", C.c_int32), ("split_wave_cap", C.c_int32),
-                ("decode_splits", C.c_int32), ("tile_override", C.POINTER(pod_tile_config))]
+                ("decode_splits", C.c_int32), ("tile_override", C.POINTER(pod_tile_config)),
+                ("precision", C.c_int32)]
 
 
 class pod_plan_info(C.Structure):

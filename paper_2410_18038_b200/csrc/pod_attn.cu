@@ -44,9 +44,12 @@ constexpr uint32_t kOffQ = 0;
 constexpr uint32_t kOffK = kOffQ + kQBytes;                 // 2 stages
 constexpr uint32_t kOffV = kOffK + 2 * kKvStageBytes;       // 2 stages
 constexpr uint32_t kOffBar = kOffV + 2 * kKvStageBytes;     // 16 mbarriers
+// engine 2 keeps Q in TMEM: K/V stages only
+constexpr uint32_t kOffK2 = 0;
+constexpr uint32_t kOffV2 = kOffK2 + 2 * kKvStageBytes;
 constexpr uint32_t kOffTmemSlot = kOffBar + 128;
 constexpr uint32_t kOffDecBar = kOffBar + 160;              // 4 warps x 3 stages of decode mbarriers
-constexpr uint32_t kOffRole = kOffTmemSlot + 16;
+constexpr uint32_t kOffRole = kOffTmemSlot + 16;          // role[0..3]
 constexpr uint32_t kSmemBytes = kOffBar + 256;              // 98560 B -> 2 CTAs / SM
 static_assert(kOffDecBar + 12 * 8 <= kSmemBytes, "decode barriers");
 static_assert(kSmemBytes * 2 + 2048 <= 233472, "two CTAs must fit one SM");
@@ -57,6 +60,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
 struct RunParams {
+    const void* q_prefill;
     const void* q_decode;
     const void* k_pool;
     const void* v_pool;
@@ -86,6 +90,8 @@ struct RunParams {
     int32_t kv_layout;
     int32_t decode_splits;
     int32_t policy;
+    int32_t p_split;  // prefill P as bf16 hi + lo (two PV MMAs)
+    int32_t pad1;
     int64_t num_pages;
     float sl2;  // log2(e) / scale  (scale is the reference's divisor)
 };
@@ -107,6 +113,24 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     return *reinterpret_cast<float2*>(&d);
 }
 
+template <int kFmt>
+__device__ __forceinline__ uint32_t pack2(float x, float y) {
+    if constexpr (kFmt == 1) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+        return *reinterpret_cast<uint32_t*>(&h);
+    } else {
+        __half2 h = __floats2half2_rn(x, y);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+}
+template <int kFmt>
+__device__ __forceinline__ float2 unpack2(uint32_t w) {
+    if constexpr (kFmt == 1) {
+        return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+    } else {
+        return __half22float2(*reinterpret_cast<const __half2*>(&w));
+    }
+}
 // ============================================================ prefill ===
 template <int kFmt>
 __device__ __forceinline__ void prefill_issue_qk(uint32_t tmem_s, uint32_t sQ, uint32_t sK) {
@@ -124,12 +148,13 @@ __device__ __forceinline__ void prefill_issue_qk(uint32_t tmem_s, uint32_t sQ, u
 // 8 columns per K=16 step) and V (64 keys x 128 d, MN-major SW128) from smem.
 template <int kFmt>
 __device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint32_t sV,
-                                                 bool accumulate) {
+                                                 bool accumulate, bool split) {
     constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);
 #pragma unroll
     for (int kk = 0; kk < kKvTile / 16; ++kk) {
         const uint64_t b = ptx::sw128_desc(sV + kk * 2048, kKvTile * 128, 1024);
         ptx::umma_f16_ts(tmem_o, tmem_p + kk * 8, b, idesc, (accumulate || kk > 0) ? 1u : 0u);
+        if (split) ptx::umma_f16_ts(tmem_o, tmem_p + 32 + kk * 8, b, idesc, 1u);  // + P_lo V
     }
 }
 
@@ -273,7 +298,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                     ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
                     ptx::tc_fence_after();
                     prefill_issue_pv<kFmt>(tmem + kTmemO, tmem + kTmemS0 + st * kKvTile, sV + st * kKvStageBytes,
-                                           t > 0);
+                                           t > 0, p.p_split != 0);
                     ptx::umma_commit(b_pv + 8 * st);
                     ptx::umma_commit(b_vempty + 8 * st);
                     if (t + 2 < br.nt) {
@@ -351,29 +376,27 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                 const float factor = need ? ptx::ex2(m_run - m_new) : 1.f;
                 l_run *= factor;
                 m_run = m_use;
-                float pk[kKvTile / 2];  // packed 16-bit P pairs (bit patterns)
+                // P -> TMEM over the consumed S row (A operand of the TS MMA), in two
+                // 32-key halves: hi = round(p) in columns [0,32); with p_split also
+                // lo = round(p - hi) in [32,64), so hi + lo carries ~16 mantissa bits.
                 float2 lsum2 = make_float2(0.f, 0.f);
-                if (m_use == -INFINITY) {
+                const float neg_m = -m_use;
+                const bool live = m_use != -INFINITY;
 #pragma unroll
-                    for (int c = 0; c < kKvTile / 2; ++c) pk[c] = 0.f;
-                } else {
-                    const float neg_m = -m_use;
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t hi[16], lo[16];
 #pragma unroll
-                    for (int c = 0; c < kKvTile; c += 2) {
+                    for (int c = 0; c < 32; c += 2) {
                         // p = 2^(s * log2(e)/scale - m): one FFMA + one MUFU per score
-                        const float p0 = ptx::ex2(fmaf(s[c], p.sl2, neg_m));
-                        const float p1 = ptx::ex2(fmaf(s[c + 1], p.sl2, neg_m));
+                        const float p0 = live ? ptx::ex2(fmaf(s[32 * hf + c], p.sl2, neg_m)) : 0.f;
+                        const float p1 = live ? ptx::ex2(fmaf(s[32 * hf + c + 1], p.sl2, neg_m)) : 0.f;
                         lsum2 = fadd2(lsum2, make_float2(p0, p1));
-                        uint32_t w;
-                        if constexpr (kFmt == 1) {
-                            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-                            w = *reinterpret_cast<uint32_t*>(&h);
-                        } else {
-                            __half2 h = __floats2half2_rn(p0, p1);
-                            w = *reinterpret_cast<uint32_t*>(&h);
-                        }
-                        pk[c / 2] = __uint_as_float(w);
+                        hi[c / 2] = pack2<kFmt>(p0, p1);
+                        const float2 hv = unpack2<kFmt>(hi[c / 2]);
+                        lo[c / 2] = pack2<kFmt>(p0 - hv.x, p1 - hv.y);
                     }
+                    ptx::tmem_st16(s_addr + 16 * hf, hi);
+                    if (p.p_split) ptx::tmem_st16(s_addr + 32 + 16 * hf, lo);
                 }
                 l_run += lsum2.x + lsum2.y;
                 // Observe PV_{t-1} (keeps the pv barrier phases in order; required
@@ -394,7 +417,6 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                     }
                 }
                 // P row -> TMEM over the consumed S row (A operand of the TS MMA)
-                ptx::tmem_st32(s_addr, *reinterpret_cast<float(*)[32]>(&pk[0]));
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -422,6 +444,322 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
             if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
             ptx::tc_fence_before();
             g += br.nt;
+        }
+    }
+}
+
+// ================================================== prefill engine (2) ===
+// The prefill-slot CTA of an SM owns all 512 TMEM columns and runs two M-blocks
+// (A, B: 2 x 128 packed rows) in ping-pong over the same K/V tiles:
+//   TMEM  Q_A [0,64)  Q_B [64,128)  S_A [128,192)  S_B [192,256)  O_A [256,384)  O_B [384,512)
+// Q lives in TMEM (loaded once per item by the softmax threads), so both QK^T
+// and PV are TS-MMAs and shared memory only streams K/V (read once for 256 rows).
+// While the softmax warps work on block B the tensor core runs PV_A + QK_A of the
+// next tile, and vice versa.
+constexpr uint32_t kT2QA = 0, kT2QB = 64, kT2SA = 128, kT2SB = 192, kT2OA = 256, kT2OB = 384;
+constexpr uint32_t kTmemCols2 = 512;
+
+struct Prefill2State {
+    int g = 0;      // KV tiles issued (K/V stage = g & 1, phase = (g >> 1) & 1)
+    int na = 0;     // A-block tiles (s_full_A / p_full_A / pv_A phases)
+    int nb = 0;     // B-block tiles
+    int pairs = 0;  // block pairs (q_full phases)
+};
+
+template <int kFmt>
+__device__ __forceinline__ void issue_qk_ts(uint32_t tmem_s, uint32_t tmem_q, uint32_t sK) {
+    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kKvTile, 0);
+#pragma unroll
+    for (int kk = 0; kk < kHeadDim / 16; ++kk) {
+        const uint64_t b = ptx::sw128_desc(sK + (kk >> 2) * (kKvTile * 128) + (kk & 3) * 32u, 16, 1024);
+        ptx::umma_f16_ts(tmem_s, tmem_q + kk * 8, b, idesc, kk > 0 ? 1u : 0u);
+    }
+}
+
+template <int kFmt>
+__device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv, int cta_id,
+                              uint8_t* smem, uint32_t tmem, Prefill2State& ps) {
+    const PrefillCta job = p.pctas[cta_id];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t sbase = ptx::smem_u32(smem);
+    const uint32_t sK = sbase + kOffK2, sV = sbase + kOffV2;
+    const uint32_t bar0 = sbase + kOffBar;
+    const uint32_t b_qfull = bar0 + 0;
+    const uint32_t b_kfull = bar0 + 16, b_kempty = bar0 + 32;  // [2]
+    const uint32_t b_vfull = bar0 + 48, b_vempty = bar0 + 64;  // [2]
+    const uint32_t b_sfull = bar0 + 80;                        // [A, B]
+    const uint32_t b_pfull = bar0 + 96;                        // [A, B], 4 arrivals
+    const uint32_t b_pv = bar0 + 112;                          // [A, B]
+    const int G = p.group;
+    const int rpb = kMBlock / G;
+    const int nblocks = (job.rows + rpb - 1) / rpb;
+    const int npairs = (nblocks + 1) / 2;
+    const int pbeg = p.page_indptr[0];
+    const int npages = p.page_indptr[1] - pbeg;
+    const Prefill2State s0 = ps;
+    // all threads advance the shared counters identically
+    for (int pr = 0; pr < npairs; ++pr) {
+        const bool hasB = 2 * pr + 1 < nblocks;
+        const BlockRange ra = prefill_block(p, job, 2 * pr);
+        const int nt = hasB ? prefill_block(p, job, 2 * pr + 1).nt : ra.nt;
+        if (nt == 0) continue;
+        ps.g += nt;
+        ps.na += nt;
+        ps.nb += hasB ? nt : 0;
+        ps.pairs += 1;
+    }
+
+    if (warp == 4) {
+        // ------------------------------------------------ TMA producer --
+        if (lane == 0) {
+            int g = s0.g;
+            for (int pr = 0; pr < npairs; ++pr) {
+                const bool hasB = 2 * pr + 1 < nblocks;
+                const BlockRange ra = prefill_block(p, job, 2 * pr);
+                const int nt = hasB ? prefill_block(p, job, 2 * pr + 1).nt : ra.nt;
+                for (int t = 0; t <= nt && nt > 0; ++t) {
+                    if (t < nt) {
+                        const int gg = g + t, st = gg & 1;
+                        if (gg >= 2) ptx::mbar_wait(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
+                        ptx::mbar_arrive_expect_tx(b_kfull + 8 * st, kKvStageBytes);
+                        prefill_load_kv_tile(p, tmk, sK + st * kKvStageBytes, b_kfull + 8 * st,
+                                             ra.kt0 + t * kKvTile, job.kv_head, pbeg, npages);
+                    }
+                    if (t > 0) {
+                        const int gg = g + t - 1, st = gg & 1;
+                        if (gg >= 2) ptx::mbar_wait(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
+                        ptx::mbar_arrive_expect_tx(b_vfull + 8 * st, kKvStageBytes);
+                        prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
+                                             ra.kt0 + (t - 1) * kKvTile, job.kv_head, pbeg, npages);
+                    }
+                }
+                g += nt;
+            }
+        }
+    } else if (warp == 5) {
+        // -------------------------------------------------- MMA issuer --
+        if (lane == 0) {
+            int g = s0.g, na = s0.na, nb = s0.nb, pq = s0.pairs;
+            for (int pr = 0; pr < npairs; ++pr) {
+                const bool hasB = 2 * pr + 1 < nblocks;
+                const BlockRange ra = prefill_block(p, job, 2 * pr);
+                const int nt = hasB ? prefill_block(p, job, 2 * pr + 1).nt : ra.nt;
+                if (nt == 0) continue;
+                ptx::mbar_wait(b_qfull, pq & 1);
+                {  // tile 0: QK_A, QK_B
+                    const int st = g & 1;
+                    ptx::mbar_wait(b_kfull + 8 * st, (g >> 1) & 1);
+                    ptx::tc_fence_after();
+                    issue_qk_ts<kFmt>(tmem + kT2SA, tmem + kT2QA, sK + st * kKvStageBytes);
+                    ptx::umma_commit(b_sfull);
+                    if (hasB) {
+                        issue_qk_ts<kFmt>(tmem + kT2SB, tmem + kT2QB, sK + st * kKvStageBytes);
+                        ptx::umma_commit(b_sfull + 8);
+                    }
+                    ptx::umma_commit(b_kempty + 8 * st);
+                }
+                for (int t = 0; t < nt; ++t) {
+                    const int gg = g + t, st = gg & 1, s1 = (gg + 1) & 1;
+                    const bool more = t + 1 < nt;
+                    // block A: PV_A(t), then QK_A(t+1) into the same S/P columns (in-order pipe)
+                    ptx::mbar_wait(b_pfull, (na + t) & 1);
+                    ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
+                    ptx::tc_fence_after();
+                    prefill_issue_pv<kFmt>(tmem + kT2OA, tmem + kT2SA, sV + st * kKvStageBytes, t > 0,
+                                           p.p_split != 0);
+                    ptx::umma_commit(b_pv);
+                    if (more) {
+                        ptx::mbar_wait(b_kfull + 8 * s1, ((gg + 1) >> 1) & 1);
+                        ptx::tc_fence_after();
+                        issue_qk_ts<kFmt>(tmem + kT2SA, tmem + kT2QA, sK + s1 * kKvStageBytes);
+                        ptx::umma_commit(b_sfull);
+                    }
+                    if (hasB) {
+                        ptx::mbar_wait(b_pfull + 8, (nb + t) & 1);
+                        ptx::tc_fence_after();
+                        prefill_issue_pv<kFmt>(tmem + kT2OB, tmem + kT2SB, sV + st * kKvStageBytes, t > 0,
+                                               p.p_split != 0);
+                        ptx::umma_commit(b_pv + 8);
+                        if (more) {
+                            issue_qk_ts<kFmt>(tmem + kT2SB, tmem + kT2QB, sK + s1 * kKvStageBytes);
+                            ptx::umma_commit(b_sfull + 8);
+                        }
+                    }
+                    ptx::umma_commit(b_vempty + 8 * st);
+                    if (more) ptx::umma_commit(b_kempty + 8 * s1);
+                }
+                g += nt;
+                na += nt;
+                nb += hasB ? nt : 0;
+                ++pq;
+            }
+        }
+    } else {
+        // ------------------------------------------ softmax (128 threads) --
+        const int m = tid;  // TMEM lane == M row of both blocks
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+        int na = s0.na, nb = s0.nb;
+        const uint16_t* qsrc = static_cast<const uint16_t*>(p.q_prefill);
+        for (int pr = 0; pr < npairs; ++pr) {
+            const bool hasB = 2 * pr + 1 < nblocks;
+            const BlockRange br[2] = {prefill_block(p, job, 2 * pr),
+                                      hasB ? prefill_block(p, job, 2 * pr + 1) : prefill_block(p, job, 2 * pr)};
+            const int nt = hasB ? br[1].nt : br[0].nt;
+            const int nblk = hasB ? 2 : 1;
+            int my_r[2], vis[2];
+            bool row_ok[2];
+            float* orow[2];
+            float* lrow[2];
+            const int qhead = job.kv_head * G + m % G;
+#pragma unroll
+            for (int bi = 0; bi < 2; ++bi) {
+                my_r[bi] = br[bi].r0 + m / G;
+                row_ok[bi] = bi < nblk && (m / G) < br[bi].nrows;
+                vis[bi] = p.offset + my_r[bi];
+                if (job.n_splits == 1) {
+                    orow[bi] = p.o_prefill + (static_cast<size_t>(my_r[bi]) * p.hq + qhead) * kHeadDim;
+                    lrow[bi] = p.lse_prefill + static_cast<size_t>(my_r[bi]) * p.hq + qhead;
+                } else {
+                    const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r[bi]) * p.hq + qhead;
+                    orow[bi] = p.ppart_o + row * kHeadDim;
+                    lrow[bi] = p.ppart_lse + row;
+                }
+            }
+            if (nt == 0) {
+#pragma unroll
+                for (int bi = 0; bi < 2; ++bi)
+                    if (row_ok[bi]) {
+                        for (int c = 0; c < kHeadDim; c += 4)
+                            *reinterpret_cast<float4*>(orow[bi] + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                        *lrow[bi] = -INFINITY;
+                    }
+                continue;
+            }
+            // ---- Q rows -> TMEM (A operand of QK^T), zero rows past the chunk
+#pragma unroll
+            for (int bi = 0; bi < 2; ++bi) {
+                if (bi >= nblk) break;
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(
+                    qsrc + (static_cast<size_t>(my_r[bi]) * p.hq + qhead) * kHeadDim);
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    float qv[32];
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4) {
+                        const uint4 v = row_ok[bi] ? __ldg(reinterpret_cast<const uint4*>(src + 32 * hf + c))
+                                                   : make_uint4(0u, 0u, 0u, 0u);
+                        qv[c] = __uint_as_float(v.x);
+                        qv[c + 1] = __uint_as_float(v.y);
+                        qv[c + 2] = __uint_as_float(v.z);
+                        qv[c + 3] = __uint_as_float(v.w);
+                    }
+                    ptx::tmem_st32(lane_base + (bi ? kT2QB : kT2QA) + 32 * hf, qv);
+                }
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(b_qfull);
+            float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+            for (int t = 0; t < nt; ++t) {
+                const int kb = br[0].kt0 + t * kKvTile;
+#pragma unroll 1
+                for (int bi = 0; bi < nblk; ++bi) {
+                    const int n = bi ? nb + t : na + t;  // this block's tile count (barrier phases)
+                    const uint32_t s_addr = lane_base + (bi ? kT2SB : kT2SA);
+                    const uint32_t o_addr = lane_base + (bi ? kT2OB : kT2OA);
+                    ptx::mbar_wait(b_sfull + 8 * bi, n & 1);
+                    ptx::tc_fence_after();
+                    float s[kKvTile];
+                    ptx::tmem_ld32(s_addr, *reinterpret_cast<float(*)[32]>(&s[0]));
+                    ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+                    ptx::tmem_wait_ld();
+                    const int lo = max(job.kv_begin - kb, 0);
+                    const int hi = row_ok[bi] ? min(min(job.kv_end, vis[bi] + 1) - kb, kKvTile) : 0;
+                    if (!__all_sync(0xffffffffu, lo == 0 && hi == kKvTile)) {
+#pragma unroll
+                        for (int c = 0; c < kKvTile; ++c)
+                            if (c < lo || c >= hi) s[c] = -INFINITY;
+                    }
+                    float tmax = s[0];
+#pragma unroll
+                    for (int c = 1; c < kKvTile; c += 2) tmax = fmaxf(tmax, fmaxf(s[c], s[min(c + 1, kKvTile - 1)]));
+                    const float mr = m_run[bi];
+                    const float m_new = fmaxf(mr, tmax * p.sl2);
+                    const bool need = m_new > mr + 8.f;
+                    const float m_use = need ? m_new : mr;
+                    const float factor = need ? ptx::ex2(mr - m_new) : 1.f;
+                    l_run[bi] *= factor;
+                    m_run[bi] = m_use;
+                    float2 lsum2 = make_float2(0.f, 0.f);
+                    const float neg_m = -m_use;
+                    const bool live = m_use != -INFINITY;
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        uint32_t hiv[16], lov[16];
+#pragma unroll
+                        for (int c = 0; c < 32; c += 2) {
+                            const float p0 = live ? ptx::ex2(fmaf(s[32 * hf + c], p.sl2, neg_m)) : 0.f;
+                            const float p1 = live ? ptx::ex2(fmaf(s[32 * hf + c + 1], p.sl2, neg_m)) : 0.f;
+                            lsum2 = fadd2(lsum2, make_float2(p0, p1));
+                            hiv[c / 2] = pack2<kFmt>(p0, p1);
+                            if (p.p_split) {
+                                const float2 hv = unpack2<kFmt>(hiv[c / 2]);
+                                lov[c / 2] = pack2<kFmt>(p0 - hv.x, p1 - hv.y);
+                            }
+                        }
+                        ptx::tmem_st16(s_addr + 16 * hf, hiv);
+                        if (p.p_split) ptx::tmem_st16(s_addr + 32 + 16 * hf, lov);
+                    }
+                    l_run[bi] += lsum2.x + lsum2.y;
+                    if (t > 0) {  // observe PV(t-1) of this block; rescale its O when the max moved
+                        ptx::mbar_wait(b_pv + 8 * bi, (n - 1) & 1);
+                        ptx::tc_fence_after();
+                        if (__any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+                            for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+                                float o[32];
+                                ptx::tmem_ld32(o_addr + ch * 32, o);
+                                ptx::tmem_wait_ld();
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) o[c] *= factor;
+                                ptx::tmem_st32(o_addr + ch * 32, o);
+                            }
+                        }
+                    }
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(b_pfull + 8 * bi);
+                }
+            }
+            // ------------------------------------------------- epilogue --
+#pragma unroll 1
+            for (int bi = 0; bi < nblk; ++bi) {
+                const int n = (bi ? nb : na) + nt - 1;
+                ptx::mbar_wait(b_pv + 8 * bi, n & 1);
+                ptx::tc_fence_after();
+                const uint32_t o_addr = lane_base + (bi ? kT2OB : kT2OA);
+                const float inv = l_run[bi] > 0.f ? 1.f / l_run[bi] : 0.f;
+#pragma unroll 1
+                for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+                    float o[32];
+                    ptx::tmem_ld32(o_addr + ch * 32, o);
+                    ptx::tmem_wait_ld();
+                    if (row_ok[bi]) {
+#pragma unroll
+                        for (int c = 0; c < 32; c += 4)
+                            *reinterpret_cast<float4*>(orow[bi] + ch * 32 + c) =
+                                make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv);
+                    }
+                }
+                if (row_ok[bi])
+                    *lrow[bi] = l_run[bi] > 0.f ? (m_run[bi] + ptx::lg2(l_run[bi])) * kLn2 : -INFINITY;
+            }
+            ptx::tc_fence_before();
+            na += nt;
+            nb += hasB ? nt : 0;
         }
     }
 }
@@ -463,24 +801,6 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(addr));
-}
-template <int kFmt>
-__device__ __forceinline__ uint32_t pack2(float x, float y) {
-    if constexpr (kFmt == 1) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
-        return *reinterpret_cast<uint32_t*>(&h);
-    } else {
-        __half2 h = __floats2half2_rn(x, y);
-        return *reinterpret_cast<uint32_t*>(&h);
-    }
-}
-template <int kFmt>
-__device__ __forceinline__ float2 unpack2(uint32_t w) {
-    if constexpr (kFmt == 1) {
-        return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
-    } else {
-        return __half22float2(*reinterpret_cast<const __half2*>(&w));
-    }
 }
 // Byte offset of (row, 16-byte chunk c in 0..15) of a 16 x 128 page stored as two
 // 128B-swizzled column halves of 2 KB (TMA SWIZZLE_128B boxes of 64 elements).
@@ -799,17 +1119,29 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sbase = ptx::smem_u32(smem);
+    const uint32_t sm = ptx::smid();
+    const bool slots = p.policy == POD_POLICY_SLOTS;
     if (tid == 0) {
         if (sbase & 1023u) __trap();  // SW128 atoms need a 1024-aligned base
-        for (int i = 0; i < 16; ++i) ptx::mbar_init(sbase + kOffBar + 8 * i, (i == 12 || i == 13) ? kPrefillWarps : 1);
+        // p_full (12, 13) get one arrival per softmax warp; so does engine 2's q_full (0),
+        // which engine 1 fills by TMA (expect_tx, one arrival)
+        for (int i = 0; i < 16; ++i)
+            ptx::mbar_init(sbase + kOffBar + 8 * i, (i == 12 || i == 13 || (i == 0 && slots)) ? kPrefillWarps : 1);
         for (int i = 0; i < kDecodeWarps * kDecStages; ++i) ptx::mbar_init(sbase + kOffDecBar + 8 * i, 1);
         ptx::fence_mbar_init();
+        // POD_POLICY_SLOTS: the first CTA resident on this SM takes the prefill slot
+        role[3] = slots ? static_cast<int>(atomicAdd(&p.ctr->sm_slot[sm], 1u)) : 0;
     }
-    // Every CTA allocates and relinquishes: on sm_100 a second CTA of a tcgen05
-    // kernel is only co-scheduled on an SM once the resident one has given up
-    // its TMEM allocation permit (decode-only launches included).
-    if (warp == 0) {
-        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), kTmemCols);
+    __syncthreads();
+    const int my_slot = role[3];
+    const bool prefill_slot = !slots || my_slot == 0;
+    // TMEM: the slots policy gives the prefill slot the whole SM (512 columns);
+    // ticket policies give every CTA 256.  Every CTA that allocates relinquishes
+    // its permit at once: on sm_100 a second CTA of a tcgen05 kernel is only
+    // co-scheduled on an SM after the resident one has relinquished.
+    const uint32_t ncols = slots ? (p.num_pctas > 0 ? kTmemCols2 : 32u) : kTmemCols;
+    if (warp == 0 && prefill_slot) {
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), ncols);
         ptx::tmem_relinquish();
     }
     if (warp == 4 && lane == 0) {
@@ -820,14 +1152,38 @@ __global__ void __launch_bounds__(kThreads, 2)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t sm = ptx::smid();
+    const uint32_t tmem = prefill_slot ? *tmem_slot : 0u;
     PrefillState ps;
+    Prefill2State ps2;
     int dpos = 0;
     while (true) {
         if (tid == 0) {
-            int32_t slot;
-            const int2 w = claim_item(p, sm, &slot);
+            int32_t slot = -1;
+            int2 w;
+            if (slots) {
+                // prefill slot: prefill items first, then decode; decode slot: decode only
+                int op = prefill_slot ? 0 : 1;
+                int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
+                if (op == 0 && id >= p.num_pctas) {
+                    op = 1;
+                    id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[1], 1u));
+                }
+                if (id >= (op == 0 ? p.num_pctas : p.num_dctas)) op = -1;
+                w = make_int2(op, id);
+                if (p.role_log && op >= 0) {
+                    slot = static_cast<int32_t>(atomicAdd(&p.ctr->arrival, 1u));
+                    int32_t* rec = p.role_log + 8 * slot;
+                    rec[0] = static_cast<int32_t>(sm);
+                    rec[1] = my_slot;
+                    rec[2] = op;
+                    rec[3] = id;
+                    rec[4] = slot;
+                    rec[5] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
+                    rec[7] = static_cast<int32_t>(blockIdx.x);
+                }
+            } else {
+                w = claim_item(p, sm, &slot);
+            }
             role[0] = w.x;
             role[1] = w.y;
             role[2] = slot;
@@ -836,10 +1192,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int op = role[0], id = role[1], slot = role[2];
         __syncthreads();  // role[] is rewritten by the next claim
         if (op < 0) break;
-        if (op == 0)
-            prefill_item<kFmt>(p, &tmq, &tmk, &tmv, id, smem, tmem, ps);
-        else
+        if (op == 0) {
+            if (slots)
+                prefill_item2<kFmt>(p, &tmk, &tmv, id, smem, tmem, ps2);
+            else
+                prefill_item<kFmt>(p, &tmq, &tmk, &tmv, id, smem, tmem, ps);
+        } else {
             decode_item<G, kFmt>(p, &tmk, &tmv, id, smem, dpos);
+        }
         ptx::tc_fence_before();
         __syncthreads();
         ptx::tc_fence_after();
@@ -848,9 +1208,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (slot >= 0) p.role_log[8 * slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
         }
     }
-    if (warp == 0) {
+    if (warp == 0 && prefill_slot) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, kTmemCols);
+        ptx::tmem_dealloc(tmem, ncols);
     }
     if (tid == 0) {
         __threadfence();
@@ -861,6 +1221,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (uint32_t i = 0; i < n; ++i) {
                 p.ctr->sm_ctr[i] = 0;
                 p.ctr->running_prefill[i] = 0;
+                p.ctr->sm_slot[i] = 0;
             }
             p.ctr->cta_assign[0] = 0;
             p.ctr->cta_assign[1] = 0;
@@ -981,11 +1342,12 @@ pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_
     return POD_OK;
 }
 
-RunParams make_params(const pod_plan* plan, const void* q_decode, const void* k_pool, const void* v_pool,
+RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q_decode, const void* k_pool, const void* v_pool,
                       int64_t num_pages, const int32_t* indptr, const int32_t* indices, float* o_prefill,
                       float* lse_prefill, float* o_decode, float* lse_decode, void* workspace) {
     RunParams p{};
     uint8_t* ws = static_cast<uint8_t*>(workspace);
+    p.q_prefill = q_prefill;
     p.q_decode = q_decode;
     p.k_pool = k_pool;
     p.v_pool = v_pool;
@@ -1015,6 +1377,7 @@ RunParams make_params(const pod_plan* plan, const void* q_decode, const void* k_
     p.kv_layout = plan->batch.kv_layout;
     p.decode_splits = static_cast<int32_t>(plan->decode_splits);
     p.policy = plan->opts.policy;
+    p.p_split = plan->opts.precision == POD_PRECISION_FAST ? 0 : 1;
     p.num_pages = num_pages;
     p.sl2 = static_cast<float>(1.4426950408889634 / plan->shape.scale);
     return p;
@@ -1045,12 +1408,13 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
         cudaFuncSetAttribute(pod_fused_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         attr_done = true;
     }
-    const int slots = 2 * plan->dev.num_sms;  // resident CTAs of the persistent grid
+    const int nsm = plan->dev.num_sms;
     auto launch = [&](const RunParams& q) {
         const int items = q.num_pctas + q.num_dctas;
+        int grid = std::min(items, 2 * nsm);  // persistent: 2 resident CTAs per SM
+        if (q.policy == POD_POLICY_SLOTS && q.num_dctas == 0) grid = std::min(items, nsm);  // prefill slots only
         if (items > 0)
-            pod_fused_kernel<G, kFmt><<<std::min(items, slots), kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v,
-                                                                                         maps.dk, maps.dv);
+            pod_fused_kernel<G, kFmt><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk, maps.dv);
     };
     if (mode == 0) {
         launch(p);
@@ -1111,7 +1475,7 @@ pod_status run_mode(const pod_plan* plan, int mode, const void* q_prefill, const
     Maps maps;
     st = make_maps(plan, q_prefill, k_pool, v_pool, num_pages, &maps);
     if (st != POD_OK) return st;
-    RunParams p = make_params(plan, q_decode, k_pool, v_pool, num_pages, indptr, indices, o_prefill,
+    RunParams p = make_params(plan, q_prefill, q_decode, k_pool, v_pool, num_pages, indptr, indices, o_prefill,
                               lse_prefill, o_decode, lse_decode, workspace);
     if (mode == 2) p.num_dctas = 0;
     if (mode == 3) p.num_pctas = 0;

@@ -52,6 +52,7 @@ struct SchedCounters {
     uint32_t done;
     uint32_t arrival;
     uint32_t running_prefill[kMaxSms];  // POD_POLICY_COMPLEMENT: prefill CTAs resident per SM
+    uint32_t sm_slot[kMaxSms];          // POD_POLICY_SLOTS: CTAs that have arrived on each SM
 };
 
 struct WorkspaceLayout {

@@ -305,6 +305,10 @@ void scheduler_ratio(pod_plan& p) {
         p.prefill_ratio = g > 0 ? P / g : (P > 0 ? 1 : 0);
         p.decode_ratio = g > 0 ? D / g : (D > 0 ? 1 : 0);
         if (p.prefill_ratio == 0 && p.decode_ratio == 0) p.prefill_ratio = 1;
+    } else if (p.opts.policy == POD_POLICY_SLOTS) {
+        // fixed 1:1 per SM: one prefill slot, one decode slot (2 CTAs/SM)
+        p.prefill_ratio = 1;
+        p.decode_ratio = 1;
     } else if (p.opts.policy == POD_POLICY_COMPLEMENT) {
         // one prefill CTA per SM (2 slots): the other slot streams decode
         p.prefill_ratio = P > 0 ? 1 : 0;
@@ -356,7 +360,9 @@ pod_tile_config b200_tile_config(const pod_plan& p) {
     // kernel's KV tile is 64 keys.  Two CTAs per SM (smem ~112 KB each).
     pod_tile_config c = make_tile_config(2);
     const int group = p.shape.num_q_heads / p.shape.num_kv_heads;
-    c.prefill_tile_q = std::max(1, pod::kMBlock / group);
+    // slots policy: two 128-row M-blocks per prefill item (ping-pong engine)
+    const int rows = (p.opts.policy == POD_POLICY_SLOTS ? 2 : 1) * pod::kMBlock;
+    c.prefill_tile_q = std::max(1, rows / group);
     c.tile_kv = pod::kKvTile;
     c.shared_mem_per_cta = static_cast<double>(pod::fused_smem_bytes());
     c.virtual_decode = 1;
@@ -411,13 +417,14 @@ void pod_device_reference_default(pod_device* out) {
 
 void pod_options_default(pod_options* out) {
     std::memset(out, 0, sizeof(*out));
-    out->policy = POD_POLICY_FIFTY_FIFTY;
+    out->policy = POD_POLICY_COMPLEMENT;
     out->tile_mode = POD_TILE_B200;
     out->ctas_per_sm = 0;
     out->virtual_decode = -1;
     out->split_wave_cap = 0;
     out->decode_splits = 0;
     out->tile_override = nullptr;
+    out->precision = POD_PRECISION_SPLIT;
 }
 
 pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const pod_device* dev,

@@ -216,13 +216,14 @@ class WorkDecomposition:
 
 @dataclass
 class PlanOptions:
-    policy: int = _abi.POD_POLICY_FIFTY_FIFTY
+    policy: int = _abi.POD_POLICY_COMPLEMENT
     tile_mode: int = _abi.POD_TILE_B200
     ctas_per_sm: int = 0
     virtual_decode: int = -1
     split_wave_cap: int = 0
     decode_splits: int = 0
     tile_override: Optional[TileConfig] = None
+    precision: int = _abi.POD_PRECISION_SPLIT
 
 
 def _task(t) -> CtaTask:
@@ -244,6 +245,7 @@ class Plan:
         o.policy, o.tile_mode, o.ctas_per_sm = options.policy, options.tile_mode, options.ctas_per_sm
         o.virtual_decode, o.split_wave_cap, o.decode_splits = (options.virtual_decode, options.split_wave_cap,
                                                               options.decode_splits)
+        o.precision = options.precision
         tc = None
         if options.tile_override is not None:
             tc = options.tile_override._c()

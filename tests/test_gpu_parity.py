@@ -13,8 +13,8 @@ import torch
 import paper_2410_18038_b200 as pkg
 from oracle import pyoracle as O
 from paper_2410_18038_b200._abi import (POD_DTYPE_FP16, POD_KV_NHD, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT,
-                                        POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_TILE_B200,
-                                        POD_TILE_REFERENCE)
+                                        POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_SLOTS,
+                                        POD_PRECISION_FAST, POD_TILE_B200, POD_TILE_REFERENCE)
 from paper_2410_18038_b200.workload import build_workload, make_batch
 from tests.common import LSE_TOL, O_TOL, compare_decode, compare_prefill
 
@@ -69,10 +69,23 @@ def test_matches_oracle(name, mode):
     batch = make_batch(pkg.ModelShape(hq, hkv, 128, SCALE), chunk=chunk, offset=off, decode_ctx=dec)
     wl, _, out = _run(batch, mode)
     _check(wl, out)
+    # the two-block ping-pong prefill engine of the slots policy
+    wl, _, out = _run(batch, mode, options=pkg.PlanOptions(policy=POD_POLICY_SLOTS), wl=wl)
+    _check(wl, out)
+
+
+def test_fast_precision_bf16_p_within_loose_bound():
+    """POD_PRECISION_FAST rounds P to one bf16 (FlashAttention-style); its error is
+    bounded by bf16's relative precision, 2^-8, not by the 2e-3 default bar."""
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=96, offset=160, decode_ctx=[300, 77])
+    wl, _, out = _run(batch, options=pkg.PlanOptions(precision=POD_PRECISION_FAST))
+    eo, el = compare_prefill(wl, out.o_prefill.cpu().numpy(), out.lse_prefill.cpu().numpy())
+    assert eo <= 2.0 ** -8 and el <= LSE_TOL
 
 
 @pytest.mark.parametrize("policy", [POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED,
-                                    POD_POLICY_COMPLEMENT])
+                                    POD_POLICY_COMPLEMENT, POD_POLICY_SLOTS])
 def test_policies_and_reference_tiles(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=200, offset=37, decode_ctx=[500, 33, 90])

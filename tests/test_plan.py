@@ -262,15 +262,20 @@ def test_plan_ratio_policies():
 
 
 def test_b200_plan_lowering():
-    """B200 tile mode: one 128-row M-block per prefill CTA; decode CTAs cover each
-    (request, kv head) with 4 virtual warps whose ranges are the reference's
-    virtual tasks when decode_splits = 1."""
+    """B200 tile mode: one 128-row M-block per prefill item (two for the slots
+    policy's ping-pong engine); decode items cover each (request, kv head) with
+    4 virtual warps whose ranges are the reference's virtual tasks when
+    decode_splits = 1."""
+    from paper_2410_18038_b200._abi import POD_POLICY_FIFTY_FIFTY, POD_POLICY_SLOTS
     shape = ModelShape(32, 8, 128, math.sqrt(128))
     b = HybridBatchSpec(prefill=PrefillSpec(1024, 16384, 15360), decodes=[DecodeSpec(16384)] * 64, shape=shape)
-    p = Plan(b, GpuSpec.b200(), PlanOptions(tile_mode=POD_TILE_B200, decode_splits=1))
-    i = p.info()
+    i = Plan(b, GpuSpec.b200(), PlanOptions(tile_mode=POD_TILE_B200, policy=POD_POLICY_FIFTY_FIFTY)).info()
     assert i.config.prefill_tile_q * shape.group_size() == 128
     assert i.num_prefill_ctas == i.num_prefill_tasks == 32 * 8 * i.prefill_splits
+    p = Plan(b, GpuSpec.b200(), PlanOptions(tile_mode=POD_TILE_B200, decode_splits=1, policy=POD_POLICY_SLOTS))
+    i = p.info()
+    assert i.config.prefill_tile_q * shape.group_size() == 256
+    assert i.num_prefill_ctas == i.num_prefill_tasks == 16 * 8 * i.prefill_splits
     assert i.num_decode_tasks == 64 * 8 * 4 and i.num_decode_ctas == 64 * 8
     wd = p.tasks()
     for t in wd.decode_tasks[:16]:

@@ -23,7 +23,8 @@ def run_case(name):
     shape = pkg.ModelShape(c["hq"], c["hkv"], 128, 128 ** 0.5)
     batch = make_batch(shape, chunk=c["chunk"], offset=c["offset"], decode_ctx=c["dec"])
     wl = build_workload(batch, device="cuda")
-    opts = pkg.PlanOptions(tile_mode=c.get("tile_mode", 1))
+    import os
+    opts = pkg.PlanOptions(tile_mode=c.get("tile_mode", 1), policy=int(os.environ.get("POD_POLICY", "3")))
     op = PodAttention(batch, options=opts)
     info = op.info
     res = {"P": info.num_prefill_ctas, "D": info.num_decode_ctas, "splits": info.prefill_splits,

@@ -24,17 +24,18 @@ def main():
     ap.add_argument("--config", default="c2_b64")
     ap.add_argument("--mode", default="fused")
     ap.add_argument("--iters", type=int, default=3)
-    ap.add_argument("--policy", type=int, default=0)
+    ap.add_argument("--policy", type=int, default=3)
     ap.add_argument("--tile-mode", type=int, default=1)
     ap.add_argument("--decode-splits", type=int, default=0)
     ap.add_argument("--roles", default="")
+    ap.add_argument("--precision", type=int, default=0)
     a = ap.parse_args()
     hq, hkv, chunk, off, b, ctx = CONFIGS[a.config]
     shape = pkg.ModelShape(hq, hkv, 128, math.sqrt(128))
     batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
     wl = build_workload(batch, device="cuda")
     op = PodAttention(batch, options=pkg.PlanOptions(policy=a.policy, tile_mode=a.tile_mode,
-                                                     decode_splits=a.decode_splits))
+                                                     decode_splits=a.decode_splits, precision=a.precision))
     log = op.enable_role_log() if a.roles else None
     out = op.alloc_outputs()
     for _ in range(a.iters):
