@@ -824,16 +824,42 @@ __device__ __forceinline__ void decode_issue_page(const RunParams& p, const CUte
     }
 }
 
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+// A-operand mma: D (16 x 8) += A (16 x 16, four regs) * B (16 x 8).
+template <int kFmt>
+__device__ __forceinline__ void mma16816a(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    if constexpr (kFmt == 1)
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+    else
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
 // One physical decode CTA: 4 warps = 4 virtual decode CTAs over
 // split_ranges(kv_end - kv_begin, 4) (work_decomp.hpp:179-197, semantics of
 // decode_attention_splitk, attention.hpp:240-292).  Each warp streams its pages
-// (K and V head-pages, 4 KB each) through its own 3-stage TMA ring, keeps the
-// online-softmax statistics of head row g = lane/4 (quad shuffles), and the 4
+// (K and V head-pages, 4 KB each) through its own 3-stage TMA ring and computes
+// in the transposed form  S^T = K Q^T  and  O^T += V^T P^T  (mma.sync m16n8k16):
+// the 16 keys of a page are the M rows and the G <= 8 query heads the N columns,
+// so a page costs 8 MMAs for the scores and 16 for P V (P split into bf16 hi + lo).
+// Lane (g, t) = (lane / 4, lane % 4) holds scores of keys g, g + 8 for heads
+// 2t, 2t + 1; per-head max / sum are shuffle reductions over g.  The 4 warp
 // partials are LSE-merged through shared memory at the end.
 template <int G, int kFmt>
 __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUtensorMap* tv, int cta_id,
                             uint8_t* smem, int& dpos) {
-    static_assert(G <= 8, "decode rows: G query heads of one KV head (<= 8)");
+    static_assert(G <= 8, "decode: G query heads of one KV head are the N = 8 MMA columns");
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     if (warp >= kDecodeWarps) return;
@@ -843,35 +869,35 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
     const int wb = job.kv_begin + warp * base + min(warp, rem);
     const int we = wb + base + (warp < rem ? 1 : 0);
     const int h = job.kv_head;
-    const int gq = lane >> 2, tq = lane & 3;  // mma fragment row (head) / column pair
+    const int gq = lane >> 2, tq = lane & 3;
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t ring = sbase + warp * kDecWarpBytes;
     const uint32_t bars = sbase + kOffDecBar + warp * (kDecStages * 8);
+    const bool h0ok = 2 * tq < G, h1ok = 2 * tq + 1 < G;  // this lane's two head columns exist
 
-    // A fragments of Q (rows = heads, zero above G): per 16-d k-step, cols 2t..2t+1 and +8
+    // B fragments of Q^T (N = heads): head gq, d = 16 ks + 2t (+8); zero for heads >= G
     using elem_t = uint16_t;
-    uint32_t qa[8][2];
+    uint32_t qb[8][2];
     {
         const elem_t* q = static_cast<const elem_t*>(p.q_decode) +
                           (static_cast<size_t>(job.request) * p.hq + h * G + gq) * kHeadDim;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-            qa[ks][0] = gq < G ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 2 * tq) : 0u;
-            qa[ks][1] = gq < G ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 8 + 2 * tq) : 0u;
+            qb[ks][0] = gq < G ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 2 * tq) : 0u;
+            qb[ks][1] = gq < G ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 8 + 2 * tq) : 0u;
         }
     }
-    float m = -INFINITY, l = 0.f;  // row gq statistics (log2 domain); l is this lane's partial
-    float o[16][4];                // O fragments: 16 n-tiles of 8 d (rows >= 8 stay zero)
+    float m0 = -INFINITY, m1 = -INFINITY;  // running max of heads 2t, 2t+1 (log2 domain)
+    float l0 = 0.f, l1 = 0.f;              // this lane's partial sums (keys g, g+8)
+    float o[8][4];                         // O^T fragments: d-tile md, rows d = 16md + g (+8), cols heads 2t, 2t+1
 #pragma unroll
-    for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
 
     const int32_t* pidx = p.page_indices + p.page_indptr[job.page_row];
     const int pg0 = wb >> 4;
     const int npg = we > wb ? ((we - 1) >> 4) - pg0 + 1 : 0;
-    // page-table cache: lane j holds the physical id of page (cache_base + j)
     int cache_base = 0;
     int cached = (lane < npg) ? __ldg(pidx + pg0 + lane) : 0;
-    // ring slot of this warp's n-th page overall: n % kDecStages, phase (n / kDecStages) & 1
 #pragma unroll
     for (int j = 0; j < kDecStages; ++j) {
         const int phys = __shfl_sync(0xffffffffu, cached, j);
@@ -879,68 +905,65 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
         if (lane == 0 && j < npg) decode_issue_page(p, tk, tv, ring + st * kDecStageBytes, bars + 8 * st, h, phys);
     }
     __syncwarp();
-    // ldmatrix row/chunk roles of this lane
-    const int lm = lane >> 3, lr = lane & 7;
+    const int lm = lane >> 3, lr = lane & 7;  // ldmatrix: matrix lm, row lr
     for (int i = 0; i < npg; ++i) {
         const int n = dpos + i;
         const int st = n % kDecStages;
         ptx::mbar_wait(bars + 8 * st, (n / kDecStages) & 1);
         const uint32_t kst = ring + st * kDecStageBytes;
         const uint32_t vst = kst + kDecPageBytes;
-        // ---- S = Q K^T for the page's 16 keys (2 n-tiles of 8)
-        float sc[2][4];
+        // ---- S^T (16 keys x 8 heads) = K Q^T: one MMA per 16-d k-step
+        float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-            sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-            const int key = nt * 8 + lr;
-#pragma unroll
-            for (int kp = 0; kp < 4; ++kp) {  // two k-steps per ldmatrix.x4
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4(kst + page_off(key, 4 * kp + lm), b0, b1, b2, b3);
-                mma16816<kFmt>(sc[nt], qa[2 * kp][0], qa[2 * kp][1], b0, b1);
-                mma16816<kFmt>(sc[nt], qa[2 * kp + 1][0], qa[2 * kp + 1][1], b2, b3);
-            }
+        for (int ks = 0; ks < 8; ++ks) {
+            uint32_t a[4];  // keys 0-7 / 8-15 x d 16ks..+7 / +8..+15
+            ldsm_x4(kst + page_off((lm & 1) * 8 + lr, 2 * ks + (lm >> 1)), a[0], a[1], a[2], a[3]);
+            mma16816a<kFmt>(sc, a, qb[ks][0], qb[ks][1]);
         }
-        // scores of row gq: keys 8 nt + 2 tq + {0,1}
-        float x[4] = {sc[0][0] * p.sl2, sc[0][1] * p.sl2, sc[1][0] * p.sl2, sc[1][1] * p.sl2};
+        // sc: (key g, head 2t), (key g, head 2t+1), (key g+8, head 2t), (key g+8, head 2t+1)
+        float x[4] = {sc[0] * p.sl2, sc[1] * p.sl2, sc[2] * p.sl2, sc[3] * p.sl2};
         const int kfirst = (pg0 + i) * 16;
-        if (kfirst < wb || kfirst + 16 > we) {  // boundary page: keys outside [wb, we)
+        if (kfirst < wb || kfirst + 16 > we) {
+            const int k0 = kfirst + gq, k1 = kfirst + gq + 8;
+            if (k0 < wb || k0 >= we) x[0] = x[1] = -INFINITY;
+            if (k1 < wb || k1 >= we) x[2] = x[3] = -INFINITY;
+        }
+        float mx0 = fmaxf(x[0], x[2]), mx1 = fmaxf(x[1], x[3]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int key = kfirst + (e >> 1) * 8 + 2 * tq + (e & 1);
-                if (key < wb || key >= we) x[e] = -INFINITY;
+        for (int off = 4; off < 32; off <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+        const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+        const float f0 = ptx::ex2(m0 - n0), f1 = ptx::ex2(m1 - n1);  // m = -inf -> 0
+        m0 = n0;
+        m1 = n1;
+        const float p00 = h0ok ? ptx::ex2(x[0] - n0) : 0.f, p01 = h1ok ? ptx::ex2(x[1] - n1) : 0.f;
+        const float p10 = h0ok ? ptx::ex2(x[2] - n0) : 0.f, p11 = h1ok ? ptx::ex2(x[3] - n1) : 0.f;
+        l0 = l0 * f0 + (p00 + p10);
+        l1 = l1 * f1 + (p01 + p11);
+        if (!__all_sync(0xffffffffu, f0 == 1.f && f1 == 1.f)) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                o[j][0] *= f0;
+                o[j][1] *= f1;
+                o[j][2] *= f0;
+                o[j][3] *= f1;
             }
         }
-        float mx = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m, mx);
-        const float f = ptx::ex2(m - m_new);  // m = -inf -> 0
-        m = m_new;
-        float pr[4];
+        // P^T as the B operand: transpose the two 8x8 (key x head) blocks; hi + lo parts
+        const uint32_t h0 = pack2<kFmt>(p00, p01), h1 = pack2<kFmt>(p10, p11);
+        const float2 u0 = unpack2<kFmt>(h0), u1 = unpack2<kFmt>(h1);
+        const uint32_t q0 = pack2<kFmt>(p00 - u0.x, p01 - u0.y), q1 = pack2<kFmt>(p10 - u1.x, p11 - u1.y);
+        const uint32_t bh0 = movmatrix_t(h0), bh1 = movmatrix_t(h1);
+        const uint32_t bl0 = movmatrix_t(q0), bl1 = movmatrix_t(q1);
+        // ---- O^T (128 d x 8 heads) += V^T P^T: one MMA per 16-d tile (x2 for hi/lo)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) pr[e] = ptx::ex2(x[e] - m_new);
-        l = l * f + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
-        if (!__all_sync(0xffffffffu, f == 1.f)) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                o[j][0] *= f;
-                o[j][1] *= f;
-            }
-        }
-        // P as the A operand: hi = round(p), lo = round(p - hi)
-        const uint32_t ph0 = pack2<kFmt>(pr[0], pr[1]), ph1 = pack2<kFmt>(pr[2], pr[3]);
-        const float2 h0 = unpack2<kFmt>(ph0), h1 = unpack2<kFmt>(ph1);
-        const uint32_t pl0 = pack2<kFmt>(pr[0] - h0.x, pr[1] - h0.y), pl1 = pack2<kFmt>(pr[2] - h1.x, pr[3] - h1.y);
-        // ---- O += P V: 16 n-tiles of 8 d, V fragments via ldmatrix.trans
-#pragma unroll
-        for (int dp = 0; dp < 8; ++dp) {  // two d-tiles per ldmatrix.x4
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(vst + page_off((lm & 1) * 8 + lr, 2 * dp + (lm >> 1)), b0, b1, b2, b3);
-            mma16816<kFmt>(o[2 * dp], ph0, ph1, b0, b1);
-            mma16816<kFmt>(o[2 * dp], pl0, pl1, b0, b1);
-            mma16816<kFmt>(o[2 * dp + 1], ph0, ph1, b2, b3);
-            mma16816<kFmt>(o[2 * dp + 1], pl0, pl1, b2, b3);
+        for (int md = 0; md < 8; ++md) {
+            uint32_t a[4];  // A = V^T: rows d 16md..+7 / +8..+15, cols keys 0-7 / 8-15
+            ldsm_x4_t(vst + page_off((lm >> 1) * 8 + lr, 2 * md + (lm & 1)), a[0], a[1], a[2], a[3]);
+            mma16816a<kFmt>(o[md], a, bh0, bh1);
+            mma16816a<kFmt>(o[md], a, bl0, bl1);
         }
         // ---- refill this stage with page i + kDecStages
         const int nxt = i + kDecStages;
@@ -955,20 +978,30 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
         }
     }
     dpos += npg;
-    l += __shfl_xor_sync(0xffffffffu, l, 1);
-    l += __shfl_xor_sync(0xffffffffu, l, 2);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    }
     // in-CTA merge of the 4 virtual CTAs (LSE merge, attention.hpp:294-326);
     // reuses warp 0's ring (every warp is past its last TMA wait).
     constexpr int kStride = kHeadDim + 4;
     float* red = reinterpret_cast<float*>(smem);
     ptx::named_bar_sync(2, kDecodeWarps * 32);
-    if (gq < G) {
-        float* dst = red + (warp * G + gq) * kStride;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) *reinterpret_cast<float2*>(dst + 8 * j + 2 * tq) = make_float2(o[j][0], o[j][1]);
-        if (tq == 0) {
-            dst[kHeadDim] = m;
-            dst[kHeadDim + 1] = l;
+    for (int hh = 0; hh < 2; ++hh) {
+        const int head = 2 * tq + hh;
+        if (head < G) {
+            float* dst = red + (warp * G + head) * kStride;
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+                dst[16 * md + gq] = o[md][hh];
+                dst[16 * md + gq + 8] = o[md][2 + hh];
+            }
+            if (gq == 0) {
+                dst[kHeadDim] = hh ? m1 : m0;
+                dst[kHeadDim + 1] = hh ? l1 : l0;
+            }
         }
     }
     ptx::named_bar_sync(2, kDecodeWarps * 32);
@@ -1109,7 +1142,7 @@ __device__ __forceinline__ int2 claim_item(const RunParams& p, uint32_t sm, int3
 // of the serial comparator.  Persistence matters on sm_100: kernels that use
 // tcgen05 get one new CTA dispatched only into an idle SM, so a classic
 // CTA-per-task grid would lose the second slot after the first wave.
-template <int G, int kFmt>
+template <int G, int kFmt, bool kSlots>
 __global__ void __launch_bounds__(kThreads, 2)
     pod_fused_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmq,
                      const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
@@ -1120,7 +1153,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t sm = ptx::smid();
-    const bool slots = p.policy == POD_POLICY_SLOTS;
+    constexpr bool slots = kSlots;  // POD_POLICY_SLOTS (engine 2) vs ticket policies (engine 1)
     if (tid == 0) {
         if (sbase & 1023u) __trap();  // SW128 atoms need a 1024-aligned base
         // p_full (12, 13) get one arrival per softmax warp; so does engine 2's q_full (0),
@@ -1160,7 +1193,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (tid == 0) {
             int32_t slot = -1;
             int2 w;
-            if (slots) {
+            if constexpr (kSlots) {
                 // prefill slot: prefill items first, then decode; decode slot: decode only
                 int op = prefill_slot ? 0 : 1;
                 int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
@@ -1193,7 +1226,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncthreads();  // role[] is rewritten by the next claim
         if (op < 0) break;
         if (op == 0) {
-            if (slots)
+            if constexpr (kSlots)
                 prefill_item2<kFmt>(p, &tmk, &tmv, id, smem, tmem, ps2);
             else
                 prefill_item<kFmt>(p, &tmq, &tmk, &tmv, id, smem, tmem, ps);
@@ -1405,16 +1438,23 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
     // mode 0 fused, 1 serial, 2 prefill only, 3 decode only
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(pod_fused_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(pod_fused_kernel<G, kFmt, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(pod_fused_kernel<G, kFmt, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         attr_done = true;
     }
     const int nsm = plan->dev.num_sms;
     auto launch = [&](const RunParams& q) {
         const int items = q.num_pctas + q.num_dctas;
-        int grid = std::min(items, 2 * nsm);  // persistent: 2 resident CTAs per SM
-        if (q.policy == POD_POLICY_SLOTS && q.num_dctas == 0) grid = std::min(items, nsm);  // prefill slots only
-        if (items > 0)
-            pod_fused_kernel<G, kFmt><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk, maps.dv);
+        if (items <= 0) return;
+        if (q.policy == POD_POLICY_SLOTS) {
+            const int grid = std::min(items, q.num_dctas == 0 ? nsm : 2 * nsm);  // prefill slots only / 2 per SM
+            pod_fused_kernel<G, kFmt, true><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk,
+                                                                               maps.dv);
+        } else {
+            const int grid = std::min(items, 2 * nsm);  // persistent: 2 resident CTAs per SM
+            pod_fused_kernel<G, kFmt, false><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk,
+                                                                                maps.dv);
+        }
     };
     if (mode == 0) {
         launch(p);
@@ -1577,8 +1617,8 @@ pod_status pod_attn_occupancy(const pod_plan* plan, int32_t* fused, int32_t* pre
     const int G = plan->shape.num_q_heads / plan->shape.num_kv_heads;
     if (G != 4) return POD_ERR_UNSUPPORTED;
     int a = 0;
-    cudaFuncSetAttribute(pod_fused_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, pod_fused_kernel<4, 1>, kThreads, kSmemBytes);
+    cudaFuncSetAttribute(pod_fused_kernel<4, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, pod_fused_kernel<4, 1, false>, kThreads, kSmemBytes);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
     // one persistent kernel serves all three launch kinds
     *fused = a;

@@ -244,16 +244,24 @@ def test_role_log_scheduler_contract(policy):
     P, D = op.info.num_prefill_ctas, op.info.num_decode_ctas
     assert sorted(rec[rec[:, 2] == 0, 3].tolist()) == list(range(P))
     assert sorted(rec[rec[:, 2] == 1, 3].tolist()) == list(range(D))
-    if policy != POD_POLICY_COMPLEMENT:
-        pr, dr = op.info.prefill_ratio, op.info.decode_ratio
-        order = np.argsort(rec[:, 4])  # claim order
-        claimed = [0, 0]
-        for i in order:
-            op_i, ticket = rec[i, 2], rec[i, 1] % (pr + dr)
-            want = 0 if ticket < pr else 1
-            if op_i != want:  # switched: the wanted pool must have been exhausted by then
-                assert claimed[want] == (P if want == 0 else D)
-            claimed[op_i] += 1
+    sms = rec[:, 0]
+    for sm in np.unique(sms):
+        mine = rec[sms == sm]
+        if policy != POD_POLICY_COMPLEMENT:
+            # per-SM tickets are the SM counter's values 0..k-1, each used once
+            assert sorted(mine[:, 1].tolist()) == list(range(len(mine)))
+            pr, dr = op.info.prefill_ratio, op.info.decode_ratio
+            # in ticket order the ops follow sm_aware_assign's pattern until the first
+            # switch; a switch means the wanted pool ran dry, so every later claim on
+            # this SM is the other op (pool exhaustion is monotone in time)
+            seq = mine[np.argsort(mine[:, 1])]
+            switched_to = None
+            for ticket, op_i in zip(seq[:, 1], seq[:, 2]):
+                want = 0 if ticket % (pr + dr) < pr else 1
+                if switched_to is not None:
+                    assert op_i == switched_to
+                elif op_i != want:
+                    switched_to = op_i
 
 
 def test_fault_injection_is_detected():
