@@ -224,7 +224,7 @@ def run_pod(args, rank, world, local_rank):
     batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
     wl = build_workload(batch, device=dev, seed_q=42 + 1000 * rank, seed_kv=43 + 1000 * rank)
     opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode, precision=args.precision,
-                           decode_splits=args.decode_splits)
+                           decode_splits=args.decode_splits, split_wave_cap=args.split_wave_cap)
     op = PodAttention(batch, options=opts, device=local_rank)
     out = op.alloc_outputs()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -320,6 +320,7 @@ def main():
     ap.add_argument("--tile-mode", type=int, default=1)
     ap.add_argument("--precision", type=int, default=0, help="0: prefill P as bf16 hi+lo (default), 1: single bf16")
     ap.add_argument("--decode-splits", type=int, default=0)
+    ap.add_argument("--split-wave-cap", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -414,7 +415,7 @@ def main():
         "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
                  "prefill_splits": info.prefill_splits, "decode_splits": info.decode_splits,
                  "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
-                 "policy": args.policy, "prefill_p": "bf16 hi+lo" if args.precision == 0 else "bf16"},
+                 "policy": args.policy, "split_wave_cap": info.config.split_wave_cap, "prefill_p": "bf16 hi+lo" if args.precision == 0 else "bf16"},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": None,
                      "kernel": "pod_fused_kernel (+merge)", "peak_source": pk["source"]},

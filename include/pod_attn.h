@@ -119,9 +119,12 @@ enum {
     POD_POLICY_CLAMPED = 2,      /* proportional, rounded to the per-SM slot count     */
     POD_POLICY_COMPLEMENT = 3,   /* bind from the roles resident on the SM:
                                     prefill while < prefill_ratio prefill CTAs run there */
-    POD_POLICY_SLOTS = 4         /* 2 CTAs/SM, fixed 1:1: the first CTA resident on an SM
+    POD_POLICY_SLOTS = 4,        /* 2 CTAs/SM, fixed 1:1: the first CTA resident on an SM
                                     is the prefill slot (all 512 TMEM columns, two-block
                                     ping-pong engine), the second streams decode */
+    POD_POLICY_BALANCED = 5      /* bind the role with more estimated remaining slot-time
+                                    (planner per-item costs), so both pools drain together;
+                                    ties go to the role not resident on the SM */
 };
 
 enum {

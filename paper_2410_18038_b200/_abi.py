@@ -19,8 +19,8 @@ STATUS_NAMES = {
 
 POD_KV_HND, POD_KV_NHD = 0, 1
 POD_DTYPE_BF16, POD_DTYPE_FP16 = 0, 1
-POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT, POD_POLICY_SLOTS = \
-    0, 1, 2, 3, 4
+POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT, POD_POLICY_SLOTS, \
+    POD_POLICY_BALANCED = 0, 1, 2, 3, 4, 5
 POD_TILE_REFERENCE, POD_TILE_B200 = 0, 1
 POD_PRECISION_SPLIT, POD_PRECISION_FAST = 0, 1
 

@@ -90,6 +90,8 @@ struct RunParams {
     int32_t kv_layout;
     int32_t decode_splits;
     int32_t policy;
+    float w_prefill;  // POD_POLICY_BALANCED: estimated slot-us per prefill / decode item
+    float w_decode;
     int32_t p_split;  // prefill P as bf16 hi + lo (two PV MMAs)
     int32_t pad1;
     int64_t num_pages;
@@ -1098,7 +1100,20 @@ __device__ __forceinline__ int2 claim_item(const RunParams& p, uint32_t sm, int3
     const int ratio = p.prefill_ratio + p.decode_ratio;
     const uint32_t raw = atomicAdd(&p.ctr->sm_ctr[sm], 1u);
     int op;
-    if (p.policy == POD_POLICY_COMPLEMENT) {
+    if (p.policy == POD_POLICY_BALANCED) {
+        // remaining work of each pool (racy snapshot of the claim counters)
+        const float rp = static_cast<float>(p.num_pctas - min(p.num_pctas, static_cast<int>(
+                             *reinterpret_cast<volatile uint32_t*>(&p.ctr->cta_assign[0])))) * p.w_prefill;
+        const float rd = static_cast<float>(p.num_dctas - min(p.num_dctas, static_cast<int>(
+                             *reinterpret_cast<volatile uint32_t*>(&p.ctr->cta_assign[1])))) * p.w_decode;
+        if (rp > 1.25f * rd)
+            op = 0;
+        else if (rd > 1.25f * rp)
+            op = 1;
+        else  // comparable: complement what is resident on this SM
+            op = *reinterpret_cast<volatile uint32_t*>(&p.ctr->running_prefill[sm]) == 0u ? 0 : 1;
+        if (op == 0) atomicAdd(&p.ctr->running_prefill[sm], 1u);
+    } else if (p.policy == POD_POLICY_COMPLEMENT) {
         // bind from what is resident on this SM: prefill while fewer than
         // prefill_ratio prefill items run here, decode otherwise
         const uint32_t resident = atomicAdd(&p.ctr->running_prefill[sm], 1u);
@@ -1110,12 +1125,13 @@ __device__ __forceinline__ int2 claim_item(const RunParams& p, uint32_t sm, int3
     }
     int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
     if (id >= (op == 0 ? p.num_pctas : p.num_dctas)) {
-        if (p.policy == POD_POLICY_COMPLEMENT && op == 0) atomicSub(&p.ctr->running_prefill[sm], 1u);
+        if ((p.policy == POD_POLICY_COMPLEMENT || p.policy == POD_POLICY_BALANCED) && op == 0)
+            atomicSub(&p.ctr->running_prefill[sm], 1u);
         op ^= 1;
         id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
         if (id >= (op == 0 ? p.num_pctas : p.num_dctas))
             op = -1;
-        else if (p.policy == POD_POLICY_COMPLEMENT && op == 0)
+        else if ((p.policy == POD_POLICY_COMPLEMENT || p.policy == POD_POLICY_BALANCED) && op == 0)
             atomicAdd(&p.ctr->running_prefill[sm], 1u);
     }
     *log_slot_out = -1;
@@ -1237,7 +1253,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncthreads();
         ptx::tc_fence_after();
         if (tid == 0) {
-            if (p.policy == POD_POLICY_COMPLEMENT && op == 0) atomicSub(&p.ctr->running_prefill[sm], 1u);
+            if ((p.policy == POD_POLICY_COMPLEMENT || p.policy == POD_POLICY_BALANCED) && op == 0)
+                atomicSub(&p.ctr->running_prefill[sm], 1u);
             if (slot >= 0) p.role_log[8 * slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
         }
     }
@@ -1410,6 +1427,8 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.kv_layout = plan->batch.kv_layout;
     p.decode_splits = static_cast<int32_t>(plan->decode_splits);
     p.policy = plan->opts.policy;
+    p.w_prefill = static_cast<float>(plan->w_prefill);
+    p.w_decode = static_cast<float>(plan->w_decode);
     p.p_split = plan->opts.precision == POD_PRECISION_FAST ? 0 : 1;
     p.num_pages = num_pages;
     p.sl2 = static_cast<float>(1.4426950408889634 / plan->shape.scale);

@@ -90,6 +90,8 @@ struct pod_plan {
     int32_t merge_rows_prefill = 0;
     int32_t merge_rows_decode = 0;
     int64_t smem_bytes = 0;
+    double w_prefill = 1.0;  // estimated slot-us per prefill item (POD_POLICY_BALANCED)
+    double w_decode = 1.0;   // estimated slot-us per decode item
     pod::WorkspaceLayout ws;
     int32_t* role_log = nullptr;
 };

@@ -293,6 +293,24 @@ void lower(pod_plan& p) {
             p.merge_rows_decode += s.num_q_heads;
 }
 
+// Per-item slot-time estimates for POD_POLICY_BALANCED, from the algorithmic
+// work and the per-CTA rates measured on B200 (one resident CTA of the role:
+// ~3.0 TFLOP/s of causal prefill, ~31 GB/s of paged decode).
+void item_costs(pod_plan& p) {
+    const double d = p.shape.head_dim;
+    const int group = p.shape.num_q_heads / p.shape.num_kv_heads;
+    double flops = 0, bytes = 0;
+    for (const pod::PrefillCta& c : p.pctas) {
+        const double keys = std::max(0, std::min(c.kv_end, static_cast<int32_t>(p.batch.prefill.position_offset) +
+                                                               c.row_begin + c.rows) - c.kv_begin);
+        flops += 4.0 * d * c.rows * group * keys;
+    }
+    for (const pod::DecodeCta& c : p.dctas) bytes += 4.0 * d * (c.kv_end - c.kv_begin);
+    const double kPrefillFlopsPerSlotUs = 3.0e6, kDecodeBytesPerSlotUs = 31.0e3;
+    p.w_prefill = p.pctas.empty() ? 1.0 : flops / p.pctas.size() / kPrefillFlopsPerSlotUs;
+    p.w_decode = p.dctas.empty() ? 1.0 : bytes / p.dctas.size() / kDecodeBytesPerSlotUs;
+}
+
 // make_scheduler_state (gpu_sim.hpp:91-107) over PHYSICAL CTA counts.
 void scheduler_ratio(pod_plan& p) {
     const long P = static_cast<long>(p.pctas.size());
@@ -305,6 +323,10 @@ void scheduler_ratio(pod_plan& p) {
         p.prefill_ratio = g > 0 ? P / g : (P > 0 ? 1 : 0);
         p.decode_ratio = g > 0 ? D / g : (D > 0 ? 1 : 0);
         if (p.prefill_ratio == 0 && p.decode_ratio == 0) p.prefill_ratio = 1;
+    } else if (p.opts.policy == POD_POLICY_BALANCED) {
+        p.prefill_ratio = P > 0 ? 1 : 0;
+        p.decode_ratio = D > 0 ? 1 : 0;
+        if (P == 0 && D == 0) p.prefill_ratio = 1;
     } else if (p.opts.policy == POD_POLICY_SLOTS) {
         // fixed 1:1 per SM: one prefill slot, one decode slot (2 CTAs/SM)
         p.prefill_ratio = 1;
@@ -378,6 +400,20 @@ void build(pod_plan& p) {
     } else if (p.opts.tile_mode == POD_TILE_B200) {
         p.cfg = b200_tile_config(p);
         if (p.opts.ctas_per_sm == 4) fail(POD_ERR_UNSUPPORTED, "B200 tile mode: 4 CTAs/SM not built yet");
+        // Split selection per batch shape: prefill items must be fine enough to
+        // fill the slots the decode leaves behind.  Decode share of the serial
+        // time from algorithmic work at measured B200 rates (prefill ~0.68 PFLOP/s,
+        // paged decode ~6.6 TB/s): > 0.55 -> 2 waves (reference rule), > 0.4 -> 4, else 8.
+        if (p.opts.split_wave_cap <= 0 && p.batch.has_prefill && !p.decode_ctx.empty()) {
+            const auto& pf = p.batch.prefill;
+            const double C = static_cast<double>(pf.chunk_size), off = static_cast<double>(pf.position_offset);
+            const double flops = 4.0 * p.shape.head_dim * p.shape.num_q_heads * (C * off + C * (C + 1) / 2.0);
+            double bytes = 0;
+            for (int64_t c : p.decode_ctx) bytes += 4.0 * c * p.shape.num_kv_heads * p.shape.head_dim;
+            const double t_p = flops / 0.68e15, t_d = bytes / 6.6e12;
+            const double share = t_d / (t_p + t_d);
+            p.cfg.split_wave_cap = share > 0.55 ? 2 : (share > 0.4 ? 4 : 8);
+        }
     } else {
         if (p.opts.ctas_per_sm != 0) {
             p.cfg = make_tile_config(p.opts.ctas_per_sm);
@@ -395,6 +431,7 @@ void build(pod_plan& p) {
     if (p.batch.has_prefill) decompose_prefill(p);
     if (!p.decode_ctx.empty()) decompose_decode(p);
     lower(p);
+    item_costs(p);
     scheduler_ratio(p);
     p.smem_bytes = pod::fused_smem_bytes();
     layout_workspace(p);
