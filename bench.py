@@ -149,7 +149,7 @@ def cpu_reference_sample(hq, hkv, chunk, off, b, ctx, target_s=12.0, threads=Non
     out = np.zeros((G, d))
     t = O.run_shards([dict(kind=1, group=G, rows=1, offset=0, q=qcal, k=kcal, v=kcal, out=out)], d, scale, 64, 64, 1)
     rate1 = G * 4096 / max(t, 1e-6)  # pairs/s on one core
-    budget_pairs = target_s * rate1 * 0.5  # ~target_s core-seconds
+    budget_pairs = target_s * rate1  # ~target_s core-seconds of the reference's own work
     # sample: prefill row blocks spread over the chunk + decode shards, in proportion
     n_shards = max(2 * threads, 8)
     pf_share = pf_pairs / total_pairs
@@ -390,6 +390,11 @@ def main():
     else:
         achieved = flops_r / (us * 1e-6) / 1e12
         peak, unit = pk["bf16_tflops"], "TFLOP/s"
+    traffic = None  # DRAM bytes of one fused launch from the committed ncu capture of this config
+    if args.config == DEFAULT_CONFIG and world == 1:
+        caps = sorted((ROOT / "profiles").glob("round*/fused_traffic.json"))
+        if caps:
+            traffic = json.loads(caps[-1].read_text()).get("dram_bytes_per_launch")
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -417,7 +422,7 @@ def main():
                  "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
                  "policy": args.policy, "split_wave_cap": info.config.split_wave_cap, "prefill_p": "bf16 hi+lo" if args.precision == 0 else "bf16"},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": "pod_fused_kernel (+merge)", "peak_source": pk["source"]},
         "cpu_baseline": cpu,
         "e2e": {"value": round(r["t_e2e"] * 1000, 2), "unit": "us/layer", "h2d_bytes_per_step": r["h2d"],
