@@ -420,7 +420,7 @@ def main():
         "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
                  "prefill_splits": info.prefill_splits, "decode_splits": info.decode_splits,
                  "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
-                 "policy": args.policy, "split_wave_cap": info.config.split_wave_cap, "prefill_p": "bf16 hi+lo" if args.precision == 0 else "bf16"},
+                 "policy": args.policy, "split_wave_cap": info.config.split_wave_cap, "prefill_p": {0: "bf16 hi+lo", 1: "bf16"}[args.precision]},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": "pod_fused_kernel (+merge)", "peak_source": pk["source"]},

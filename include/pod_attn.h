@@ -122,9 +122,12 @@ enum {
     POD_POLICY_SLOTS = 4,        /* 2 CTAs/SM, fixed 1:1: the first CTA resident on an SM
                                     is the prefill slot (all 512 TMEM columns, two-block
                                     ping-pong engine), the second streams decode */
-    POD_POLICY_BALANCED = 5      /* bind the role with more estimated remaining slot-time
+    POD_POLICY_BALANCED = 5,     /* bind the role with more estimated remaining slot-time
                                     (planner per-item costs), so both pools drain together;
                                     ties go to the role not resident on the SM */
+    POD_POLICY_PARTITION = 6     /* SM-aware spatial split: prefill_sms SMs (spread evenly
+                                    over the SM ids) bind prefill on both slots, the others
+                                    decode; an exhausted pool switches to the other */
 };
 
 enum {

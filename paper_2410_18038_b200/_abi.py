@@ -6,6 +6,7 @@ fails loudly if the library is missing: there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
@@ -20,7 +21,7 @@ STATUS_NAMES = {
 POD_KV_HND, POD_KV_NHD = 0, 1
 POD_DTYPE_BF16, POD_DTYPE_FP16 = 0, 1
 POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT, POD_POLICY_SLOTS, \
-    POD_POLICY_BALANCED = 0, 1, 2, 3, 4, 5
+    POD_POLICY_BALANCED, POD_POLICY_PARTITION = 0, 1, 2, 3, 4, 5, 6
 POD_TILE_REFERENCE, POD_TILE_B200 = 0, 1
 POD_PRECISION_SPLIT, POD_PRECISION_FAST = 0, 1
 
@@ -115,11 +116,12 @@ def lib() -> C.CDLL:
     """Loads libpod_attn.so (raises if it has not been built)."""
     global _lib
     if _lib is None:
-        if not LIB_PATH.exists():
+        path = Path(os.environ["POD_LIB"]) if os.environ.get("POD_LIB") else LIB_PATH  # experiment builds
+        if not path.exists():
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                 "(there is no CPU fallback for the POD kernels)")
-        l = C.CDLL(str(LIB_PATH))
+        l = C.CDLL(str(path))
         for name, res, args in SYMBOLS:
             fn = getattr(l, name)
             fn.restype = res

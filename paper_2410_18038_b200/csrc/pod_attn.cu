@@ -43,16 +43,33 @@ constexpr uint32_t kKvStageBytes = kKvTile * kHeadDim * 2;  // 16 KB
 constexpr uint32_t kOffQ = 0;
 constexpr uint32_t kOffK = kOffQ + kQBytes;                 // 2 stages
 constexpr uint32_t kOffV = kOffK + 2 * kKvStageBytes;       // 2 stages
-constexpr uint32_t kOffBar = kOffV + 2 * kKvStageBytes;     // 16 mbarriers
+// Decode role: per-warp TMA rings of K+V head-pages below the barrier block.
+#ifndef POD_DEC_STAGES
+#define POD_DEC_STAGES 3
+#endif
+#ifndef POD_DEC_WARPS
+#define POD_DEC_WARPS 4
+#endif
+// Warps that stream one decode item (the planner's 4 virtual decode CTAs,
+// kDecodeWarps, are the item's logical split; the kernel may use more warps).
+constexpr int kDecWarpsK = POD_DEC_WARPS;
+static_assert(kDecWarpsK <= kThreads / 32, "decode warps");
+constexpr int kDecStages = POD_DEC_STAGES;             // pages in flight per warp
+constexpr uint32_t kDecPageBytes = 16 * kHeadDim * 2;  // one head-page of K (or V): 4 KB
+constexpr uint32_t kDecStageBytes = 2 * kDecPageBytes; // K + V
+constexpr uint32_t kDecWarpBytes = kDecStages * kDecStageBytes;
+constexpr uint32_t kPrefillBytes = kOffV + 2 * kKvStageBytes;
+constexpr uint32_t kOffBar = kPrefillBytes > kDecWarpsK * kDecWarpBytes ? kPrefillBytes
+                                                                          : kDecWarpsK * kDecWarpBytes;  // 16 mbarriers
 // engine 2 keeps Q in TMEM: K/V stages only
 constexpr uint32_t kOffK2 = 0;
 constexpr uint32_t kOffV2 = kOffK2 + 2 * kKvStageBytes;
 constexpr uint32_t kOffTmemSlot = kOffBar + 128;
-constexpr uint32_t kOffDecBar = kOffBar + 160;              // 4 warps x 3 stages of decode mbarriers
+constexpr uint32_t kOffDecBar = kOffBar + 160;              // 4 warps x kDecStages decode mbarriers
 constexpr uint32_t kOffRole = kOffTmemSlot + 16;          // role[0..3]
-constexpr uint32_t kSmemBytes = kOffBar + 256;              // 98560 B -> 2 CTAs / SM
-static_assert(kOffDecBar + 12 * 8 <= kSmemBytes, "decode barriers");
-static_assert(kSmemBytes * 2 + 2048 <= 233472, "two CTAs must fit one SM");
+constexpr uint32_t kSmemBytes = kOffDecBar + kDecWarpsK * kDecStages * 8 + 32;  // 98560 B -> 2 CTAs / SM
+static_assert(kOffRole + 16 <= kOffDecBar, "role slots");
+static_assert(POD_DEC_STAGES != 3 || kSmemBytes * 2 + 2048 <= 233472, "two CTAs must fit one SM");
 constexpr uint32_t kTmemCols = 256;                         // S0 | S1 | O(128)
 constexpr uint32_t kTmemS0 = 0, kTmemO = 128;
 
@@ -93,7 +110,11 @@ struct RunParams {
     float w_prefill;  // POD_POLICY_BALANCED: estimated slot-us per prefill / decode item
     float w_decode;
     int32_t p_split;  // prefill P as bf16 hi + lo (two PV MMAs)
-    int32_t pad1;
+    int32_t grid_per_sm;   // resident CTAs per SM of the persistent launch (1 or 2)
+    int32_t trace;         // debug: per-tile cycle stamps of CTA 0's first prefill item after the role log
+    int32_t trace_mode;    // debug: 2 = serialise MMA issue with completion (execution latency probe)
+    int32_t prefill_sms;   // POD_POLICY_PARTITION: SMs that bind prefill first
+    int32_t num_sms;
     int64_t num_pages;
     float sl2;  // log2(e) / scale  (scale is the reference's divisor)
 };
@@ -142,7 +163,7 @@ __device__ __forceinline__ void prefill_issue_qk(uint32_t tmem_s, uint32_t sQ, u
         const uint32_t koff = (kk & 3) * 32u;  // 16 elements = 32 B inside the 128 B swizzle row
         const uint64_t a = ptx::sw128_desc(sQ + (kk >> 2) * (kMBlock * 128) + koff, 16, 1024);
         const uint64_t b = ptx::sw128_desc(sK + (kk >> 2) * (kKvTile * 128) + koff, 16, 1024);
-        ptx::umma_f16_ss(tmem_s, a, b, idesc, kk > 0 ? 1u : 0u);
+        ptx::umma_f16_ss_elect(tmem_s, a, b, idesc, kk > 0 ? 1u : 0u);
     }
 }
 
@@ -155,9 +176,49 @@ __device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t tmem_
 #pragma unroll
     for (int kk = 0; kk < kKvTile / 16; ++kk) {
         const uint64_t b = ptx::sw128_desc(sV + kk * 2048, kKvTile * 128, 1024);
-        ptx::umma_f16_ts(tmem_o, tmem_p + kk * 8, b, idesc, (accumulate || kk > 0) ? 1u : 0u);
-        if (split) ptx::umma_f16_ts(tmem_o, tmem_p + 32 + kk * 8, b, idesc, 1u);  // + P_lo V
+        ptx::umma_f16_ts_elect(tmem_o, tmem_p + kk * 8, b, idesc, (accumulate || kk > 0) ? 1u : 0u);
+        if (split) ptx::umma_f16_ts_elect(tmem_o, tmem_p + 32 + kk * 8, b, idesc, 1u);  // + P_lo V
     }
+}
+
+// One softmax row of a 64-key tile: p = 2^(s * sl2 - m) (one FFMA2 per pair, one
+// MUFU per score), P written over the row's S columns in TMEM as the A operand of
+// the TS MMA.  Returns the row sum of p (fp32).
+//   kMode 0: one P, rounded to nearest (columns [0,32))
+//   kMode 1: bf16 hi + lo by truncation (integer byte permutes, no conversion unit):
+//            hi = top 16 bits of p, lo = p - hi (exact in fp32) truncated; hi in
+//            [0,32), lo in [32,64); hi + lo keeps ~15 mantissa bits
+//   kMode 2: hi + lo rounded to nearest (fp16 inputs)
+template <int kFmt, int kMode>
+__device__ __forceinline__ float softmax_p_row(const float (&s)[kKvTile], float sl2, float neg_m, uint32_t s_addr) {
+    const float2 sl2v = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
+    float2 lsum2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+            const float2 x = ffma2(make_float2(s[32 * hf + c], s[32 * hf + c + 1]), sl2v, nm2);
+            const float p0 = ptx::ex2(x.x), p1 = ptx::ex2(x.y);
+            lsum2 = fadd2(lsum2, make_float2(p0, p1));
+            if constexpr (kMode == 1) {
+                const uint32_t u0 = __float_as_uint(p0), u1 = __float_as_uint(p1);
+                hi[c / 2] = __byte_perm(u0, u1, 0x7632);
+                const float2 lv = fadd2(make_float2(p0, p1), make_float2(-__uint_as_float(u0 & 0xffff0000u),
+                                                                         -__uint_as_float(u1 & 0xffff0000u)));
+                lo[c / 2] = __byte_perm(__float_as_uint(lv.x), __float_as_uint(lv.y), 0x7632);
+            } else {
+                hi[c / 2] = pack2<kFmt>(p0, p1);
+                if constexpr (kMode == 2) {
+                    const float2 hv = unpack2<kFmt>(hi[c / 2]);
+                    lo[c / 2] = pack2<kFmt>(p0 - hv.x, p1 - hv.y);
+                }
+            }
+        }
+        ptx::tmem_st16(s_addr + 16 * hf, hi);
+        if constexpr (kMode != 0) ptx::tmem_st16(s_addr + 32 + 16 * hf, lo);
+    }
+    return lsum2.x + lsum2.y;
 }
 
 struct BlockRange {
@@ -192,9 +253,9 @@ __device__ __forceinline__ void prefill_load_kv_tile(const RunParams& p, const C
         for (int dh = 0; dh < 2; ++dh) {
             const uint32_t d = dst + dh * (kKvTile * 128) + pg * 2048;
             if (p.kv_layout == POD_KV_HND)
-                ptx::tma_load_4d(d, tm, bar, dh * 64, 0, kv_head, phys);
+                ptx::tma_load_4d_elect(d, tm, bar, dh * 64, 0, kv_head, phys);
             else
-                ptx::tma_load_4d(d, tm, bar, dh * 64, kv_head, 0, phys);
+                ptx::tma_load_4d_elect(d, tm, bar, dh * 64, kv_head, 0, phys);
         }
     }
 }
@@ -212,7 +273,16 @@ __device__ __forceinline__ void prefill_load_kv_tile(const RunParams& p, const C
 struct PrefillState {
     int g = 0;   // KV tiles issued so far (stage = g & 1, phase = (g >> 1) & 1)
     int qb = 0;  // Q blocks loaded so far
+    int items = 0;
 };
+
+// Debug trace (RunParams::trace): CTA 0, first prefill item, first 256 tiles.
+__device__ __forceinline__ void trace_stamp(const RunParams& p, int items, int t, int k) {
+    if (p.trace && blockIdx.x == 0 && items == 0 && t < 768 && p.role_log) {
+        int32_t* tr = p.role_log + p.trace;
+        tr[t * 8 + k] = static_cast<int32_t>(clock64());
+    }
+}
 
 template <int kFmt>
 __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const CUtensorMap* tmk,
@@ -245,33 +315,39 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
             ps.qb += 1;
         }
     }
+    ps.items += 1;
 
     if (warp == 4) {
         // ------------------------------------------------ TMA producer --
-        if (lane == 0) {
+        // (warp-uniform loop; single-thread instructions are elect-predicated)
+        {
             int g = g0, qb = qb0;
             for (int b = 0; b < nblocks; ++b) {
                 const BlockRange br = prefill_block(p, job, b);
                 if (br.nt == 0) continue;
                 if (qb > 0) ptx::mbar_wait(b_qempty, (qb - 1) & 1);
-                ptx::mbar_arrive_expect_tx(b_qfull, kQBytes);
-                ptx::tma_load_3d(sQ, tmq, b_qfull, 0, job.kv_head * G, br.r0);
-                ptx::tma_load_3d(sQ + kMBlock * 128, tmq, b_qfull, 64, job.kv_head * G, br.r0);
+                ptx::mbar_arrive_expect_tx_elect(b_qfull, kQBytes);
+                ptx::tma_load_3d_elect(sQ, tmq, b_qfull, 0, job.kv_head * G, br.r0);
+                ptx::tma_load_3d_elect(sQ + kMBlock * 128, tmq, b_qfull, 64, job.kv_head * G, br.r0);
                 ++qb;
                 for (int t = 0; t <= br.nt; ++t) {
                     if (t < br.nt) {  // K of tile t
                         const int gg = g + t, st = gg & 1;
                         if (gg >= 2) ptx::mbar_wait(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
-                        ptx::mbar_arrive_expect_tx(b_kfull + 8 * st, kKvStageBytes);
+                        trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t, 4);
+                        ptx::mbar_arrive_expect_tx_elect(b_kfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmk, sK + st * kKvStageBytes, b_kfull + 8 * st,
                                              br.kt0 + t * kKvTile, job.kv_head, pbeg, npages);
+                        trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t, 5);
                     }
                     if (t > 0) {  // V of tile t-1
                         const int gg = g + t - 1, st = gg & 1;
                         if (gg >= 2) ptx::mbar_wait(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
-                        ptx::mbar_arrive_expect_tx(b_vfull + 8 * st, kKvStageBytes);
+                        trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t - 1, 6);
+                        ptx::mbar_arrive_expect_tx_elect(b_vfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
                                              br.kt0 + (t - 1) * kKvTile, job.kv_head, pbeg, npages);
+                        trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t - 1, 7);
                     }
                 }
                 g += br.nt;
@@ -279,7 +355,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
         }
     } else if (warp == 5) {
         // -------------------------------------------------- MMA issuer --
-        if (lane == 0) {
+        {
             int g = g0, qb = qb0;
             for (int b = 0; b < nblocks; ++b) {
                 const BlockRange br = prefill_block(p, job, b);
@@ -290,27 +366,40 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                     ptx::mbar_wait(b_kfull + 8 * st, (gg >> 1) & 1);
                     ptx::tc_fence_after();
                     prefill_issue_qk<kFmt>(tmem + kTmemS0 + st * kKvTile, sQ, sK + st * kKvStageBytes);
-                    ptx::umma_commit(b_sfull + 8 * st);
-                    ptx::umma_commit(b_kempty + 8 * st);
-                    if (j == br.nt - 1) ptx::umma_commit(b_qempty);
+                    ptx::umma_commit_elect(b_sfull + 8 * st);
+                    ptx::umma_commit_elect(b_kempty + 8 * st);
+                    if (j == br.nt - 1) ptx::umma_commit_elect(b_qempty);
                 }
                 for (int t = 0; t < br.nt; ++t) {
                     const int gg = g + t, st = gg & 1;
                     ptx::mbar_wait(b_pfull + 8 * st, (gg >> 1) & 1);
+                    trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 3);
                     ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
+                    trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 4);
                     ptx::tc_fence_after();
                     prefill_issue_pv<kFmt>(tmem + kTmemO, tmem + kTmemS0 + st * kKvTile, sV + st * kKvStageBytes,
                                            t > 0, p.p_split != 0);
-                    ptx::umma_commit(b_pv + 8 * st);
-                    ptx::umma_commit(b_vempty + 8 * st);
+                    ptx::umma_commit_elect(b_pv + 8 * st);
+                    ptx::umma_commit_elect(b_vempty + 8 * st);
+                    trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 7);
+                    if (p.trace_mode == 2 && blockIdx.x == 0 && ps.items == 1 && b == 0) {
+                        ptx::mbar_wait(b_pv + 8 * st, (gg >> 1) & 1);  // debug: PV execution latency
+                        trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 512 + t, 0);
+                    }
                     if (t + 2 < br.nt) {
                         const int g2 = gg + 2;
                         ptx::mbar_wait(b_kfull + 8 * st, (g2 >> 1) & 1);
+                        trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 5);
                         ptx::tc_fence_after();
                         prefill_issue_qk<kFmt>(tmem + kTmemS0 + st * kKvTile, sQ, sK + st * kKvStageBytes);
-                        ptx::umma_commit(b_sfull + 8 * st);
-                        ptx::umma_commit(b_kempty + 8 * st);
-                        if (t + 2 == br.nt - 1) ptx::umma_commit(b_qempty);
+                        ptx::umma_commit_elect(b_sfull + 8 * st);
+                        ptx::umma_commit_elect(b_kempty + 8 * st);
+                        if (t + 2 == br.nt - 1) ptx::umma_commit_elect(b_qempty);
+                        trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 512 + t, 1);
+                        if (p.trace_mode == 2 && blockIdx.x == 0 && ps.items == 1 && b == 0) {
+                            ptx::mbar_wait(b_sfull + 8 * st, (g2 >> 1) & 1);  // debug: QK execution latency
+                            trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 512 + t, 2);
+                        }
                     }
                 }
                 g += br.nt;
@@ -351,7 +440,9 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
             for (int t = 0; t < br.nt; ++t) {
                 const int gg = g + t, st = gg & 1;
                 const uint32_t s_addr = lane_base + kTmemS0 + st * kKvTile;
+                if (tid == 0) trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 0);
                 ptx::mbar_wait(b_sfull + 8 * st, (gg >> 1) & 1);
+                if (tid == 0) trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 1);
                 ptx::tc_fence_after();
                 float s[kKvTile];
                 ptx::tmem_ld32(s_addr, *reinterpret_cast<float(*)[32]>(&s[0]));
@@ -379,49 +470,41 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                 l_run *= factor;
                 m_run = m_use;
                 // P -> TMEM over the consumed S row (A operand of the TS MMA), in two
-                // 32-key halves: hi = round(p) in columns [0,32); with p_split also
-                // lo = round(p - hi) in [32,64), so hi + lo carries ~16 mantissa bits.
-                float2 lsum2 = make_float2(0.f, 0.f);
-                const float neg_m = -m_use;
-                const bool live = m_use != -INFINITY;
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t hi[16], lo[16];
-#pragma unroll
-                    for (int c = 0; c < 32; c += 2) {
-                        // p = 2^(s * log2(e)/scale - m): one FFMA + one MUFU per score
-                        const float p0 = live ? ptx::ex2(fmaf(s[32 * hf + c], p.sl2, neg_m)) : 0.f;
-                        const float p1 = live ? ptx::ex2(fmaf(s[32 * hf + c + 1], p.sl2, neg_m)) : 0.f;
-                        lsum2 = fadd2(lsum2, make_float2(p0, p1));
-                        hi[c / 2] = pack2<kFmt>(p0, p1);
-                        const float2 hv = unpack2<kFmt>(hi[c / 2]);
-                        lo[c / 2] = pack2<kFmt>(p0 - hv.x, p1 - hv.y);
-                    }
-                    ptx::tmem_st16(s_addr + 16 * hf, hi);
-                    if (p.p_split) ptx::tmem_st16(s_addr + 32 + 16 * hf, lo);
-                }
-                l_run += lsum2.x + lsum2.y;
-                // Observe PV_{t-1} (keeps the pv barrier phases in order; required
-                // before O is rescaled).
-                if (t > 0) {
+                // 32-key halves of hi parts in columns [0,32); with p_split the lo
+                // parts (p - hi) go to [32,64), so hi + lo carries ~15 mantissa bits.
+                // A row with nothing visible yet has m = -inf and all scores -inf:
+                // offset 0 keeps ex2(-inf) = 0 without a predicate per score.
+                const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
+                float lsum;
+                if (kFmt == 1 && p.p_split)
+                    lsum = softmax_p_row<kFmt, 1>(s, p.sl2, neg_m, s_addr);
+                else if (p.p_split)
+                    lsum = softmax_p_row<kFmt, 2>(s, p.sl2, neg_m, s_addr);
+                else
+                    lsum = softmax_p_row<kFmt, 0>(s, p.sl2, neg_m, s_addr);
+                l_run += lsum;
+                if (tid == 0) trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 2);
+                // O is rescaled only when the reference max moved (rare, lazy): only
+                // then wait for PV_{t-1}, the newest MMA that writes O (PV_t cannot be
+                // issued before this warp arrives, so the parity wait is unambiguous).
+                if (t > 0 && __any_sync(0xffffffffu, need)) {
                     ptx::mbar_wait(b_pv + 8 * ((gg - 1) & 1), ((gg - 1) >> 1) & 1);
+                    if (tid == 0) trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 6);
                     ptx::tc_fence_after();
-                    if (__any_sync(0xffffffffu, need)) {
 #pragma unroll 1
-                        for (int ch = 0; ch < kHeadDim / 32; ++ch) {
-                            float o[32];
-                            ptx::tmem_ld32(lane_base + kTmemO + ch * 32, o);
-                            ptx::tmem_wait_ld();
+                    for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+                        float o[32];
+                        ptx::tmem_ld32(lane_base + kTmemO + ch * 32, o);
+                        ptx::tmem_wait_ld();
 #pragma unroll
-                            for (int c = 0; c < 32; ++c) o[c] *= factor;
-                            ptx::tmem_st32(lane_base + kTmemO + ch * 32, o);
-                        }
+                        for (int c = 0; c < 32; ++c) o[c] *= factor;
+                        ptx::tmem_st32(lane_base + kTmemO + ch * 32, o);
                     }
                 }
-                // P row -> TMEM over the consumed S row (A operand of the TS MMA)
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 __syncwarp();
+                if (lane == 0) trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t, warp);
                 if (lane == 0) ptx::mbar_arrive(b_pfull + 8 * st);
             }
             // ------------------------------------------------- epilogue --
@@ -474,7 +557,7 @@ __device__ __forceinline__ void issue_qk_ts(uint32_t tmem_s, uint32_t tmem_q, ui
 #pragma unroll
     for (int kk = 0; kk < kHeadDim / 16; ++kk) {
         const uint64_t b = ptx::sw128_desc(sK + (kk >> 2) * (kKvTile * 128) + (kk & 3) * 32u, 16, 1024);
-        ptx::umma_f16_ts(tmem_s, tmem_q + kk * 8, b, idesc, kk > 0 ? 1u : 0u);
+        ptx::umma_f16_ts_elect(tmem_s, tmem_q + kk * 8, b, idesc, kk > 0 ? 1u : 0u);
     }
 }
 
@@ -514,7 +597,7 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
 
     if (warp == 4) {
         // ------------------------------------------------ TMA producer --
-        if (lane == 0) {
+        {  // warp-uniform; single-thread instructions are elect-predicated
             int g = s0.g;
             for (int pr = 0; pr < npairs; ++pr) {
                 const bool hasB = 2 * pr + 1 < nblocks;
@@ -524,14 +607,14 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
                     if (t < nt) {
                         const int gg = g + t, st = gg & 1;
                         if (gg >= 2) ptx::mbar_wait(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
-                        ptx::mbar_arrive_expect_tx(b_kfull + 8 * st, kKvStageBytes);
+                        ptx::mbar_arrive_expect_tx_elect(b_kfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmk, sK + st * kKvStageBytes, b_kfull + 8 * st,
                                              ra.kt0 + t * kKvTile, job.kv_head, pbeg, npages);
                     }
                     if (t > 0) {
                         const int gg = g + t - 1, st = gg & 1;
                         if (gg >= 2) ptx::mbar_wait(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
-                        ptx::mbar_arrive_expect_tx(b_vfull + 8 * st, kKvStageBytes);
+                        ptx::mbar_arrive_expect_tx_elect(b_vfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
                                              ra.kt0 + (t - 1) * kKvTile, job.kv_head, pbeg, npages);
                     }
@@ -541,7 +624,7 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
         }
     } else if (warp == 5) {
         // -------------------------------------------------- MMA issuer --
-        if (lane == 0) {
+        {  // warp-uniform; single-thread instructions are elect-predicated
             int g = s0.g, na = s0.na, nb = s0.nb, pq = s0.pairs;
             for (int pr = 0; pr < npairs; ++pr) {
                 const bool hasB = 2 * pr + 1 < nblocks;
@@ -554,12 +637,12 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
                     ptx::mbar_wait(b_kfull + 8 * st, (g >> 1) & 1);
                     ptx::tc_fence_after();
                     issue_qk_ts<kFmt>(tmem + kT2SA, tmem + kT2QA, sK + st * kKvStageBytes);
-                    ptx::umma_commit(b_sfull);
+                    ptx::umma_commit_elect(b_sfull);
                     if (hasB) {
                         issue_qk_ts<kFmt>(tmem + kT2SB, tmem + kT2QB, sK + st * kKvStageBytes);
-                        ptx::umma_commit(b_sfull + 8);
+                        ptx::umma_commit_elect(b_sfull + 8);
                     }
-                    ptx::umma_commit(b_kempty + 8 * st);
+                    ptx::umma_commit_elect(b_kempty + 8 * st);
                 }
                 for (int t = 0; t < nt; ++t) {
                     const int gg = g + t, st = gg & 1, s1 = (gg + 1) & 1;
@@ -570,26 +653,26 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
                     ptx::tc_fence_after();
                     prefill_issue_pv<kFmt>(tmem + kT2OA, tmem + kT2SA, sV + st * kKvStageBytes, t > 0,
                                            p.p_split != 0);
-                    ptx::umma_commit(b_pv);
+                    ptx::umma_commit_elect(b_pv);
                     if (more) {
                         ptx::mbar_wait(b_kfull + 8 * s1, ((gg + 1) >> 1) & 1);
                         ptx::tc_fence_after();
                         issue_qk_ts<kFmt>(tmem + kT2SA, tmem + kT2QA, sK + s1 * kKvStageBytes);
-                        ptx::umma_commit(b_sfull);
+                        ptx::umma_commit_elect(b_sfull);
                     }
                     if (hasB) {
                         ptx::mbar_wait(b_pfull + 8, (nb + t) & 1);
                         ptx::tc_fence_after();
                         prefill_issue_pv<kFmt>(tmem + kT2OB, tmem + kT2SB, sV + st * kKvStageBytes, t > 0,
                                                p.p_split != 0);
-                        ptx::umma_commit(b_pv + 8);
+                        ptx::umma_commit_elect(b_pv + 8);
                         if (more) {
                             issue_qk_ts<kFmt>(tmem + kT2SB, tmem + kT2QB, sK + s1 * kKvStageBytes);
-                            ptx::umma_commit(b_sfull + 8);
+                            ptx::umma_commit_elect(b_sfull + 8);
                         }
                     }
-                    ptx::umma_commit(b_vempty + 8 * st);
-                    if (more) ptx::umma_commit(b_kempty + 8 * s1);
+                    ptx::umma_commit_elect(b_vempty + 8 * st);
+                    if (more) ptx::umma_commit_elect(b_kempty + 8 * s1);
                 }
                 g += nt;
                 na += nt;
@@ -767,11 +850,7 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
 }
 
 // ============================================================= decode ===
-constexpr int kDecStages = 3;                          // pages in flight per warp
-constexpr uint32_t kDecPageBytes = 16 * kHeadDim * 2;  // one head-page of K (or V): 4 KB
-constexpr uint32_t kDecStageBytes = 2 * kDecPageBytes; // K + V
-constexpr uint32_t kDecWarpBytes = kDecStages * kDecStageBytes;
-static_assert(kDecodeWarps * kDecWarpBytes <= kOffBar, "decode rings must fit below the barrier block");
+static_assert(kDecWarpsK * kDecWarpBytes <= kOffBar, "decode rings must fit below the barrier block");
 
 // Decode inner products on the warp-level tensor path (mma.sync m16n8k16,
 // fp32 accumulate): the G query heads of a KV head are the M rows (padded to
@@ -813,17 +892,9 @@ __device__ __forceinline__ uint32_t page_off(int row, int c) {
 __device__ __forceinline__ void decode_issue_page(const RunParams& p, const CUtensorMap* tk,
                                                   const CUtensorMap* tv, uint32_t dst, uint32_t bar,
                                                   int h, int phys) {
-    ptx::mbar_arrive_expect_tx(bar, kDecStageBytes);
-#pragma unroll
-    for (int dh = 0; dh < 2; ++dh) {
-        if (p.kv_layout == POD_KV_HND) {
-            ptx::tma_load_4d(dst + dh * 2048, tk, bar, dh * 64, 0, h, phys);
-            ptx::tma_load_4d(dst + kDecPageBytes + dh * 2048, tv, bar, dh * 64, 0, h, phys);
-        } else {
-            ptx::tma_load_4d(dst + dh * 2048, tk, bar, dh * 64, h, 0, phys);
-            ptx::tma_load_4d(dst + kDecPageBytes + dh * 2048, tv, bar, dh * 64, h, 0, phys);
-        }
-    }
+    ptx::mbar_arrive_expect_tx_elect(bar, kDecStageBytes);
+    ptx::tma_load_5d_elect(dst, tk, bar, 0, 0, 0, h, phys);
+    ptx::tma_load_5d_elect(dst + kDecPageBytes, tv, bar, 0, 0, 0, h, phys);
 }
 
 __device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
@@ -835,13 +906,13 @@ __device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
 template <int kFmt>
 __device__ __forceinline__ void mma16816a(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     if constexpr (kFmt == 1)
-        asm volatile(
+        asm(
             "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
             "{%0,%1,%2,%3};"
             : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
             : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
     else
-        asm volatile(
+        asm(
             "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
             "{%0,%1,%2,%3};"
             : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
@@ -864,10 +935,10 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
     static_assert(G <= 8, "decode: G query heads of one KV head are the N = 8 MMA columns");
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    if (warp >= kDecodeWarps) return;
+    if (warp >= kDecWarpsK) return;
     const DecodeCta job = p.dctas[cta_id];
     const int len = job.kv_end - job.kv_begin;
-    const int base = len / kDecodeWarps, rem = len % kDecodeWarps;
+    const int base = len / kDecWarpsK, rem = len % kDecWarpsK;
     const int wb = job.kv_begin + warp * base + min(warp, rem);
     const int we = wb + base + (warp < rem ? 1 : 0);
     const int h = job.kv_head;
@@ -898,29 +969,51 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
     const int32_t* pidx = p.page_indices + p.page_indptr[job.page_row];
     const int pg0 = wb >> 4;
     const int npg = we > wb ? ((we - 1) >> 4) - pg0 + 1 : 0;
+    // page ids: two 32-entry windows [cache_base, +32) and [+32, +64), one id per lane
+    // (the second window is loaded one window ahead, off the critical path)
     int cache_base = 0;
     int cached = (lane < npg) ? __ldg(pidx + pg0 + lane) : 0;
+    int cached2 = (32 + lane < npg) ? __ldg(pidx + pg0 + 32 + lane) : 0;
 #pragma unroll
     for (int j = 0; j < kDecStages; ++j) {
         const int phys = __shfl_sync(0xffffffffu, cached, j);
         const int st = (dpos + j) % kDecStages;
-        if (lane == 0 && j < npg) decode_issue_page(p, tk, tv, ring + st * kDecStageBytes, bars + 8 * st, h, phys);
+        if (j < npg) decode_issue_page(p, tk, tv, ring + st * kDecStageBytes, bars + 8 * st, h, phys);
     }
     __syncwarp();
     const int lm = lane >> 3, lr = lane & 7;  // ldmatrix: matrix lm, row lr
+    // S^T (16 keys x 8 heads) = K Q^T of one page: 8 k-steps as two independent
+    // MMA chains (even / odd k-steps) to halve the dependent-latency chain.
+    auto scores = [&](uint32_t kst, float (&sc)[4]) {
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int ks = 0; ks < 8; ks += 2) {
+            uint32_t a[4], b[4];  // keys 0-7 / 8-15 x d 16ks..+7 / +8..+15
+            ldsm_x4(kst + page_off((lm & 1) * 8 + lr, 2 * ks + (lm >> 1)), a[0], a[1], a[2], a[3]);
+            ldsm_x4(kst + page_off((lm & 1) * 8 + lr, 2 * ks + 2 + (lm >> 1)), b[0], b[1], b[2], b[3]);
+            mma16816a<kFmt>(sa, a, qb[ks][0], qb[ks][1]);
+            mma16816a<kFmt>(sb, b, qb[ks + 1][0], qb[ks + 1][1]);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sc[c] = sa[c] + sb[c];
+    };
+    // Software pipeline over pages: the score MMAs of page i+1 are issued before the
+    // softmax and P V of page i, so their latency overlaps the dependent chain of i.
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (npg > 0) {
+        const int st = dpos % kDecStages;
+        ptx::mbar_wait(bars + 8 * st, (dpos / kDecStages) & 1);
+        scores(ring + st * kDecStageBytes, sc);
+    }
     for (int i = 0; i < npg; ++i) {
         const int n = dpos + i;
         const int st = n % kDecStages;
-        ptx::mbar_wait(bars + 8 * st, (n / kDecStages) & 1);
-        const uint32_t kst = ring + st * kDecStageBytes;
-        const uint32_t vst = kst + kDecPageBytes;
-        // ---- S^T (16 keys x 8 heads) = K Q^T: one MMA per 16-d k-step
-        float sc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-            uint32_t a[4];  // keys 0-7 / 8-15 x d 16ks..+7 / +8..+15
-            ldsm_x4(kst + page_off((lm & 1) * 8 + lr, 2 * ks + (lm >> 1)), a[0], a[1], a[2], a[3]);
-            mma16816a<kFmt>(sc, a, qb[ks][0], qb[ks][1]);
+        const uint32_t vst = ring + st * kDecStageBytes + kDecPageBytes;
+        float scn[4] = {0.f, 0.f, 0.f, 0.f};
+        if (i + 1 < npg) {
+            const int st1 = (n + 1) % kDecStages;
+            ptx::mbar_wait(bars + 8 * st1, ((n + 1) / kDecStages) & 1);
+            scores(ring + st1 * kDecStageBytes, scn);
         }
         // sc: (key g, head 2t), (key g, head 2t+1), (key g+8, head 2t), (key g+8, head 2t+1)
         float x[4] = {sc[0] * p.sl2, sc[1] * p.sl2, sc[2] * p.sl2, sc[3] * p.sl2};
@@ -967,16 +1060,19 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
             mma16816a<kFmt>(o[md], a, bh0, bh1);
             mma16816a<kFmt>(o[md], a, bl0, bl1);
         }
-        // ---- refill this stage with page i + kDecStages
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sc[c] = scn[c];
+        // ---- refill this stage (K consumed last iteration, V just now) with page i + kDecStages
         const int nxt = i + kDecStages;
         if (nxt < npg) {
             if (nxt - cache_base >= 32) {
                 cache_base += 32;
-                cached = (cache_base + lane < npg) ? __ldg(pidx + pg0 + cache_base + lane) : 0;
+                cached = cached2;
+                cached2 = (cache_base + 32 + lane < npg) ? __ldg(pidx + pg0 + cache_base + 32 + lane) : 0;
             }
             const int phys = __shfl_sync(0xffffffffu, cached, nxt - cache_base);
             __syncwarp();
-            if (lane == 0) decode_issue_page(p, tk, tv, ring + st * kDecStageBytes, bars + 8 * st, h, phys);
+            decode_issue_page(p, tk, tv, ring + st * kDecStageBytes, bars + 8 * st, h, phys);
         }
     }
     dpos += npg;
@@ -989,7 +1085,7 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
     // reuses warp 0's ring (every warp is past its last TMA wait).
     constexpr int kStride = kHeadDim + 4;
     float* red = reinterpret_cast<float*>(smem);
-    ptx::named_bar_sync(2, kDecodeWarps * 32);
+    ptx::named_bar_sync(2, kDecWarpsK * 32);
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
         const int head = 2 * tq + hh;
@@ -1006,18 +1102,18 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
             }
         }
     }
-    ptx::named_bar_sync(2, kDecodeWarps * 32);
-    for (int idx = tid; idx < G * kHeadDim; idx += kDecodeWarps * 32) {
+    ptx::named_bar_sync(2, kDecWarpsK * 32);
+    for (int idx = tid; idx < G * kHeadDim; idx += kDecWarpsK * 32) {
         const int g = idx / kHeadDim, d = idx % kHeadDim;
-        float mw[kDecodeWarps], M = -INFINITY;
+        float mw[kDecWarpsK], M = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < kDecodeWarps; ++w) {
+        for (int w = 0; w < kDecWarpsK; ++w) {
             mw[w] = red[(w * G + g) * kStride + kHeadDim];
             M = fmaxf(M, mw[w]);
         }
         float L = 0.f, acc = 0.f;
 #pragma unroll
-        for (int w = 0; w < kDecodeWarps; ++w) {
+        for (int w = 0; w < kDecWarpsK; ++w) {
             const float wt = ptx::ex2(mw[w] - M);  // empty warp: m = -inf -> 0
             L += red[(w * G + g) * kStride + kHeadDim + 1] * wt;
             acc += red[(w * G + g) * kStride + d] * wt;
@@ -1113,6 +1209,12 @@ __device__ __forceinline__ int2 claim_item(const RunParams& p, uint32_t sm, int3
         else  // comparable: complement what is resident on this SM
             op = *reinterpret_cast<volatile uint32_t*>(&p.ctr->running_prefill[sm]) == 0u ? 0 : 1;
         if (op == 0) atomicAdd(&p.ctr->running_prefill[sm], 1u);
+    } else if (p.policy == POD_POLICY_PARTITION) {
+        // spatial split spread evenly over the SM ids: SM s binds prefill iff
+        // floor((s + 1) x / n) > floor(s x / n)
+        // (fraction prefill_sms / num_sms applied over the %smid range, which may have gaps)
+        const float f = static_cast<float>(p.prefill_sms) / static_cast<float>(max(p.num_sms, 1));
+        op = floorf((sm + 1) * f) > floorf(sm * f) ? 0 : 1;
     } else if (p.policy == POD_POLICY_COMPLEMENT) {
         // bind from what is resident on this SM: prefill while fewer than
         // prefill_ratio prefill items run here, decode otherwise
@@ -1176,7 +1278,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // which engine 1 fills by TMA (expect_tx, one arrival)
         for (int i = 0; i < 16; ++i)
             ptx::mbar_init(sbase + kOffBar + 8 * i, (i == 12 || i == 13 || (i == 0 && slots)) ? kPrefillWarps : 1);
-        for (int i = 0; i < kDecodeWarps * kDecStages; ++i) ptx::mbar_init(sbase + kOffDecBar + 8 * i, 1);
+        for (int i = 0; i < kDecWarpsK * kDecStages; ++i) ptx::mbar_init(sbase + kOffDecBar + 8 * i, 1);
         ptx::fence_mbar_init();
         // POD_POLICY_SLOTS: the first CTA resident on this SM takes the prefill slot
         role[3] = slots ? static_cast<int>(atomicAdd(&p.ctr->sm_slot[sm], 1u)) : 0;
@@ -1197,6 +1299,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (p.num_pctas > 0) ptx::prefetch_tmap(&tmq);
         ptx::prefetch_tmap(&tmk);
         ptx::prefetch_tmap(&tmv);
+        ptx::prefetch_tmap(&tdk);
+        ptx::prefetch_tmap(&tdv);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -1247,7 +1351,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             else
                 prefill_item<kFmt>(p, &tmq, &tmk, &tmv, id, smem, tmem, ps);
         } else {
-            decode_item<G, kFmt>(p, &tmk, &tmv, id, smem, dpos);
+            decode_item<G, kFmt>(p, &tdk, &tdv, id, smem, dpos);
         }
         ptx::tc_fence_before();
         __syncthreads();
@@ -1329,7 +1433,7 @@ int64_t fused_smem_bytes() { return kSmemBytes; }
 
 struct Maps {
     CUtensorMap q, k, v;  // prefill role: SW128 boxes of 64 d x 16 tokens, Q boxes of 64 d x 128 rows
-    CUtensorMap dk, dv;   // decode role: one whole head-page (128 d x 16 tokens), no swizzle
+    CUtensorMap dk, dv;   // decode role: one whole head-page per box (5D view, SW128 halves)
 };
 
 pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_pool, const void* v_pool,
@@ -1366,9 +1470,21 @@ pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_
                 set_last_error("cuTensorMapEncodeTiled(kv) failed: " + std::to_string(static_cast<int>(r)));
                 return POD_ERR_CUDA;
             }
-            cuuint32_t dbox[4] = {kHeadDim, box[1], box[2], 1};
-            r = enc(which == 0 ? &m->dk : &m->dv, dt, 4, const_cast<void*>(which == 0 ? k_pool : v_pool), dims,
-                    strides, dbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            // Decode role: one 4 KB box per head-page.  The page is viewed as
+            // (64 d, 16 slots, 2 d-halves, head, page) so a single TMA op lands it
+            // as two 128B-swizzled 2 KB halves ([half][slot][64 d]), the same smem
+            // image as two SW128 boxes (TMA issue rate, not bytes, bounds small boxes).
+            cuuint64_t d5[5], s5[4];
+            const cuuint32_t box5[5] = {64, 16, 2, 1, 1}, estr5[5] = {1, 1, 1, 1, 1};
+            d5[0] = 64; d5[1] = 16; d5[2] = 2; d5[3] = hkv; d5[4] = num_pages;
+            if (plan->batch.kv_layout == POD_KV_HND) {
+                s5[0] = kHeadDim * 2; s5[1] = 128; s5[2] = 16ull * kHeadDim * 2; s5[3] = 16ull * hkv * kHeadDim * 2;
+            } else {
+                s5[0] = static_cast<cuuint64_t>(hkv) * kHeadDim * 2; s5[1] = 128; s5[2] = kHeadDim * 2;
+                s5[3] = 16ull * hkv * kHeadDim * 2;
+            }
+            r = enc(which == 0 ? &m->dk : &m->dv, dt, 5, const_cast<void*>(which == 0 ? k_pool : v_pool), d5, s5,
+                    box5, estr5, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) {
                 set_last_error("cuTensorMapEncodeTiled(decode kv) failed: " + std::to_string(static_cast<int>(r)));
@@ -1429,7 +1545,18 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.policy = plan->opts.policy;
     p.w_prefill = static_cast<float>(plan->w_prefill);
     p.w_decode = static_cast<float>(plan->w_decode);
-    p.p_split = plan->opts.precision == POD_PRECISION_FAST ? 0 : 1;
+    p.p_split = plan->opts.precision == POD_PRECISION_SPLIT ? 1 : 0;
+    {
+        const char* e = std::getenv("POD_GRID_PER_SM");  // experiment knob
+        p.grid_per_sm = e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+    }
+    {
+        const char* e = std::getenv("POD_TRACE");  // debug knob
+        p.trace = (e && std::atoi(e)) ? static_cast<int32_t>(8 * (plan->pctas.size() + plan->dctas.size())) : 0;
+        p.trace_mode = e ? std::atoi(e) : 0;
+    }
+    p.prefill_sms = plan->prefill_sms;
+    p.num_sms = plan->dev.num_sms;
     p.num_pages = num_pages;
     p.sl2 = static_cast<float>(1.4426950408889634 / plan->shape.scale);
     return p;
@@ -1470,7 +1597,8 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
             pod_fused_kernel<G, kFmt, true><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk,
                                                                                maps.dv);
         } else {
-            const int grid = std::min(items, 2 * nsm);  // persistent: 2 resident CTAs per SM
+            int grid = std::min(items, q.grid_per_sm * nsm);  // persistent: 2 resident CTAs per SM
+            if (const char* e = std::getenv("POD_GRID_CTAS")) grid = std::min(grid, std::max(1, std::atoi(e)));
             pod_fused_kernel<G, kFmt, false><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk,
                                                                                 maps.dv);
         }

@@ -92,6 +92,7 @@ struct pod_plan {
     int64_t smem_bytes = 0;
     double w_prefill = 1.0;  // estimated slot-us per prefill item (POD_POLICY_BALANCED)
     double w_decode = 1.0;   // estimated slot-us per decode item
+    int32_t prefill_sms = 0; // POD_POLICY_PARTITION: SMs whose slots bind prefill first
     pod::WorkspaceLayout ws;
     int32_t* role_log = nullptr;
 };

@@ -14,6 +14,7 @@
 // and then lowers the tasks to the physical CTA tables the sm_100a kernels
 // consume, plus the workspace layout.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -311,6 +312,40 @@ void item_costs(pod_plan& p) {
     p.w_decode = p.dctas.empty() ? 1.0 : bytes / p.dctas.size() / kDecodeBytesPerSlotUs;
 }
 
+// POD_POLICY_PARTITION: how many SMs bind prefill first.  Prefill on x SMs runs
+// at its 2-CTA/SM rate; decode on the other SMs at min(per-SM stream rate, the
+// HBM share); x balances the two finish times.  B200 rates:
+// ~4.6 TFLOP/s of causal prefill per SM (2 CTAs), ~90 GB/s of paged decode per
+// SM (2 CTAs) up to the measured HBM copy bandwidth.
+int32_t partition_prefill_sms(const pod_plan& p) {
+    const int n = p.dev.num_sms > 0 ? p.dev.num_sms : 148;
+    if (const char* e = std::getenv("POD_PART_SMS")) return std::clamp(std::atoi(e), 0, n);  // experiment knob
+    if (p.pctas.empty()) return 0;
+    if (p.dctas.empty()) return n;
+    const double d = p.shape.head_dim;
+    const int group = p.shape.num_q_heads / p.shape.num_kv_heads;
+    double flops = 0, bytes = 0;
+    for (const pod::PrefillCta& c : p.pctas) {
+        const double keys = std::max(0, std::min(c.kv_end, static_cast<int32_t>(p.batch.prefill.position_offset) +
+                                                               c.row_begin + c.rows) - c.kv_begin);
+        flops += 4.0 * d * c.rows * group * keys;
+    }
+    for (const pod::DecodeCta& c : p.dctas) bytes += 4.0 * d * (c.kv_end - c.kv_begin);
+    const double kPrefillFlopsPerSmUs = 4.6e6, kDecodeBytesPerSmUs = 90.0e3, kHbmBytesPerUs = 6.5e6;
+    int best = 1;
+    double best_t = 1e300;
+    for (int x = 1; x < n; ++x) {
+        const double tp = flops / (x * kPrefillFlopsPerSmUs);
+        const double td = bytes / std::min(kHbmBytesPerUs, (n - x) * kDecodeBytesPerSmUs);
+        const double t = std::max(tp, td);
+        if (t < best_t) {
+            best_t = t;
+            best = x;
+        }
+    }
+    return best;
+}
+
 // make_scheduler_state (gpu_sim.hpp:91-107) over PHYSICAL CTA counts.
 void scheduler_ratio(pod_plan& p) {
     const long P = static_cast<long>(p.pctas.size());
@@ -335,6 +370,11 @@ void scheduler_ratio(pod_plan& p) {
         // one prefill CTA per SM (2 slots): the other slot streams decode
         p.prefill_ratio = P > 0 ? 1 : 0;
         p.decode_ratio = 1;
+    } else if (p.opts.policy == POD_POLICY_PARTITION) {
+        p.prefill_ratio = P > 0 ? 1 : 0;
+        p.decode_ratio = D > 0 ? 1 : 0;
+        if (P == 0 && D == 0) p.prefill_ratio = 1;
+        p.prefill_sms = partition_prefill_sms(p);
     } else {
         // proportional share rounded to the per-SM slot count, never starving an op
         const int slots = std::max(2, p.cfg.ctas_per_sm);

@@ -48,9 +48,9 @@ class PodAttention:
                "pod_attn_workspace_init")
         self.role_log: Optional[torch.Tensor] = None
 
-    def enable_role_log(self) -> torch.Tensor:
+    def enable_role_log(self, extra_ints: int = 0) -> torch.Tensor:
         n = int(self.info.num_prefill_ctas + self.info.num_decode_ctas)
-        self.role_log = torch.zeros(max(1, n) * 8, dtype=torch.int32, device=self.device)
+        self.role_log = torch.zeros(max(1, n) * 8 + extra_ints, dtype=torch.int32, device=self.device)
         _check(lib().pod_attn_set_role_log(self.plan.handle, _ptr(self.role_log)), "set_role_log")
         return self.role_log
 

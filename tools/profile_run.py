@@ -31,19 +31,30 @@ def main():
     ap.add_argument("--precision", type=int, default=0)
     a = ap.parse_args()
     hq, hkv, chunk, off, b, ctx = CONFIGS[a.config]
+    b_ = b
     shape = pkg.ModelShape(hq, hkv, 128, math.sqrt(128))
     batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
     wl = build_workload(batch, device="cuda")
     op = PodAttention(batch, options=pkg.PlanOptions(policy=a.policy, tile_mode=a.tile_mode,
                                                      decode_splits=a.decode_splits, precision=a.precision))
-    log = op.enable_role_log() if a.roles else None
+    log = op.enable_role_log(768 * 8) if a.roles else None
     out = op.alloc_outputs()
     for _ in range(a.iters):
         op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=out,
                mode=a.mode)
     torch.cuda.synchronize()
     if log is not None:
-        rec = log.view(-1, 8).cpu().tolist()
+        allrec = log.view(-1, 8).cpu()
+        nrec = int(op.info.num_prefill_ctas + op.info.num_decode_ctas)
+        rec = allrec[:nrec].tolist()
+        tr = allrec[nrec:].tolist()
+        if any(any(x) for x in tr):
+            import os
+            print("trace: t | sfull_wait_begin, sfull_ok, softmax_done(pre pv wait), mma_pfull_seen, mma_vfull_ok, mma_kfull_ok(QK t+2), pv_wait_ok, mma_pv_issued | arrive w0..w3, K(t) issue begin/end, V(t) issue begin/end | mma: pv done(probe), qk issued, qk done(probe)")
+            base = tr[0][0]
+            for t in list(range(0, 12)) + list(range(100, 106)):
+                row = tr[t] + tr[256 + t] + tr[512 + t][:3]
+                print(t, [((x - base) & 0xffffffff) if x else None for x in row])
         t0 = min(r[5] for r in rec)
         rows = [{"sm": r[0], "ticket": r[1], "op": r[2], "id": r[3], "arrival": r[4],
                  "start_us": (r[5] - t0) / 1000.0, "end_us": ((r[6] - t0) % (1 << 31)) / 1000.0} for r in rec]
@@ -55,6 +66,22 @@ def main():
                 print(f"{name}: n={len(rs)} start[min,max]=({min(r['start_us'] for r in rs):.1f},"
                       f"{max(r['start_us'] for r in rs):.1f}) end_max={max(r['end_us'] for r in rs):.1f} "
                       f"dur[p10,p50,p90]=({dur[len(dur)//10]:.1f},{dur[len(dur)//2]:.1f},{dur[9*len(dur)//10]:.1f})")
+        ds = [r for r in rows if r["op"] == 1]
+        ps = [r for r in rows if r["op"] == 0]
+        if ds:
+            item_bytes = b_ * ctx * hkv * 128 * 4 / len(ds)  # bf16 K + V of one decode item
+            rate = sorted(item_bytes / (r["end_us"] - r["start_us"]) / 1e3 for r in ds)
+            print(f"decode item {item_bytes/1e6:.2f} MB; per-CTA GB/s p10/p50/p90 = "
+                  f"{rate[len(rate)//10]:.1f}/{rate[len(rate)//2]:.1f}/{rate[9*len(rate)//10]:.1f}")
+            if ps:
+                t_p = max(r["end_us"] for r in ps)
+                t_end = max(r["end_us"] for r in rows)
+                done_b = sum(item_bytes * max(0.0, min(1.0, (t_p - r["start_us"]) / (r["end_us"] - r["start_us"])))
+                             for r in ds if r["start_us"] < t_p)
+                print(f"prefill drains at {t_p:.1f} us (end {t_end:.1f}); decode during prefill phase "
+                      f"{done_b/1e9:.3f} GB = {done_b/t_p/1e3:.0f} GB/s; after: "
+                      f"{(len(ds)*item_bytes-done_b)/1e9:.3f} GB in {t_end-t_p:.1f} us = "
+                      f"{(len(ds)*item_bytes-done_b)/max(t_end-t_p,1e-3)/1e3:.0f} GB/s")
         # concurrency per SM
         import collections
         bysm = collections.defaultdict(list)
