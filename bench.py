@@ -316,7 +316,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="pod", choices=["pod", "reference"])
-    ap.add_argument("--policy", type=int, default=3)
+    ap.add_argument("--policy", type=int, default=8, help="POD_POLICY_*: 8 = AUTO (default), 7 = WARPSPEC, 3 = COMPLEMENT")
     ap.add_argument("--tile-mode", type=int, default=1)
     ap.add_argument("--precision", type=int, default=0, help="0: prefill P as bf16 hi+lo (default), 1: single bf16")
     ap.add_argument("--decode-splits", type=int, default=0)
@@ -420,7 +420,7 @@ def main():
         "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
                  "prefill_splits": info.prefill_splits, "decode_splits": info.decode_splits,
                  "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
-                 "policy": args.policy, "split_wave_cap": info.config.split_wave_cap, "prefill_p": {0: "bf16 hi+lo", 1: "bf16"}[args.precision]},
+                 "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_p": {0: "bf16 hi+lo", 1: "bf16"}[args.precision]},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": "pod_fused_kernel (+merge)", "peak_source": pk["source"]},

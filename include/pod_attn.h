@@ -125,9 +125,15 @@ enum {
     POD_POLICY_BALANCED = 5,     /* bind the role with more estimated remaining slot-time
                                     (planner per-item costs), so both pools drain together;
                                     ties go to the role not resident on the SM */
-    POD_POLICY_PARTITION = 6     /* SM-aware spatial split: prefill_sms SMs (spread evenly
+    POD_POLICY_PARTITION = 6,    /* SM-aware spatial split: prefill_sms SMs (spread evenly
                                     over the SM ids) bind prefill on both slots, the others
                                     decode; an exhausted pool switches to the other */
+    POD_POLICY_WARPSPEC = 7,     /* one CTA per SM hosting a prefill engine (two 128-row
+                                    M-blocks, Q/S/P/O in TMEM) and a decode warp group side
+                                    by side; each binds items from its pool at runtime */
+    POD_POLICY_AUTO = 8          /* default: WARPSPEC when the decode share of the serial
+                                    time is >= 0.25 (decode-heavy batches), else COMPLEMENT
+                                    (the plan records the resolved policy) */
 };
 
 enum {
@@ -166,6 +172,8 @@ typedef struct pod_plan_info {
     int64_t workspace_bytes;
     int32_t num_merge_rows_prefill; /* (row, q head) pairs needing a split merge */
     int32_t num_merge_rows_decode;
+    int32_t policy;             /* the POD_POLICY_* the plan runs (POD_POLICY_AUTO resolved) */
+    int32_t pad_;
 } pod_plan_info;
 
 typedef struct pod_plan pod_plan;

@@ -21,7 +21,7 @@ STATUS_NAMES = {
 POD_KV_HND, POD_KV_NHD = 0, 1
 POD_DTYPE_BF16, POD_DTYPE_FP16 = 0, 1
 POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT, POD_POLICY_SLOTS, \
-    POD_POLICY_BALANCED, POD_POLICY_PARTITION = 0, 1, 2, 3, 4, 5, 6
+    POD_POLICY_BALANCED, POD_POLICY_PARTITION, POD_POLICY_WARPSPEC, POD_POLICY_AUTO = 0, 1, 2, 3, 4, 5, 6, 7, 8
 POD_TILE_REFERENCE, POD_TILE_B200 = 0, 1
 POD_PRECISION_SPLIT, POD_PRECISION_FAST = 0, 1
 
@@ -78,7 +78,7 @@ class pod_plan_info(C.Structure):
                 ("decode_splits", C.c_int64), ("prefill_ratio", C.c_int64),
                 ("decode_ratio", C.c_int64), ("smem_bytes", C.c_int64),
                 ("workspace_bytes", C.c_int64), ("num_merge_rows_prefill", C.c_int32),
-                ("num_merge_rows_decode", C.c_int32)]
+                ("num_merge_rows_decode", C.c_int32), ("policy", C.c_int32), ("pad_", C.c_int32)]
 
 
 # (name, restype, argtypes) for every symbol include/pod_attn.h declares.

@@ -39,7 +39,7 @@ def _stale(target: Path, sources) -> bool:
 
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     sources = [CSRC / "pod_attn.cu", CSRC / "pod_plan.cpp"]
-    deps = sources + [CSRC / "pod_internal.h", CSRC / "sm100_ptx.cuh", ROOT / "include" / "pod_attn.h"]
+    deps = sources + sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "pod_attn.h"]
     if not force and not _stale(LIB, deps):
         return LIB
     tmp = LIB.with_suffix(".so.tmp")

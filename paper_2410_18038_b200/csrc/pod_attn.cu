@@ -189,12 +189,12 @@ __device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t tmem_
 //            hi = top 16 bits of p, lo = p - hi (exact in fp32) truncated; hi in
 //            [0,32), lo in [32,64); hi + lo keeps ~15 mantissa bits
 //   kMode 2: hi + lo rounded to nearest (fp16 inputs)
-template <int kFmt, int kMode>
-__device__ __forceinline__ float softmax_p_row(const float (&s)[kKvTile], float sl2, float neg_m, uint32_t s_addr) {
+template <int kFmt, int kMode, int kN = kKvTile>
+__device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, float neg_m, uint32_t s_addr) {
     const float2 sl2v = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
     float2 lsum2 = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
+    for (int hf = 0; hf < kN / 32; ++hf) {
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
@@ -216,7 +216,7 @@ __device__ __forceinline__ float softmax_p_row(const float (&s)[kKvTile], float 
             }
         }
         ptx::tmem_st16(s_addr + 16 * hf, hi);
-        if constexpr (kMode != 0) ptx::tmem_st16(s_addr + 32 + 16 * hf, lo);
+        if constexpr (kMode != 0) ptx::tmem_st16(s_addr + kN / 2 + 16 * hf, lo);
     }
     return lsum2.x + lsum2.y;
 }
@@ -241,14 +241,30 @@ __device__ __forceinline__ BlockRange prefill_block(const RunParams& p, const Pr
     return br;
 }
 
-// Issue the 8 TMA boxes (4 pages x 2 swizzle columns) of one 64-key tile.
+// Page ids of one block-table row.  (A per-lane shuffle cache of the ids measured
+// slower than these direct L1-resident loads in the producer warp: 483 vs 405 us
+// prefill-alone, C2 -- so the lookup stays a plain __ldg.)
+struct PageIds {
+    const int32_t* row;
+    int n;  // pages in the row
+    __device__ __forceinline__ void init(const int32_t* r, int npages, int /*first*/) {
+        row = r;
+        n = npages;
+    }
+    __device__ __forceinline__ int get(int j) const { return __ldg(row + j); }
+};
+
+// Issue the 8 TMA boxes (4 pages x 2 swizzle columns) of one 64-key tile
+// (warp-uniform call; page ids from the warp's cache).
 __device__ __forceinline__ void prefill_load_kv_tile(const RunParams& p, const CUtensorMap* tm,
                                                      uint32_t dst, uint32_t bar, int kt, int kv_head,
-                                                     int pbeg, int npages) {
+                                                     PageIds& ids) {
+    int phys_pg[kKvTile / 16];
+#pragma unroll
+    for (int pg = 0; pg < kKvTile / 16; ++pg) phys_pg[pg] = ids.get(min(kt / 16 + pg, ids.n - 1));
 #pragma unroll
     for (int pg = 0; pg < kKvTile / 16; ++pg) {
-        const int lp = min(kt / 16 + pg, npages - 1);
-        const int phys = __ldg(p.page_indices + pbeg + lp);
+        const int phys = phys_pg[pg];
 #pragma unroll
         for (int dh = 0; dh < 2; ++dh) {
             const uint32_t d = dst + dh * (kKvTile * 128) + pg * 2048;
@@ -321,10 +337,17 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
         // ------------------------------------------------ TMA producer --
         // (warp-uniform loop; single-thread instructions are elect-predicated)
         {
+            PageIds pk, pvi;
+            pk.init(p.page_indices + pbeg, npages, (job.kv_begin / 16));
+            pvi.init(p.page_indices + pbeg, npages, (job.kv_begin / 16));
             int g = g0, qb = qb0;
             for (int b = 0; b < nblocks; ++b) {
                 const BlockRange br = prefill_block(p, job, b);
                 if (br.nt == 0) continue;
+                if (b > 0) {  // every block restarts at the item's first key
+                    pk.init(p.page_indices + pbeg, npages, br.kt0 / 16);
+                    pvi.init(p.page_indices + pbeg, npages, br.kt0 / 16);
+                }
                 if (qb > 0) ptx::mbar_wait(b_qempty, (qb - 1) & 1);
                 ptx::mbar_arrive_expect_tx_elect(b_qfull, kQBytes);
                 ptx::tma_load_3d_elect(sQ, tmq, b_qfull, 0, job.kv_head * G, br.r0);
@@ -337,7 +360,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t, 4);
                         ptx::mbar_arrive_expect_tx_elect(b_kfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmk, sK + st * kKvStageBytes, b_kfull + 8 * st,
-                                             br.kt0 + t * kKvTile, job.kv_head, pbeg, npages);
+                                             br.kt0 + t * kKvTile, job.kv_head, pk);
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t, 5);
                     }
                     if (t > 0) {  // V of tile t-1
@@ -346,7 +369,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t - 1, 6);
                         ptx::mbar_arrive_expect_tx_elect(b_vfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
-                                             br.kt0 + (t - 1) * kKvTile, job.kv_head, pbeg, npages);
+                                             br.kt0 + (t - 1) * kKvTile, job.kv_head, pvi);
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t - 1, 7);
                     }
                 }
@@ -603,20 +626,23 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
                 const bool hasB = 2 * pr + 1 < nblocks;
                 const BlockRange ra = prefill_block(p, job, 2 * pr);
                 const int nt = hasB ? prefill_block(p, job, 2 * pr + 1).nt : ra.nt;
+                PageIds pk, pvi;
+                pk.init(p.page_indices + pbeg, npages, ra.kt0 / 16);
+                pvi.init(p.page_indices + pbeg, npages, ra.kt0 / 16);
                 for (int t = 0; t <= nt && nt > 0; ++t) {
                     if (t < nt) {
                         const int gg = g + t, st = gg & 1;
                         if (gg >= 2) ptx::mbar_wait(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
                         ptx::mbar_arrive_expect_tx_elect(b_kfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmk, sK + st * kKvStageBytes, b_kfull + 8 * st,
-                                             ra.kt0 + t * kKvTile, job.kv_head, pbeg, npages);
+                                             ra.kt0 + t * kKvTile, job.kv_head, pk);
                     }
                     if (t > 0) {
                         const int gg = g + t - 1, st = gg & 1;
                         if (gg >= 2) ptx::mbar_wait(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
                         ptx::mbar_arrive_expect_tx_elect(b_vfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
-                                             ra.kt0 + (t - 1) * kKvTile, job.kv_head, pbeg, npages);
+                                             ra.kt0 + (t - 1) * kKvTile, job.kv_head, pvi);
                     }
                 }
                 g += nt;
@@ -929,24 +955,30 @@ __device__ __forceinline__ void mma16816a(float (&d)[4], const uint32_t (&a)[4],
 // Lane (g, t) = (lane / 4, lane % 4) holds scores of keys g, g + 8 for heads
 // 2t, 2t + 1; per-head max / sum are shuffle reductions over g.  The 4 warp
 // partials are LSE-merged through shared memory at the end.
-template <int G, int kFmt>
+// Decode group geometry: kW warps, each with a kS-stage ring of K+V head-pages.
+// `ring0` / `bars0`: shared addresses of warp 0's ring and barriers; `red` aliases
+// the ring region for the in-group merge; `bar_id` names the group's barrier.
+template <int G, int kFmt, int kW, int kS>
 __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUtensorMap* tv, int cta_id,
-                            uint8_t* smem, int& dpos) {
+                            int warp, uint32_t ring0, uint32_t bars0, float* red, int bar_id, int& dpos) {
     static_assert(G <= 8, "decode: G query heads of one KV head are the N = 8 MMA columns");
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
-    if (warp >= kDecWarpsK) return;
+    constexpr int kDecStages = kS;
+    const int lane = threadIdx.x & 31;
+    const int tid = warp * 32 + lane;
     const DecodeCta job = p.dctas[cta_id];
     const int len = job.kv_end - job.kv_begin;
-    const int base = len / kDecWarpsK, rem = len % kDecWarpsK;
+    const int base = len / kW, rem = len % kW;
     const int wb = job.kv_begin + warp * base + min(warp, rem);
     const int we = wb + base + (warp < rem ? 1 : 0);
     const int h = job.kv_head;
     const int gq = lane >> 2, tq = lane & 3;
-    const uint32_t sbase = ptx::smem_u32(smem);
-    const uint32_t ring = sbase + warp * kDecWarpBytes;
-    const uint32_t bars = sbase + kOffDecBar + warp * (kDecStages * 8);
+    const uint32_t ring = ring0 + warp * (kS * kDecStageBytes);
+    const uint32_t bars = bars0 + warp * (kS * 8);
     const bool h0ok = 2 * tq < G, h1ok = 2 * tq + 1 < G;  // this lane's two head columns exist
+    // G = 2, 4: P lo is packed into the free head columns (lane t ^ G/2)
+    constexpr bool kPack = G == 2 || G == 4;
+    constexpr int kPackXor = G / 2;
+    const bool lo_lane = kPack && tq >= G / 2;
 
     // B fragments of Q^T (N = heads): head gq, d = 16 ks + 2t (+8); zero for heads >= G
     using elem_t = uint16_t;
@@ -1037,28 +1069,53 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
         const float p10 = h0ok ? ptx::ex2(x[2] - n0) : 0.f, p11 = h1ok ? ptx::ex2(x[3] - n1) : 0.f;
         l0 = l0 * f0 + (p00 + p10);
         l1 = l1 * f1 + (p01 + p11);
-        if (!__all_sync(0xffffffffu, f0 == 1.f && f1 == 1.f)) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                o[j][0] *= f0;
-                o[j][1] *= f1;
-                o[j][2] *= f0;
-                o[j][3] *= f1;
-            }
-        }
         // P^T as the B operand: transpose the two 8x8 (key x head) blocks; hi + lo parts
         const uint32_t h0 = pack2<kFmt>(p00, p01), h1 = pack2<kFmt>(p10, p11);
         const float2 u0 = unpack2<kFmt>(h0), u1 = unpack2<kFmt>(h1);
         const uint32_t q0 = pack2<kFmt>(p00 - u0.x, p01 - u0.y), q1 = pack2<kFmt>(p10 - u1.x, p11 - u1.y);
-        const uint32_t bh0 = movmatrix_t(h0), bh1 = movmatrix_t(h1);
-        const uint32_t bl0 = movmatrix_t(q0), bl1 = movmatrix_t(q1);
-        // ---- O^T (128 d x 8 heads) += V^T P^T: one MMA per 16-d tile (x2 for hi/lo)
+        if constexpr (kPack) {
+            // G <= 4: the lo parts ride in the unused head columns [G, 2G) (lanes
+            // t ^ G/2), so one MMA per d-tile accumulates O_hi and O_lo side by side
+            const float f0s = __shfl_xor_sync(0xffffffffu, f0, kPackXor), f1s = __shfl_xor_sync(0xffffffffu, f1, kPackXor);
+            const uint32_t q0s = __shfl_xor_sync(0xffffffffu, q0, kPackXor), q1s = __shfl_xor_sync(0xffffffffu, q1, kPackXor);
+            const float rf0 = lo_lane ? f0s : f0, rf1 = lo_lane ? f1s : f1;
+            if (!__all_sync(0xffffffffu, rf0 == 1.f && rf1 == 1.f)) {
 #pragma unroll
-        for (int md = 0; md < 8; ++md) {
-            uint32_t a[4];  // A = V^T: rows d 16md..+7 / +8..+15, cols keys 0-7 / 8-15
-            ldsm_x4_t(vst + page_off((lm >> 1) * 8 + lr, 2 * md + (lm & 1)), a[0], a[1], a[2], a[3]);
-            mma16816a<kFmt>(o[md], a, bh0, bh1);
-            mma16816a<kFmt>(o[md], a, bl0, bl1);
+                for (int j = 0; j < 8; ++j) {
+                    o[j][0] *= rf0;
+                    o[j][1] *= rf1;
+                    o[j][2] *= rf0;
+                    o[j][3] *= rf1;
+                }
+            }
+            const uint32_t b0 = movmatrix_t(lo_lane ? q0s : h0), b1 = movmatrix_t(lo_lane ? q1s : h1);
+            // ---- O^T (128 d x [hi heads | lo heads]) += V^T P^T: one MMA per 16-d tile
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+                uint32_t a[4];  // A = V^T: rows d 16md..+7 / +8..+15, cols keys 0-7 / 8-15
+                ldsm_x4_t(vst + page_off((lm >> 1) * 8 + lr, 2 * md + (lm & 1)), a[0], a[1], a[2], a[3]);
+                mma16816a<kFmt>(o[md], a, b0, b1);
+            }
+        } else {
+            if (!__all_sync(0xffffffffu, f0 == 1.f && f1 == 1.f)) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    o[j][0] *= f0;
+                    o[j][1] *= f1;
+                    o[j][2] *= f0;
+                    o[j][3] *= f1;
+                }
+            }
+            const uint32_t bh0 = movmatrix_t(h0), bh1 = movmatrix_t(h1);
+            const uint32_t bl0 = movmatrix_t(q0), bl1 = movmatrix_t(q1);
+            // ---- O^T (128 d x 8 heads) += V^T P^T: one MMA per 16-d tile (x2 for hi/lo)
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+                uint32_t a[4];  // A = V^T: rows d 16md..+7 / +8..+15, cols keys 0-7 / 8-15
+                ldsm_x4_t(vst + page_off((lm >> 1) * 8 + lr, 2 * md + (lm & 1)), a[0], a[1], a[2], a[3]);
+                mma16816a<kFmt>(o[md], a, bh0, bh1);
+                mma16816a<kFmt>(o[md], a, bl0, bl1);
+            }
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) sc[c] = scn[c];
@@ -1076,16 +1133,22 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
         }
     }
     dpos += npg;
+    if constexpr (kPack) {  // O = O_hi + O_lo (hi lanes keep the sum)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) o[j][c] += __shfl_xor_sync(0xffffffffu, o[j][c], kPackXor);
+    }
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
         l0 += __shfl_xor_sync(0xffffffffu, l0, off);
         l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
-    // in-CTA merge of the 4 virtual CTAs (LSE merge, attention.hpp:294-326);
-    // reuses warp 0's ring (every warp is past its last TMA wait).
+    // in-group merge of the warps' ranges (LSE merge, attention.hpp:294-326);
+    // reuses the ring region (every warp is past its last TMA wait).
     constexpr int kStride = kHeadDim + 4;
-    float* red = reinterpret_cast<float*>(smem);
-    ptx::named_bar_sync(2, kDecWarpsK * 32);
+    static_assert(kW * 8 * (kHeadDim + 4) * 4 <= kW * kS * kDecStageBytes, "merge scratch fits the rings");
+    ptx::named_bar_sync(bar_id, kW * 32);
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
         const int head = 2 * tq + hh;
@@ -1102,18 +1165,18 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
             }
         }
     }
-    ptx::named_bar_sync(2, kDecWarpsK * 32);
-    for (int idx = tid; idx < G * kHeadDim; idx += kDecWarpsK * 32) {
+    ptx::named_bar_sync(bar_id, kW * 32);
+    for (int idx = tid; idx < G * kHeadDim; idx += kW * 32) {
         const int g = idx / kHeadDim, d = idx % kHeadDim;
-        float mw[kDecWarpsK], M = -INFINITY;
+        float mw[kW], M = -INFINITY;
 #pragma unroll
-        for (int w = 0; w < kDecWarpsK; ++w) {
+        for (int w = 0; w < kW; ++w) {
             mw[w] = red[(w * G + g) * kStride + kHeadDim];
             M = fmaxf(M, mw[w]);
         }
         float L = 0.f, acc = 0.f;
 #pragma unroll
-        for (int w = 0; w < kDecWarpsK; ++w) {
+        for (int w = 0; w < kW; ++w) {
             const float wt = ptx::ex2(mw[w] - M);  // empty warp: m = -inf -> 0
             L += red[(w * G + g) * kStride + kHeadDim + 1] * wt;
             acc += red[(w * G + g) * kStride + d] * wt;
@@ -1351,7 +1414,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             else
                 prefill_item<kFmt>(p, &tmq, &tmk, &tmv, id, smem, tmem, ps);
         } else {
-            decode_item<G, kFmt>(p, &tdk, &tdv, id, smem, dpos);
+            if (warp < kDecWarpsK)
+                decode_item<G, kFmt, kDecWarpsK, kDecStages>(p, &tdk, &tdv, id, warp, sbase, sbase + kOffDecBar,
+                                                             reinterpret_cast<float*>(smem), 2, dpos);
         }
         ptx::tc_fence_before();
         __syncthreads();
@@ -1385,6 +1450,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
     }
 }
+
+#include "pod_sm.cuh"
 
 __global__ void gather_probe_kernel(const uint16_t* pool, int layout, int hkv, const int32_t* indptr,
                                     const int32_t* indices, int req, int ctx, uint16_t* out) {
@@ -1430,6 +1497,7 @@ pod_status cuda_fail(cudaError_t e, const char* where) {
 }
 
 int64_t fused_smem_bytes() { return kSmemBytes; }
+int64_t sm_smem_bytes() { return sm3::kSmem; }
 
 struct Maps {
     CUtensorMap q, k, v;  // prefill role: SW128 boxes of 64 d x 16 tokens, Q boxes of 64 d x 128 rows
@@ -1589,10 +1657,17 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
         attr_done = true;
     }
     const int nsm = plan->dev.num_sms;
+    static bool attr_sm = false;
+    if (!attr_sm) {
+        cudaFuncSetAttribute(pod_sm_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3::kSmem);
+        attr_sm = true;
+    }
     auto launch = [&](const RunParams& q) {
         const int items = q.num_pctas + q.num_dctas;
         if (items <= 0) return;
-        if (q.policy == POD_POLICY_SLOTS) {
+        if (q.policy == POD_POLICY_WARPSPEC) {
+            pod_sm_kernel<G, kFmt><<<nsm, sm3::kThreads, sm3::kSmem, s>>>(q, maps.k, maps.v, maps.dk, maps.dv);
+        } else if (q.policy == POD_POLICY_SLOTS) {
             const int grid = std::min(items, q.num_dctas == 0 ? nsm : 2 * nsm);  // prefill slots only / 2 per SM
             pod_fused_kernel<G, kFmt, true><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk,
                                                                                maps.dv);

@@ -15,6 +15,7 @@ constexpr int kHeadDim = 128;       // only d = 128 is compiled (all BASELINE co
 constexpr int kMBlock = 128;        // tcgen05 M: packed (row, q-head) rows per prefill block
 constexpr int kKvTile = 64;         // prefill keys per tcgen05 N tile (4 pages of 16)
 constexpr int kDecodeWarps = 4;     // virtual decode CTAs per physical CTA
+constexpr int kSmDecodeWarps = 6;   // decode warps of the warp-specialised kernel (pod_sm.cuh)
 constexpr int kPrefillWarps = 4;    // softmax warps (one TMEM lane quadrant each)
 constexpr int kThreads = 192;       // 4 softmax warps + 1 TMA-producer warp + 1 MMA warp
 constexpr int kMaxSms = 1024;       // sm counter slots (sized for %nsmid, not %smid density)
@@ -100,5 +101,7 @@ struct pod_plan {
 namespace pod {
 // Dynamic shared memory of the fused / prefill kernel (defined in pod_attn.cu).
 int64_t fused_smem_bytes();
+// Dynamic shared memory of the warp-specialised one-CTA-per-SM kernel.
+int64_t sm_smem_bytes();
 void set_last_error(const std::string& s);
 }  // namespace pod

@@ -245,15 +245,24 @@ void lower(pod_plan& p) {
     // exactly (4 warps x split_ranges(ctx, 4)).
     const int64_t parents = static_cast<int64_t>(p.decode_ctx.size()) * s.num_kv_heads;
     int64_t splits = p.opts.decode_splits;
+    const bool warpspec = p.opts.policy == POD_POLICY_WARPSPEC;
     if (splits <= 0) {
-        const int64_t slots = static_cast<int64_t>(p.dev.num_sms) * 2;
-        splits = parents >= slots || parents == 0 ? 1 : ceil_div(slots, parents);
+        if (warpspec) {
+            // one decode group per SM: about 6 items per group keeps the tail (the
+            // last items finishing on a few SMs) short
+            const int64_t target = static_cast<int64_t>(p.dev.num_sms) * 6;
+            splits = parents == 0 ? 1 : ceil_div(target, parents);
+        } else {
+            const int64_t slots = static_cast<int64_t>(p.dev.num_sms) * 2;
+            splits = parents >= slots || parents == 0 ? 1 : ceil_div(slots, parents);
+        }
     }
     int64_t min_ctx = INT64_MAX;
     for (int64_t c : p.decode_ctx) min_ctx = std::min(min_ctx, c);
     if (!p.decode_ctx.empty()) {
         // each warp keeps at least one page of keys
-        const int64_t cap = std::max<int64_t>(1, min_ctx / (pod::kDecodeWarps * 16));
+        const int warps = warpspec ? pod::kSmDecodeWarps : pod::kDecodeWarps;
+        const int64_t cap = std::max<int64_t>(1, min_ctx / (warps * 16));
         if (p.opts.decode_splits <= 0) splits = std::min(splits, cap);
     }
     p.decode_splits = std::max<int64_t>(1, splits);
@@ -370,6 +379,11 @@ void scheduler_ratio(pod_plan& p) {
         // one prefill CTA per SM (2 slots): the other slot streams decode
         p.prefill_ratio = P > 0 ? 1 : 0;
         p.decode_ratio = 1;
+    } else if (p.opts.policy == POD_POLICY_WARPSPEC) {
+        // both roles on every SM for as long as both pools have work
+        p.prefill_ratio = P > 0 ? 1 : 0;
+        p.decode_ratio = D > 0 ? 1 : 0;
+        if (P == 0 && D == 0) p.prefill_ratio = 1;
     } else if (p.opts.policy == POD_POLICY_PARTITION) {
         p.prefill_ratio = P > 0 ? 1 : 0;
         p.decode_ratio = D > 0 ? 1 : 0;
@@ -423,16 +437,40 @@ pod_tile_config b200_tile_config(const pod_plan& p) {
     pod_tile_config c = make_tile_config(2);
     const int group = p.shape.num_q_heads / p.shape.num_kv_heads;
     // slots policy: two 128-row M-blocks per prefill item (ping-pong engine)
-    const int rows = (p.opts.policy == POD_POLICY_SLOTS ? 2 : 1) * pod::kMBlock;
+    const bool two_blocks = p.opts.policy == POD_POLICY_SLOTS || p.opts.policy == POD_POLICY_WARPSPEC;
+    const int rows = (two_blocks ? 2 : 1) * pod::kMBlock;
     c.prefill_tile_q = std::max(1, rows / group);
     c.tile_kv = pod::kKvTile;
-    c.shared_mem_per_cta = static_cast<double>(pod::fused_smem_bytes());
+    c.shared_mem_per_cta = static_cast<double>(p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes()
+                                                                                   : pod::fused_smem_bytes());
     c.virtual_decode = 1;
     return c;
 }
 
+// Decode share of the serial time from algorithmic work at measured B200 rates
+// (prefill ~0.68 PFLOP/s with the hi+lo P split, paged decode ~6.6 TB/s).
+double decode_share(const pod_plan& p) {
+    if (!p.batch.has_prefill) return 1.0;
+    if (p.decode_ctx.empty()) return 0.0;
+    const auto& pf = p.batch.prefill;
+    const double C = static_cast<double>(pf.chunk_size), off = static_cast<double>(pf.position_offset);
+    const double flops = 4.0 * p.shape.head_dim * p.shape.num_q_heads * (C * off + C * (C + 1) / 2.0);
+    double bytes = 0;
+    for (int64_t c : p.decode_ctx) bytes += 4.0 * c * p.shape.num_kv_heads * p.shape.head_dim;
+    const double t_p = flops / 0.68e15, t_d = bytes / 6.6e12;
+    return t_d / (t_p + t_d);
+}
+
 void build(pod_plan& p) {
     validate_batch(p);
+    if (p.opts.policy == POD_POLICY_AUTO) {
+        // measured on B200: the one-CTA-per-SM kernel wins once the
+        // decode stream dominates (it keeps HBM saturated next to the prefill);
+        // prefill-heavy batches run faster on two POD CTAs per SM
+        // (C2 at B = 8/16/32/64: 508 vs 542, 554 vs 557, 592 vs 671, 738 vs 800 us;
+        // C1: 82 vs 89 us -- one-CTA-per-SM vs two-CTA POD, best split caps)
+        p.opts.policy = decode_share(p) >= 0.25 ? POD_POLICY_WARPSPEC : POD_POLICY_COMPLEMENT;
+    }
     if (p.opts.tile_override) {
         p.cfg = *p.opts.tile_override;
         if (p.cfg.prefill_tile_q < 1 || p.cfg.tile_kv < 1 || p.cfg.warps_per_cta < 1)
@@ -445,14 +483,13 @@ void build(pod_plan& p) {
         // time from algorithmic work at measured B200 rates (prefill ~0.68 PFLOP/s,
         // paged decode ~6.6 TB/s): > 0.55 -> 2 waves (reference rule), > 0.4 -> 4, else 8.
         if (p.opts.split_wave_cap <= 0 && p.batch.has_prefill && !p.decode_ctx.empty()) {
-            const auto& pf = p.batch.prefill;
-            const double C = static_cast<double>(pf.chunk_size), off = static_cast<double>(pf.position_offset);
-            const double flops = 4.0 * p.shape.head_dim * p.shape.num_q_heads * (C * off + C * (C + 1) / 2.0);
-            double bytes = 0;
-            for (int64_t c : p.decode_ctx) bytes += 4.0 * c * p.shape.num_kv_heads * p.shape.head_dim;
-            const double t_p = flops / 0.68e15, t_d = bytes / 6.6e12;
-            const double share = t_d / (t_p + t_d);
-            p.cfg.split_wave_cap = share > 0.55 ? 2 : (share > 0.4 ? 4 : 8);
+            const double share = decode_share(p);
+            if (p.opts.policy == POD_POLICY_WARPSPEC)
+                // one prefill engine per SM keeps working while the decode runs;
+                // KV splits only pay their merge (measured: cap 1 best for C1, C2)
+                p.cfg.split_wave_cap = 1;
+            else
+                p.cfg.split_wave_cap = share > 0.55 ? 2 : (share > 0.4 ? 4 : 8);
         }
     } else {
         if (p.opts.ctas_per_sm != 0) {
@@ -473,7 +510,7 @@ void build(pod_plan& p) {
     lower(p);
     item_costs(p);
     scheduler_ratio(p);
-    p.smem_bytes = pod::fused_smem_bytes();
+    p.smem_bytes = p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes() : pod::fused_smem_bytes();
     layout_workspace(p);
 }
 
@@ -494,7 +531,7 @@ void pod_device_reference_default(pod_device* out) {
 
 void pod_options_default(pod_options* out) {
     std::memset(out, 0, sizeof(*out));
-    out->policy = POD_POLICY_COMPLEMENT;
+    out->policy = POD_POLICY_AUTO;
     out->tile_mode = POD_TILE_B200;
     out->ctas_per_sm = 0;
     out->virtual_decode = -1;
@@ -557,6 +594,7 @@ pod_status pod_attn_plan_get_info(const pod_plan* p, pod_plan_info* out) {
     out->workspace_bytes = static_cast<int64_t>(p->ws.total);
     out->num_merge_rows_prefill = p->merge_rows_prefill;
     out->num_merge_rows_decode = p->merge_rows_decode;
+    out->policy = p->opts.policy;
     return POD_OK;
 }
 

@@ -1,0 +1,527 @@
+// pod_sm.cuh -- the warp-specialised POD kernel (POD_POLICY_WARPSPEC): one CTA per
+// SM that owns the whole SM (227 KB smem, 512 TMEM columns, 16 warps) and runs a
+// prefill engine and a decode engine side by side, each binding work items from
+// its own pool at runtime.  Included by pod_attn.cu (uses its helpers).
+//
+//   warps 0-3   softmax of prefill M-block A   (TMEM lane quadrant = warp % 4)
+//   warps 4-7   softmax of prefill M-block B
+//   warp  8     prefill TMA producer (K/V tiles through the page table)
+//   warp  9     prefill MMA issuer: S = Q K^T and O += P V, both TS-MMAs (Q, P in TMEM)
+//   warps 10-15 decode group: 6 warps stream one (request, KV head, split) item,
+//               each through its own TMA ring of head-pages, LSE-merged in smem
+//
+// Why: a decode CTA co-resident with a prefill CTA is bounded by the shared
+// memory it can keep in flight (~96 KB ring -> ~34 GB/s per SM next to a prefill
+// CTA); with one CTA per SM the prefill keeps Q, S, P and O in TMEM and
+// needs only 64 KB of K/V stages, and the decode group gets 144 KB of rings.  The
+// prefill engine runs two 128-row M-blocks over the same K/V tiles (half the K/V
+// traffic per row), ping-ponging the tensor core between the blocks' softmax.
+//
+// Role binding is still SM-aware and dynamic: every SM hosts both roles for as
+// long as both pools have work (the placement the POD scheduler aims for,
+// PAPER.md:379), an engine whose pool is exhausted retires, and the claims are
+// atomic tickets on the same counters (gpu_sim.hpp:114-131).
+#pragma once
+
+namespace sm3 {
+#ifndef POD_SM_DUAL_MMA
+#define POD_SM_DUAL_MMA 0
+#endif
+#ifndef POD_SM_DEC_WARPS
+#define POD_SM_DEC_WARPS (6 - POD_SM_DUAL_MMA)
+#endif
+#ifndef POD_SM_DEC_STAGES
+#define POD_SM_DEC_STAGES 3
+#endif
+constexpr int kDW = POD_SM_DEC_WARPS;   // decode warps
+static_assert(POD_SM_DUAL_MMA || kDW == kSmDecodeWarps, "planner's decode-warp count");
+constexpr int kDS = POD_SM_DEC_STAGES;  // ring stages per decode warp
+// With POD_SM_DUAL_MMA, warp 9 issues block A's MMAs and warp 10 block B's (each
+// block's chain in its own issuing thread); by default warp 9 issues both and the
+// sixth decode warp takes warp 10's place (measured faster fused).
+constexpr bool kDualMma = POD_SM_DUAL_MMA != 0;
+constexpr int kProdWarp = 8, kMmaWarp = 9, kMmaWarpB = kDualMma ? 10 : 9, kDecWarp0 = kDualMma ? 11 : 10;
+constexpr int kPrefillThreads = kDecWarp0 * 32;
+constexpr int kThreads = (kDecWarp0 + kDW) * 32;
+// Prefill K/V tiles of 32 keys (2 pages): S is double-buffered per block inside
+// the block's 64 TMEM columns, so QK_X(t+1) runs while the softmax of tile t does.
+constexpr int kTN = 32;
+constexpr int kNS = 4;                                         // K and V ring stages
+constexpr uint32_t kStage = kTN * kHeadDim * 2;                // 8 KB: [d-half][32 keys][64 d], SW128
+constexpr uint32_t kOffKs = 0;
+constexpr uint32_t kOffVs = kNS * kStage;
+constexpr uint32_t kOffDec = 2 * kNS * kStage;                 // decode rings (64 KB in)
+constexpr uint32_t kOffBars = kOffDec + kDW * kDS * kDecStageBytes;
+// prefill mbarriers: 0 qA, 1 qB, 2-5 k_full, 6-9 k_empty, 10-13 v_full, 14-17 v_empty,
+// 18-19 sA[2], 20-21 sB[2], 22-23 pA[2], 24-25 pB[2], 26-27 pvA[2], 28-29 pvB[2]
+// (k_empty / v_empty take two arrivals: one commit per block's issuing thread)
+// (pv per S buffer: a waiter is never more than one completion behind on a
+// barrier, so parity waits stay unambiguous even when the softmax skips them)
+constexpr int kNumBars = 30;
+constexpr uint32_t kOffDecBars = kOffBars + kNumBars * 8;
+constexpr uint32_t kOffMisc = kOffDecBars + kDW * kDS * 8;     // tmem slot, claim slots
+constexpr uint32_t kSmem = kOffMisc + 64;
+static_assert(kSmem <= 232448, "one CTA per SM: <= 227 KB dynamic smem");
+static_assert(kOffDec % 1024 == 0 && kDecStageBytes % 1024 == 0, "SW128 stages are 1024-aligned");
+// TMEM columns (512): Q_A, Q_B (bf16 pairs), S_A[2], S_B[2] (fp32 / P over S), O_A, O_B
+constexpr uint32_t kQA = 0, kQB = 64, kSA = 128, kSB = 192, kOA = 256, kOB = 384;
+
+struct PfState {
+    int g = 0;            // K/V tiles issued (stage = g % kNS, phase = (g / kNS) & 1)
+    int n[2] = {0, 0};    // tiles per block (S buffer = n & 1; s/p/pv phases (n >> 1) & 1)
+    int nq[2] = {0, 0};   // Q loads per block (q_full phases)
+};
+
+// S = Q K^T for one 32-key tile: A = Q (TMEM, 128 rows x 128 d), B = K (smem,
+// K-major SW128 [d-half][32 keys][64 d]), N = 32.
+template <int kFmt>
+__device__ __forceinline__ void issue_qk32(uint32_t tmem_s, uint32_t tmem_q, uint32_t sK) {
+    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kTN, 0);
+    ptx::umma_ts_k128_elect<kTN * 128>(tmem_s, tmem_q, ptx::sw128_desc(sK, 16, 1024), idesc);
+}
+// O (+)= P V for one 32-key tile: A = P (TMEM; hi in columns [0,16), lo in [16,32)),
+// B = V (smem, MN-major SW128 [d-half][32 keys][64 d]), N = 128.
+template <int kFmt>
+__device__ __forceinline__ void issue_pv32(uint32_t tmem_o, uint32_t tmem_p, uint32_t sV, bool accumulate,
+                                           bool split) {
+    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);
+    static_assert(kTN == 32, "umma_pv32_elect: two K-steps, lo part 16 columns after hi");
+    const uint64_t b = ptx::sw128_desc(sV, kTN * 128, 1024);
+    if (split)
+        ptx::umma_pv32_elect<true>(tmem_o, tmem_p, b, idesc, accumulate ? 1u : 0u);
+    else
+        ptx::umma_pv32_elect<false>(tmem_o, tmem_p, b, idesc, accumulate ? 1u : 0u);
+}
+// The 4 TMA boxes (2 pages x 2 d-halves, 128B swizzle) of one 32-key tile.
+__device__ __forceinline__ void load_tile32(const RunParams& p, const CUtensorMap* tm, uint32_t dst, uint32_t bar,
+                                            int kt, int kv_head, const PageIds& ids) {
+    const int ph0 = ids.get(min(kt / 16, ids.n - 1)), ph1 = ids.get(min(kt / 16 + 1, ids.n - 1));
+#pragma unroll
+    for (int pg = 0; pg < 2; ++pg) {
+#pragma unroll
+        for (int dh = 0; dh < 2; ++dh) {
+            const uint32_t d = dst + dh * (kTN * 128) + pg * 2048;
+            const int phys = pg ? ph1 : ph0;
+            if (p.kv_layout == POD_KV_HND)
+                ptx::tma_load_4d_elect(d, tm, bar, dh * 64, 0, kv_head, phys);
+            else
+                ptx::tma_load_4d_elect(d, tm, bar, dh * 64, kv_head, 0, phys);
+        }
+    }
+}
+}  // namespace sm3
+
+// One prefill item of the warp-specialised engine: up to two 128-row M-blocks of
+// one (q tile, KV head, KV split) CtaTask over the same 32-key K/V tiles.
+template <int kFmt>
+__device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv, int item,
+                                uint32_t sbase, uint32_t tmem, sm3::PfState& ps, int warp, int lane) {
+    using namespace sm3;
+    const PrefillCta job = p.pctas[item];
+    const int G = p.group;
+    const int rpb = kMBlock / G;
+    const int nblocks = (job.rows + rpb - 1) / rpb;  // 1 or 2
+    const bool hasB = nblocks > 1;
+    const BlockRange rA = prefill_block(p, job, 0);
+    const BlockRange rB = hasB ? prefill_block(p, job, 1) : rA;
+    // 32-key tiles from the (page-aligned) first key up to the last key either block sees
+    const int kv_hi = min(job.kv_end, p.offset + (hasB ? rB.r0 + rB.nrows : rA.r0 + rA.nrows));
+    const int kt0 = rA.kt0;
+    const int nt = kv_hi > job.kv_begin ? (kv_hi - kt0 + kTN - 1) / kTN : 0;
+    const PfState s0 = ps;
+    if (nt > 0) {
+        ps.g += nt;
+        ps.n[0] += nt;
+        ps.nq[0] += 1;
+        if (hasB) {
+            ps.n[1] += nt;
+            ps.nq[1] += 1;
+        }
+    }
+    const int pbeg = p.page_indptr[0];
+    const int npages = p.page_indptr[1] - pbeg;
+    const uint32_t bar0 = sbase + kOffBars;
+    auto bar = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
+    const uint32_t sK = sbase + kOffKs, sV = sbase + kOffVs;
+    const int first = s0.n[0] == 0 ? 0 : 1;  // trace only the CTA's first item
+
+    if (warp == kProdWarp) {
+        // ------------------------------------------------ TMA producer --
+        PageIds ids;
+        ids.init(p.page_indices + pbeg, npages, kt0 / 16);
+        for (int t = 0; t <= nt && nt > 0; ++t) {
+            if (t < nt) {  // K of tile t
+                const int gg = s0.g + t, st = gg % kNS;
+                if (gg >= kNS) ptx::mbar_wait(bar(6 + st), ((gg / kNS) - 1) & 1);
+                ptx::mbar_arrive_expect_tx_elect(bar(2 + st), kStage);
+                load_tile32(p, tmk, sK + st * kStage, bar(2 + st), kt0 + t * kTN, job.kv_head, ids);
+            }
+            if (t > 0) {  // V of tile t-1
+                const int gg = s0.g + t - 1, st = gg % kNS;
+                if (gg >= kNS) ptx::mbar_wait(bar(14 + st), ((gg / kNS) - 1) & 1);
+                ptx::mbar_arrive_expect_tx_elect(bar(10 + st), kStage);
+                load_tile32(p, tmv, sV + st * kStage, bar(10 + st), kt0 + (t - 1) * kTN, job.kv_head, ids);
+            }
+        }
+    } else if (!kDualMma && warp == kMmaWarp) {
+        // -------------------------------------------------- MMA issuer --
+        // Per block, QK_X(t+2) reuses the S buffer of tile t after PV_X(t) (in-order
+        // pipe), so the softmax of tile t+1 overlaps PV_X(t) and QK_X(t+2); the two
+        // blocks interleave on the tensor core.
+        if (nt > 0) {
+            ptx::mbar_wait(bar(0), s0.nq[0] & 1);
+            if (hasB) ptx::mbar_wait(bar(1), s0.nq[1] & 1);
+            for (int j = 0; j < 2 && j < nt; ++j) {
+                const int gg = s0.g + j, st = gg % kNS;
+                ptx::mbar_wait(bar(2 + st), (gg / kNS) & 1);
+                ptx::tc_fence_after();
+                const int bA = (s0.n[0] + j) & 1, bB = (s0.n[1] + j) & 1;
+                issue_qk32<kFmt>(tmem + kSA + 32 * bA, tmem + kQA, sK + st * kStage);
+                ptx::umma_commit_elect(bar(18 + bA));
+                if (hasB) {
+                    issue_qk32<kFmt>(tmem + kSB + 32 * bB, tmem + kQB, sK + st * kStage);
+                    ptx::umma_commit_elect(bar(20 + bB));
+                }
+                ptx::umma_commit_elect(bar(6 + st));
+            }
+            for (int t = 0; t < nt; ++t) {
+                const int gg = s0.g + t, st = gg % kNS;
+                const int g2 = gg + 2, st2 = g2 % kNS;
+                const bool more = t + 2 < nt;
+                const int nA = s0.n[0] + t, bA = nA & 1;
+                ptx::mbar_wait(bar(22 + bA), (nA >> 1) & 1);
+                trace_stamp(p, first, t, 4);
+                ptx::mbar_wait(bar(10 + st), (gg / kNS) & 1);
+                ptx::tc_fence_after();
+                issue_pv32<kFmt>(tmem + kOA, tmem + kSA + 32 * bA, sV + st * kStage, t > 0, p.p_split != 0);
+                ptx::umma_commit_elect(bar(26 + bA));
+                trace_stamp(p, first, t, 5);
+                if (more) {
+                    ptx::mbar_wait(bar(2 + st2), (g2 / kNS) & 1);
+                    ptx::tc_fence_after();
+                    issue_qk32<kFmt>(tmem + kSA + 32 * bA, tmem + kQA, sK + st2 * kStage);
+                    ptx::umma_commit_elect(bar(18 + bA));
+                }
+                trace_stamp(p, first, t, 6);
+                if (hasB) {
+                    const int nB = s0.n[1] + t, bB = nB & 1;
+                    ptx::mbar_wait(bar(24 + bB), (nB >> 1) & 1);
+                    ptx::tc_fence_after();
+                    issue_pv32<kFmt>(tmem + kOB, tmem + kSB + 32 * bB, sV + st * kStage, t > 0, p.p_split != 0);
+                    ptx::umma_commit_elect(bar(28 + bB));
+                    if (more) {
+                        issue_qk32<kFmt>(tmem + kSB + 32 * bB, tmem + kQB, sK + st2 * kStage);
+                        ptx::umma_commit_elect(bar(20 + bB));
+                    }
+                }
+                ptx::umma_commit_elect(bar(14 + st));
+                if (more) ptx::umma_commit_elect(bar(6 + st2));
+            }
+        }
+    } else if (kDualMma && (warp == kMmaWarp || warp == kMmaWarpB)) {
+        // ------------------------------------------ MMA issuers (per block) --
+        // Block X: QK_X(t+2) reuses the S buffer of tile t after PV_X(t) (in-order
+        // per issuing thread), so the softmax of tile t+1 overlaps PV_X(t) and
+        // QK_X(t+2).  A commit only tracks its own thread's MMAs, so the K/V empty
+        // barriers count two arrivals: one per block thread (block A's thread
+        // arrives twice when the item has no block B).
+        const int X = warp == kMmaWarpB ? 1 : 0;
+        const int rel = hasB ? 1 : 2;
+        auto release = [&](uint32_t b) {
+            ptx::umma_commit_elect(b);
+            if (rel == 2) ptx::umma_commit_elect(b);
+        };
+        if (nt > 0 && (X == 0 || hasB)) {
+            const uint32_t tS = tmem + (X ? kSB : kSA), tQ = tmem + (X ? kQB : kQA), tO = tmem + (X ? kOB : kOA);
+            ptx::mbar_wait(bar(X), s0.nq[X] & 1);
+            for (int j = 0; j < 2 && j < nt; ++j) {
+                const int gg = s0.g + j, st = gg % kNS;
+                ptx::mbar_wait(bar(2 + st), (gg / kNS) & 1);
+                ptx::tc_fence_after();
+                const int bx = (s0.n[X] + j) & 1;
+                issue_qk32<kFmt>(tS + 32 * bx, tQ, sK + st * kStage);
+                ptx::umma_commit_elect(bar(18 + 2 * X + bx));
+                release(bar(6 + st));
+            }
+            for (int t = 0; t < nt; ++t) {
+                const int gg = s0.g + t, st = gg % kNS;
+                const int g2 = gg + 2, st2 = g2 % kNS;
+                const bool more = t + 2 < nt;
+                const int n = s0.n[X] + t, bx = n & 1;
+                ptx::mbar_wait(bar(22 + 2 * X + bx), (n >> 1) & 1);
+                trace_stamp(p, first, 256 * X + t, 4);
+                ptx::mbar_wait(bar(10 + st), (gg / kNS) & 1);
+                ptx::tc_fence_after();
+                issue_pv32<kFmt>(tO, tS + 32 * bx, sV + st * kStage, t > 0, p.p_split != 0);
+                ptx::umma_commit_elect(bar(26 + 2 * X + bx));
+                trace_stamp(p, first, 256 * X + t, 5);
+                if (more) {
+                    ptx::mbar_wait(bar(2 + st2), (g2 / kNS) & 1);
+                    ptx::tc_fence_after();
+                    issue_qk32<kFmt>(tS + 32 * bx, tQ, sK + st2 * kStage);
+                    ptx::umma_commit_elect(bar(18 + 2 * X + bx));
+                }
+                trace_stamp(p, first, 256 * X + t, 6);
+                release(bar(14 + st));
+                if (more) release(bar(6 + st2));
+            }
+        }
+    } else {
+        // ------------------------------------ softmax (4 warps per block) --
+        const int X = warp >> 2;  // block
+        if (X == 1 && !hasB) return;
+        const int q = warp & 3;   // TMEM lane quadrant
+        const BlockRange br = X ? rB : rA;
+        const int m = q * 32 + lane;  // row of the block
+        const int my_r = br.r0 + m / G;
+        const bool row_ok = (m / G) < br.nrows;
+        const int vis = p.offset + my_r;
+        const int qhead = job.kv_head * G + m % G;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        const uint32_t o_addr = lane_base + (X ? kOB : kOA);
+        float* orow;
+        float* lrow;
+        if (job.n_splits == 1) {
+            orow = p.o_prefill + (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim;
+            lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
+        } else {
+            const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
+            orow = p.ppart_o + row * kHeadDim;
+            lrow = p.ppart_lse + row;
+        }
+        if (nt == 0) {
+            if (row_ok) {
+                for (int c = 0; c < kHeadDim; c += 4)
+                    *reinterpret_cast<float4*>(orow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                *lrow = -INFINITY;
+            }
+            return;
+        }
+        // ---- Q row -> TMEM (A operand of QK^T); rows past the chunk are zero
+        {
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(static_cast<const uint16_t*>(p.q_prefill) +
+                                                                    (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                float qv[32];
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    const uint4 v = row_ok ? __ldg(reinterpret_cast<const uint4*>(src + 32 * hf + c))
+                                           : make_uint4(0u, 0u, 0u, 0u);
+                    qv[c] = __uint_as_float(v.x);
+                    qv[c + 1] = __uint_as_float(v.y);
+                    qv[c + 2] = __uint_as_float(v.z);
+                    qv[c + 3] = __uint_as_float(v.w);
+                }
+                ptx::tmem_st32(lane_base + (X ? kQB : kQA) + 32 * hf, qv);
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(bar(X));
+        }
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int t = 0; t < nt; ++t) {
+            const int n = s0.n[X] + t, b = n & 1;
+            const uint32_t s_addr = lane_base + (X ? kSB : kSA) + 32 * b;
+            if (lane == 0 && q == 0) trace_stamp(p, first, 256 * X + t, 0);
+            ptx::mbar_wait(bar(18 + 2 * X + b), (n >> 1) & 1);
+            if (lane == 0 && q == 0) trace_stamp(p, first, 256 * X + t, 1);
+            ptx::tc_fence_after();
+            float s[kTN];
+            ptx::tmem_ld32(s_addr, s);
+            ptx::tmem_wait_ld();
+            const int kb = kt0 + t * kTN;
+            const int lo = max(job.kv_begin - kb, 0);
+            const int hi = row_ok ? min(min(job.kv_end, vis + 1) - kb, kTN) : 0;
+            if (!__all_sync(0xffffffffu, lo == 0 && hi == kTN)) {
+#pragma unroll
+                for (int c = 0; c < kTN; ++c)
+                    if (c < lo || c >= hi) s[c] = -INFINITY;
+            }
+            float tmax = s[0];
+#pragma unroll
+            for (int c = 1; c < kTN; c += 2) tmax = fmaxf(tmax, fmaxf(s[c], s[min(c + 1, kTN - 1)]));
+            const float m_new = fmaxf(m_run, tmax * p.sl2);
+            const bool need = m_new > m_run + 8.f;  // lazy rescale (see prefill_item)
+            const float m_use = need ? m_new : m_run;
+            const float factor = need ? ptx::ex2(m_run - m_new) : 1.f;
+            l_run *= factor;
+            m_run = m_use;
+            // O is rescaled only when the reference max moved: then wait for
+            // PV_X(t-1), the newest MMA writing O_X (PV_X(t) needs our arrival).
+            if (t > 0 && __any_sync(0xffffffffu, need)) {
+                ptx::mbar_wait(bar(26 + 2 * X + ((n - 1) & 1)), ((n - 1) >> 1) & 1);
+                ptx::tc_fence_after();
+#pragma unroll 1
+                for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+                    float o[32];
+                    ptx::tmem_ld32(o_addr + ch * 32, o);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) o[c] *= factor;
+                    ptx::tmem_st32(o_addr + ch * 32, o);
+                }
+            }
+            const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
+            float lsum;
+            if (kFmt == 1 && p.p_split)
+                lsum = softmax_p_row<kFmt, 1, kTN>(s, p.sl2, neg_m, s_addr);
+            else if (p.p_split)
+                lsum = softmax_p_row<kFmt, 2, kTN>(s, p.sl2, neg_m, s_addr);
+            else
+                lsum = softmax_p_row<kFmt, 0, kTN>(s, p.sl2, neg_m, s_addr);
+            l_run += lsum;
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0 && q == 0) trace_stamp(p, first, 256 * X + t, 2);
+            if (lane == 0 && q == 3) trace_stamp(p, first, 256 * X + t, 3);
+            if (lane == 0) ptx::mbar_arrive(bar(22 + 2 * X + b));
+        }
+        // ------------------------------------------------- epilogue --
+        {  // the last PV's commit covers every earlier MMA of this thread
+            const int nl = s0.n[X] + nt - 1;
+            ptx::mbar_wait(bar(26 + 2 * X + (nl & 1)), (nl >> 1) & 1);
+        }
+        ptx::tc_fence_after();
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll 1
+        for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+            float o[32];
+            ptx::tmem_ld32(o_addr + ch * 32, o);
+            ptx::tmem_wait_ld();
+            if (row_ok) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 4)
+                    *reinterpret_cast<float4*>(orow + ch * 32 + c) =
+                        make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv);
+            }
+        }
+        if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
+        ptx::tc_fence_before();
+    }
+}
+
+__device__ __forceinline__ void sm_log_claim(const RunParams& p, int op, int id, int32_t* slot_out) {
+    *slot_out = -1;
+    if (!p.role_log || id < 0) return;
+    const uint32_t sm = ptx::smid();
+    const uint32_t slot = atomicAdd(&p.ctr->arrival, 1u);
+    int32_t* rec = p.role_log + 8 * slot;
+    rec[0] = static_cast<int32_t>(sm);
+    rec[1] = static_cast<int32_t>(atomicAdd(&p.ctr->sm_ctr[sm], 1u));
+    rec[2] = op;
+    rec[3] = id;
+    rec[4] = static_cast<int32_t>(slot);
+    rec[5] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
+    rec[7] = static_cast<int32_t>(blockIdx.x);
+    *slot_out = static_cast<int32_t>(slot);
+}
+
+// One CTA per SM; both engines bind items from their pools until drained.
+template <int G, int kFmt>
+__global__ void __launch_bounds__(sm3::kThreads, 1)
+    pod_sm_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmk,
+                  const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tdk,
+                  const __grid_constant__ CUtensorMap tdv) {
+    using namespace sm3;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sbase = ptx::smem_u32(smem);
+    volatile int32_t* misc = reinterpret_cast<volatile int32_t*>(smem + kOffMisc);  // [0] tmem, [2..3] pf, [4..5] dec
+    if (tid == 0) {
+        if (sbase & 1023u) __trap();
+        // q_full (0, 1) and p_full (22-25): one arrival per softmax warp of the block
+        for (int i = 0; i < kNumBars; ++i)
+            ptx::mbar_init(sbase + kOffBars + 8 * i, (i <= 1 || (i >= 22 && i <= 25)) ? kPrefillWarps
+                                                     : (kDualMma && ((i >= 6 && i <= 9) || (i >= 14 && i <= 17))) ? 2 : 1);
+        for (int i = 0; i < kDW * kDS; ++i) ptx::mbar_init(sbase + kOffDecBars + 8 * i, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) {
+        if (p.num_pctas > 0) ptx::tmem_alloc(ptx::smem_u32(const_cast<int32_t*>(misc)), 512);
+        ptx::tmem_relinquish();
+    }
+    if (warp == kProdWarp && lane == 0) {
+        ptx::prefetch_tmap(&tmk);
+        ptx::prefetch_tmap(&tmv);
+        ptx::prefetch_tmap(&tdk);
+        ptx::prefetch_tmap(&tdv);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+
+    if (warp < kDecWarp0) {
+        // ============================================ prefill engine ===
+        // The CTA owns all 512 columns, so the allocation starts at lane 0, column 0:
+        // a compile-time TMEM base keeps every MMA operand in uniform registers.
+        if (p.num_pctas > 0 && tid == 0 && misc[0] != 0) __trap();
+        constexpr uint32_t tmem = 0u;
+        PfState ps;
+        while (p.num_pctas > 0) {
+            if (warp == kProdWarp && lane == 0) {
+                int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[0], 1u));
+                if (id >= p.num_pctas) id = -1;
+                int32_t slot;
+                sm_log_claim(p, 0, id, &slot);
+                misc[2] = id;
+                misc[3] = slot;
+            }
+            ptx::named_bar_sync(1, kPrefillThreads);
+            const int id = misc[2], slot = misc[3];
+            ptx::named_bar_sync(1, kPrefillThreads);
+            if (id < 0) break;
+            prefill_item_sm<kFmt>(p, &tmk, &tmv, id, sbase, tmem, ps, warp, lane);
+            if (slot >= 0 && warp == kProdWarp && lane == 0) {
+                // stamp the end when the producer is done issuing (softmax epilogues may still run)
+                p.role_log[8 * slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
+            }
+        }
+        ptx::tc_fence_before();
+        ptx::named_bar_sync(1, kPrefillThreads);
+        ptx::tc_fence_after();
+        if (warp == 0 && p.num_pctas > 0) ptx::tmem_dealloc(tmem, 512);
+    } else {
+        // ============================================= decode engine ===
+        const int dw = warp - kDecWarp0;
+        int dpos = 0;
+        while (p.num_dctas > 0) {
+            if (dw == 0 && lane == 0) {
+                int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[1], 1u));
+                if (id >= p.num_dctas) id = -1;
+                int32_t slot;
+                sm_log_claim(p, 1, id, &slot);
+                misc[4] = id;
+                misc[5] = slot;
+            }
+            ptx::named_bar_sync(3, kDW * 32);
+            const int id = misc[4], slot = misc[5];
+            ptx::named_bar_sync(3, kDW * 32);
+            if (id < 0) break;
+            decode_item<G, kFmt, kDW, kDS>(p, &tdk, &tdv, id, dw, sbase + kOffDec, sbase + kOffDecBars,
+                                           reinterpret_cast<float*>(smem + kOffDec), 2, dpos);
+            if (slot >= 0 && dw == 0 && lane == 0)
+                p.role_log[8 * slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(&p.ctr->done, 1u);
+        if (prev == gridDim.x - 1) {
+            const uint32_t n = min(ptx::nsmid(), static_cast<uint32_t>(kMaxSms));
+            for (uint32_t i = 0; i < n; ++i) {
+                p.ctr->sm_ctr[i] = 0;
+                p.ctr->running_prefill[i] = 0;
+                p.ctr->sm_slot[i] = 0;
+            }
+            p.ctr->cta_assign[0] = 0;
+            p.ctr->cta_assign[1] = 0;
+            p.ctr->arrival = 0;
+            p.ctr->done = 0;
+            __threadfence();
+        }
+    }
+}

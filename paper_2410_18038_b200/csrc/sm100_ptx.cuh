@@ -246,6 +246,57 @@ __device__ __forceinline__ void umma_f16_ts_elect(uint32_t d_tmem, uint32_t a_tm
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// One full K = 128 contraction as 8 back-to-back kind::f16 TS-MMAs in a single
+// asm block (one elect, descriptor / TMEM offsets as immediates): A = 128 rows x
+// 128 (TMEM, 8 columns per K-step), B K-major SW128 with the two 64-element
+// K-halves kHalf bytes apart.  Cuts the per-MMA issue cost for small N.
+template <uint32_t kHalf>
+__device__ __forceinline__ void umma_ts_k128_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc) {
+    constexpr uint64_t h = kHalf >> 4;
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b64 b1, b2, b3, b4, b5, b6, b7;\n\t.reg .b32 a1, a2, a3, a4, a5, a6, a7;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "add.s64 b4, %2, %4;\n\tadd.s64 b5, b4, 2;\n\tadd.s64 b6, b4, 4;\n\tadd.s64 b7, b4, 6;\n\t"
+        "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\tadd.u32 a4, %1, 32;\n\t"
+        "add.u32 a5, %1, 40;\n\tadd.u32 a6, %1, 48;\n\tadd.u32 a7, %1, 56;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], b4, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], b5, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], b6, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], b7, %3, 1;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "n"(h)
+        : "memory");
+}
+// O (+)= P V over 32 keys (2 K-steps of 16) with P as bf16 hi (A columns +0, +8)
+// and, if kSplit, lo (columns +16, +24); B MN-major SW128, K-steps 2 KB apart.
+template <bool kSplit>
+__device__ __forceinline__ void umma_pv32_elect(uint32_t d_tmem, uint32_t p_tmem, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+    if constexpr (kSplit)
+        asm volatile(
+            "{\n\t.reg .pred e, acc;\n\t.reg .b64 b1;\n\t.reg .b32 a1, a2, a3;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 acc, %4, 0;\n\t"
+            "add.s64 b1, %2, 128;\n\tadd.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, acc;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], %2, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b1, %3, 1;\n\t}" ::"r"(d_tmem),
+            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred e, acc;\n\t.reg .b64 b1;\n\t.reg .b32 a1;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 acc, %4, 0;\n\t"
+            "add.s64 b1, %2, 128;\n\tadd.u32 a1, %1, 8;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, acc;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t}" ::"r"(d_tmem),
+            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+}
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"

@@ -216,7 +216,7 @@ class WorkDecomposition:
 
 @dataclass
 class PlanOptions:
-    policy: int = _abi.POD_POLICY_COMPLEMENT
+    policy: int = _abi.POD_POLICY_AUTO
     tile_mode: int = _abi.POD_TILE_B200
     ctas_per_sm: int = 0
     virtual_decode: int = -1

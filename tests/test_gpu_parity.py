@@ -14,6 +14,7 @@ import paper_2410_18038_b200 as pkg
 from oracle import pyoracle as O
 from paper_2410_18038_b200._abi import (POD_DTYPE_FP16, POD_KV_NHD, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT,
                                         POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_SLOTS,
+                                        POD_POLICY_WARPSPEC,
                                         POD_PRECISION_FAST, POD_TILE_B200, POD_TILE_REFERENCE)
 from paper_2410_18038_b200.workload import build_workload, make_batch
 from tests.common import LSE_TOL, O_TOL, compare_decode, compare_prefill
@@ -71,6 +72,9 @@ def test_matches_oracle(name, mode):
     _check(wl, out)
     # the two-block ping-pong prefill engine of the slots policy
     wl, _, out = _run(batch, mode, options=pkg.PlanOptions(policy=POD_POLICY_SLOTS), wl=wl)
+    _check(wl, out)
+    # the warp-specialised one-CTA-per-SM kernel
+    wl, _, out = _run(batch, mode, options=pkg.PlanOptions(policy=POD_POLICY_WARPSPEC), wl=wl)
     _check(wl, out)
 
 

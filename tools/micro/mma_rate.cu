@@ -24,8 +24,8 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int n, long long* out) {
     long long t0 = 0, t1 = 0;
     if (warp == 1) {
         // shapes: 0 SS M128 N64 K16; 1 TS M128 N128 K16 (A tmem); 2 SS M128 N128 K16; 3 TS M128 N64 K16
-        constexpr uint32_t N = (kShape == 1 || kShape == 2 || kShape >= 4) ? 128 : 64;
-        constexpr uint32_t idesc = ptx::idesc_f16(1, 128, N, (kShape == 1 || kShape >= 4) ? 1 : 0);
+        constexpr uint32_t N = kShape == 6 ? 32 : kShape == 7 ? 16 : (kShape == 1 || kShape == 2 || kShape >= 4) ? 128 : 64;
+        constexpr uint32_t idesc = ptx::idesc_f16(1, 128, N, (kShape == 1 || kShape == 4 || kShape == 5) ? 1 : 0);
         const uint64_t a = ptx::sw128_desc(sb, 16, 1024);
         const uint64_t b = ptx::sw128_desc(sb + 65536, 16, 1024);
         __syncwarp();
@@ -34,6 +34,9 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int n, long long* out) {
             if constexpr (kShape == 0 || kShape == 2)
                 ptx::umma_f16_ss_elect(tmem, a + ((i & 7) * 2), b + ((i & 7) * 2), idesc, 1u);
             else if constexpr (kShape == 4) {  // operands through vector registers (R2UR per MMA)
+                const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(&tmem_slot);
+                ptx::umma_f16_ts_elect(tm + 256, tm + (i & 7) * 8, b + ((i & 7) * 2), idesc, 1u);
+            } else if constexpr (kShape == 6 || kShape == 7) {  // TS N32 / N16 (vector-reg tmem)
                 const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(&tmem_slot);
                 ptx::umma_f16_ts_elect(tm + 256, tm + (i & 7) * 8, b + ((i & 7) * 2), idesc, 1u);
             } else if constexpr (kShape == 5) {  // lane-0 issue (divergent branch, no elect)
@@ -57,12 +60,12 @@ int main() {
     long long* d;
     cudaMalloc(&d, 1024 * 8);
     long long h[1024];
-    const char* names[6] = {"SS M128 N64 K16", "TS M128 N128 K16 (A=TMEM, B MN-major)", "SS M128 N128 K16",
-                            "TS M128 N64 K16 (A=TMEM)", "TS N128, tmem via vector reg + elect", "TS N128, lane-0 branch"};
-    for (int shape = 0; shape < 6; ++shape) {
+    const char* names[8] = {"SS M128 N64 K16", "TS M128 N128 K16 (A=TMEM, B MN-major)", "SS M128 N128 K16",
+                            "TS M128 N64 K16 (A=TMEM)", "TS N128, tmem via vector reg + elect", "TS N128, lane-0 branch", "TS N32 (vector tmem, elect)", "TS N16 (vector tmem, elect)"};
+    for (int shape = 0; shape < 8; ++shape) {
         for (int grid : {1, 148}) {
             for (int n : {64, 1024}) {
-                auto k = shape == 0 ? mma_rate<0> : shape == 1 ? mma_rate<1> : shape == 2 ? mma_rate<2> : shape == 3 ? mma_rate<3> : shape == 4 ? mma_rate<4> : mma_rate<5>;
+                auto k = shape == 0 ? mma_rate<0> : shape == 1 ? mma_rate<1> : shape == 2 ? mma_rate<2> : shape == 3 ? mma_rate<3> : shape == 4 ? mma_rate<4> : shape == 5 ? mma_rate<5> : shape == 6 ? mma_rate<6> : mma_rate<7>;
                 cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                 k<<<grid, 128, 200 * 1024>>>(n, d);
                 k<<<grid, 128, 200 * 1024>>>(n, d);

@@ -24,11 +24,12 @@ def main():
     ap.add_argument("--config", default="c2_b64")
     ap.add_argument("--mode", default="fused")
     ap.add_argument("--iters", type=int, default=3)
-    ap.add_argument("--policy", type=int, default=3)
+    ap.add_argument("--policy", type=int, default=8)
     ap.add_argument("--tile-mode", type=int, default=1)
     ap.add_argument("--decode-splits", type=int, default=0)
     ap.add_argument("--roles", default="")
     ap.add_argument("--precision", type=int, default=0)
+    ap.add_argument("--split-wave-cap", type=int, default=0)
     a = ap.parse_args()
     hq, hkv, chunk, off, b, ctx = CONFIGS[a.config]
     b_ = b
@@ -36,7 +37,8 @@ def main():
     batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
     wl = build_workload(batch, device="cuda")
     op = PodAttention(batch, options=pkg.PlanOptions(policy=a.policy, tile_mode=a.tile_mode,
-                                                     decode_splits=a.decode_splits, precision=a.precision))
+                                                     decode_splits=a.decode_splits, precision=a.precision,
+                                                     split_wave_cap=a.split_wave_cap))
     log = op.enable_role_log(768 * 8) if a.roles else None
     out = op.alloc_outputs()
     for _ in range(a.iters):
@@ -48,7 +50,14 @@ def main():
         nrec = int(op.info.num_prefill_ctas + op.info.num_decode_ctas)
         rec = allrec[:nrec].tolist()
         tr = allrec[nrec:].tolist()
-        if any(any(x) for x in tr):
+        print("trace words nonzero:", int((allrec[nrec:] != 0).sum()), "policy", a.policy)
+        if any(any(x) for x in tr) and op.info.policy == 7:
+            print("trace (warpspec): t | A: swait, sok, w0 done, w3 done, mma pA seen, PV_A issued, QK_A issued | B: same")
+            base = tr[0][0]
+            for t in list(range(0, 10)) + list(range(100, 104)):
+                row = tr[t][:7] + tr[256 + t][:7]
+                print(t, [((x - base) & 0xffffffff) if x else None for x in row])
+        elif any(any(x) for x in tr):
             import os
             print("trace: t | sfull_wait_begin, sfull_ok, softmax_done(pre pv wait), mma_pfull_seen, mma_vfull_ok, mma_kfull_ok(QK t+2), pv_wait_ok, mma_pv_issued | arrive w0..w3, K(t) issue begin/end, V(t) issue begin/end | mma: pv done(probe), qk issued, qk done(probe)")
             base = tr[0][0]
