@@ -321,7 +321,7 @@ def main():
     ap.add_argument("--precision", type=int, default=0, help="0: prefill P as bf16 hi+lo (default), 1: single bf16")
     ap.add_argument("--decode-splits", type=int, default=0)
     ap.add_argument("--split-wave-cap", type=int, default=0)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="wall seconds of the CPU reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -398,7 +398,9 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            cus, thr, desc, _ = cpu_reference_sample(hq, hkv, chunk, off, b, ctx, target_s=args.cpu_seconds)
+            # ~cpu_seconds of wall time on all host threads (cpu_seconds x threads core-seconds)
+            cus, thr, desc, _ = cpu_reference_sample(hq, hkv, chunk, off, b, ctx,
+                                                     target_s=args.cpu_seconds * (os.cpu_count() or 1))
             cpu = {"value": round(cus, 1), "unit": "us/layer", "cores": thr, "kind": "reference", "sample": desc}
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": "us/layer", "cores": os.cpu_count(), "kind": "reference",
@@ -423,7 +425,8 @@ def main():
                  "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_p": {0: "bf16 hi+lo", 1: "bf16"}[args.precision]},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "pod_fused_kernel (+merge)", "peak_source": pk["source"]},
+                     "kernel": {7: "pod_sm_kernel (+merge)"}.get(r["info"].policy, "pod_fused_kernel (+merge)"),
+                     "peak_source": pk["source"]},
         "cpu_baseline": cpu,
         "e2e": {"value": round(r["t_e2e"] * 1000, 2), "unit": "us/layer", "h2d_bytes_per_step": r["h2d"],
                 "d2h_bytes_per_step": r["d2h"]},
