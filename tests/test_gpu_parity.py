@@ -268,6 +268,53 @@ def test_role_log_scheduler_contract(policy):
                     switched_to = op_i
 
 
+def test_warpspec_role_log_co_residency():
+    """Warp-specialised kernel: every id of both pools is claimed exactly once, each
+    SM's CTA claims items of both roles, and on SMs that ran a prefill item some
+    decode item ran at the same time (the POD placement: both roles co-run on an SM)."""
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=1024, offset=3072, decode_ctx=[4096] * 32)
+    wl = build_workload(batch, device="cuda")
+    op = PodAttention(batch, options=pkg.PlanOptions(policy=POD_POLICY_WARPSPEC))
+    log = op.enable_role_log()
+    op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+    torch.cuda.synchronize()
+    assert op.info.policy == POD_POLICY_WARPSPEC
+    rec = log.view(-1, 8).cpu().numpy().astype(np.int64)
+    P, D = op.info.num_prefill_ctas, op.info.num_decode_ctas
+    assert sorted(rec[rec[:, 2] == 0, 3].tolist()) == list(range(P))
+    assert sorted(rec[rec[:, 2] == 1, 3].tolist()) == list(range(D))
+    both = overlapped = 0
+    for sm in np.unique(rec[:, 0]):
+        mine = rec[rec[:, 0] == sm]
+        pf, dc = mine[mine[:, 2] == 0], mine[mine[:, 2] == 1]
+        if len(pf) and len(dc):
+            both += 1
+            if any(max(a[5], b[5]) < min(a[6], b[6]) for a in pf for b in dc):
+                overlapped += 1
+    assert both >= min(P, 148) // 2, both
+    assert overlapped >= both // 2, (overlapped, both)
+    _check(wl, op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices),
+           kv_heads=[0, 5], requests=[0, 31])
+
+
+def test_auto_policy_resolution():
+    """AUTO runs the one-CTA-per-SM kernel on decode-heavy batches and the two-CTA POD
+    kernel on prefill-heavy ones; both match the oracle."""
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+
+    heavy_dec = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=64, offset=2048, decode_ctx=[2048] * 16)
+    heavy_pf = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=512, offset=4096, decode_ctx=[300])
+    for batch, want in ((heavy_dec, POD_POLICY_WARPSPEC), (heavy_pf, POD_POLICY_COMPLEMENT)):
+        op = PodAttention(batch)
+        assert op.info.policy == want
+        wl, _, out = _run(batch)
+        _check(wl, out, kv_heads=[0, 7], requests=[0])
+
+
 def test_fault_injection_is_detected():
     """A wrong block-table entry must make the parity check fail (the checks bite)."""
     _need_gpu()
