@@ -1696,6 +1696,8 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
     if (e != cudaSuccess) return cuda_fail(e, "pod kernel launch");
     // split merges
     const bool do_p = (mode != 3) && plan->merge_rows_prefill > 0;
+    // (an in-kernel merge by the group finishing a parent's last split measured ~8 us
+    // slower at C2 B=64 than this 5 us launch: per-item fences + barriers)
     const bool do_d = (mode != 2) && plan->merge_rows_decode > 0;
     const uint8_t* ws = reinterpret_cast<const uint8_t*>(p.ctr);
     const int32_t* tile_splits = reinterpret_cast<const int32_t*>(ws - plan->ws.off_counters + plan->ws.off_tile_splits);

@@ -460,8 +460,11 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
         if (p.num_pctas > 0 && tid == 0 && misc[0] != 0) __trap();
         constexpr uint32_t tmem = 0u;
         PfState ps;
+        int prev_slot = -1;
         while (p.num_pctas > 0) {
+            ptx::named_bar_sync(1, kPrefillThreads);  // the previous item is complete in every warp
             if (warp == kProdWarp && lane == 0) {
+                if (prev_slot >= 0) p.role_log[8 * prev_slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
                 int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[0], 1u));
                 if (id >= p.num_pctas) id = -1;
                 int32_t slot;
@@ -470,14 +473,10 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
                 misc[3] = slot;
             }
             ptx::named_bar_sync(1, kPrefillThreads);
-            const int id = misc[2], slot = misc[3];
-            ptx::named_bar_sync(1, kPrefillThreads);
+            const int id = misc[2];
+            prev_slot = misc[3];
             if (id < 0) break;
             prefill_item_sm<kFmt>(p, &tmk, &tmv, id, sbase, tmem, ps, warp, lane);
-            if (slot >= 0 && warp == kProdWarp && lane == 0) {
-                // stamp the end when the producer is done issuing (softmax epilogues may still run)
-                p.role_log[8 * slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
-            }
         }
         ptx::tc_fence_before();
         ptx::named_bar_sync(1, kPrefillThreads);

@@ -41,10 +41,16 @@ def main():
                                                      split_wave_cap=a.split_wave_cap))
     log = op.enable_role_log(768 * 8) if a.roles else None
     out = op.alloc_outputs()
+    evs = []
     for _ in range(a.iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=out,
                mode=a.mode)
+        e1.record()
+        evs.append((e0, e1))
     torch.cuda.synchronize()
+    print("event times (us):", [round(x.elapsed_time(y) * 1000, 1) for x, y in evs])
     if log is not None:
         allrec = log.view(-1, 8).cpu()
         nrec = int(op.info.num_prefill_ctas + op.info.num_decode_ctas)
