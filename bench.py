@@ -257,6 +257,36 @@ def run_pod(args, rank, world, local_rank):
             t = float(x.item())
         return t, ms
 
+    # KV append (the write step before attention): the batch's new
+    # K/V rows (chunk tokens + one per decode, read back from their slots) scattered
+    # into the paged pools.  Reported beside the attention metric, not part of it.
+    ix = wl.page_indices.cpu().tolist()
+    ip = wl.page_indptr.cpu().tolist()
+    slots = [(ix[ip[0] + t // 16], t % 16) for t in range(off, off + chunk)] if chunk else []
+    slots += [(ix[ip[(1 if chunk else 0) + i] + (ctx - 1) // 16], (ctx - 1) % 16) for i in range(b)]
+    pg = torch.tensor([p_ for p_, _ in slots], device=dev)
+    sl = torch.tensor([s_ for _, s_ in slots], device=dev)
+    k_rows = wl.k_pool[pg, :, sl, :].contiguous()
+    v_rows = wl.v_pool[pg, :, sl, :].contiguous()
+
+    def append():
+        op.append_kv(k_rows[:chunk] if chunk else None, v_rows[:chunk] if chunk else None,
+                     k_rows[chunk:] if b else None, v_rows[chunk:] if b else None,
+                     wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+
+    for _ in range(args.warmup):
+        append()
+    torch.cuda.synchronize()
+    aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        aev[i][0].record()
+        append()
+        aev[i][1].record()
+    torch.cuda.synchronize()
+    t_append = sum(x.elapsed_time(y) for x, y in aev) / args.steps
+    append_bytes = 2 * 2 * k_rows.numel() * k_rows.element_size()  # K + V, read + write
+
     sampler = ClockSampler(local_rank)
     with sampler:
         t_fused, ms_fused = timed("fused", args.steps, args.warmup)
@@ -265,36 +295,69 @@ def run_pod(args, rank, world, local_rank):
         t_dec, _ = timed("decode", args.steps, args.warmup) if b else (0.0, [])
     clocks = sampler.summary()
 
-    # e2e through the C ABI with HOST buffers (pinned): H2D of the step's queries, the
-    # fused launch, D2H of the outputs (O + LSE).  The paged KV cache is device-resident state.
+    # e2e through the C ABI with HOST buffers (pinned): every step copies its queries
+    # H2D, runs the fused layer and copies its outputs (O + LSE) D2H.  Steps are
+    # pipelined the way a serving loop runs them: double-buffered device Q / O, the
+    # H2D of step i+1 and the D2H of step i-1 on their own copy streams (separate
+    # copy engines) overlap the kernel of step i.  The paged KV cache is device state.
     qp_h = wl.q_prefill.cpu().pin_memory() if chunk else None
     qd_h = wl.q_decode.cpu().pin_memory() if b else None
-    host_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in
-                (out.o_prefill, out.lse_prefill, out.o_decode, out.lse_decode) if t is not None]
-    dev_out = [t for t in (out.o_prefill, out.lse_prefill, out.o_decode, out.lse_decode) if t is not None]
+    outs = [out, op.alloc_outputs()]
+    q_dev = [(wl.q_prefill, wl.q_decode),
+             (wl.q_prefill.clone() if chunk else None, wl.q_decode.clone() if b else None)]
+
+    def _dev_out(o):
+        return [t for t in (o.o_prefill, o.lse_prefill, o.o_decode, o.lse_decode) if t is not None]
+
+    host_out = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in _dev_out(o)] for o in outs]
     h2d = (qp_h.numel() * 2 if qp_h is not None else 0) + (qd_h.numel() * 2 if qd_h is not None else 0)
-    d2h = sum(t.numel() * 4 for t in dev_out)
+    d2h = sum(t.numel() * 4 for t in _dev_out(out))
+    s_c = torch.cuda.current_stream(dev)
+    s_h, s_d = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev_h = [torch.cuda.Event() for _ in range(2)]
+    ev_c = [torch.cuda.Event() for _ in range(2)]
+    ev_d = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_c + ev_d:
+        e.record(s_c)
 
-    def e2e_step():
-        if qp_h is not None:
-            wl.q_prefill.copy_(qp_h, non_blocking=True)
-        if qd_h is not None:
-            wl.q_decode.copy_(qd_h, non_blocking=True)
-        step("fused")
-        for hsrc, dsrc in zip(host_out, dev_out):
-            hsrc.copy_(dsrc, non_blocking=True)
+    def e2e_step(i):
+        j = i % 2
+        qp, qd = q_dev[j]
+        with torch.cuda.stream(s_h):  # H2D of this step's queries (buffer free once kernel i-2 is done)
+            s_h.wait_event(ev_c[j])
+            if qp_h is not None:
+                qp.copy_(qp_h, non_blocking=True)
+            if qd_h is not None:
+                qd.copy_(qd_h, non_blocking=True)
+            ev_h[j].record(s_h)
+        s_c.wait_event(ev_h[j])
+        s_c.wait_event(ev_d[j])  # O buffer j drained by the D2H of step i-2
+        op.run(qp, qd, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=outs[j], mode="fused",
+               stream=s_c)
+        if world > 1:
+            local = torch.cat([outs[j].o_prefill.reshape(-1), outs[j].o_decode.reshape(-1)])
+            gather_outputs(local, world)
+        ev_c[j].record(s_c)
+        with torch.cuda.stream(s_d):  # D2H of this step's outputs
+            s_d.wait_event(ev_c[j])
+            for hsrc, dsrc in zip(host_out[j], _dev_out(outs[j])):
+                hsrc.copy_(dsrc, non_blocking=True)
+            ev_d[j].record(s_d)
 
-    for _ in range(args.warmup):
-        e2e_step()
+    for i in range(args.warmup):
+        e2e_step(i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
-    for _ in range(args.steps):
-        e2e_step()
-    t1.record()
+    t0.record(s_c)
+    s_h.wait_event(t0)
+    for i in range(args.steps):
+        e2e_step(args.warmup + i)
+    for e in ev_d:
+        s_c.wait_event(e)  # the last step's D2H is inside the timed region
+    t1.record(s_c)
     torch.cuda.synchronize()
     t_e2e = t0.elapsed_time(t1) / args.steps
     if world > 1:
@@ -305,6 +368,7 @@ def run_pod(args, rank, world, local_rank):
     info = op.info
     launches_per_step = 1 + (1 if info.num_merge_rows_prefill > 0 else 0) + (1 if info.num_merge_rows_decode > 0 else 0)
     res = dict(t_fused=t_fused, ms_fused=ms_fused, t_serial=t_serial, t_pf=t_pf, t_dec=t_dec, t_e2e=t_e2e,
+               t_append=t_append, append_bytes=append_bytes,
                clocks=clocks, info=info, launches=launches_per_step, h2d=h2d, d2h=d2h, hq_r=hq_r, hkv_r=hkv_r)
     return res
 
@@ -428,6 +492,9 @@ def main():
                      "kernel": {7: "pod_sm_kernel (+merge)"}.get(r["info"].policy, "pod_fused_kernel (+merge)"),
                      "peak_source": pk["source"]},
         "cpu_baseline": cpu,
+        "kv_append": {"us": round(r["t_append"] * 1000, 2), "bytes": r["append_bytes"],
+                      "gb_s": round(r["append_bytes"] / (r["t_append"] * 1e-3) / 1e9, 1),
+                      "note": "pod_attn_append_kv of the batch's new K/V tokens into the paged pools (not in value)"},
         "e2e": {"value": round(r["t_e2e"] * 1000, 2), "unit": "us/layer", "h2d_bytes_per_step": r["h2d"],
                 "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": r["launches"] * args.steps,

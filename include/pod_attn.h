@@ -248,6 +248,22 @@ pod_status pod_attn_gather_probe(const pod_plan* plan, const void* kv_pool, int6
                                  const int32_t* page_indptr, const int32_t* page_indices,
                                  int32_t req, int64_t ctx, uint16_t* out, void* stream);
 
+/* KV append (the step before attention in a layer): scatters the
+ * batch's new K/V tokens into the paged pools through the block table.  The prefill
+ * chunk's tokens take positions [position_offset, position_offset + chunk_size) of
+ * request 0, decode b's single token takes position context_len_b - 1 of request b+1
+ * (the newest key each query attends to).  Token t of request r lands in page
+ * page_indices[page_indptr[r] + t / page_size], slot t % page_size, for every KV head
+ * (HND or NHD as planned).  Inputs: k_new / v_new rows [chunk][Hkv][d] (prefill) and
+ * [B][Hkv][d] (decode), the pool dtype.  A pure copy: bit-exact.  Stream-ordered;
+ * run it before pod_attn_run on the same stream.  (No reference counterpart: the
+ * reference keeps contiguous caches.)  `workspace` is the plan's
+ * (pod_attn_workspace_init'ed): it holds the decode positions. */
+pod_status pod_attn_append_kv(const pod_plan* plan, const void* k_new_prefill, const void* v_new_prefill,
+                              const void* k_new_decode, const void* v_new_decode, void* k_pool, void* v_pool,
+                              int64_t num_pages, const int32_t* page_indptr, const int32_t* page_indices,
+                              void* workspace, void* stream);
+
 /* Resident CTAs per SM the driver allows for the fused / prefill-only /
  * decode-only kernels of this plan's instantiation (cudaOccupancyMaxActiveBlocksPerMultiprocessor). */
 pod_status pod_attn_occupancy(const pod_plan* plan, int32_t* fused, int32_t* prefill, int32_t* decode);

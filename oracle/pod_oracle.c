@@ -352,6 +352,33 @@ int orc_gather_pages(const uint16_t* pool, int layout, long num_pages, int hkv, 
     return ORC_OK;
 }
 
+/* KV append (SURVEY.md 8(f) N2 -- the write step before attention; the reference
+ * keeps contiguous caches, so this restates the paged-layout contract
+ * of orc_gather_pages in the other direction): rows [ntok][hkv][d] (16-bit words)
+ * land at positions pos0 .. pos0+ntok-1 of request `req`.  A pure copy. */
+int orc_append_kv(uint16_t* pool, int layout, long num_pages, int hkv, int page_size, int d,
+                  const int32_t* page_indptr, const int32_t* page_indices, int req, long pos0, long ntok,
+                  const uint16_t* rows) {
+    const long npages = page_indptr[req + 1] - page_indptr[req];
+    if (pos0 < 0 || (pos0 + ntok + page_size - 1) / page_size > npages) return ORC_LOGIC;
+    for (long i = 0; i < ntok; ++i) {
+        const long t = pos0 + i;
+        const long page = page_indices[page_indptr[req] + t / page_size];
+        const long slot = t % page_size;
+        if (page < 0 || page >= num_pages) return ORC_OUT_OF_RANGE;
+        for (int h = 0; h < hkv; ++h) {
+            size_t base;
+            if (layout == 0)
+                base = (((size_t)page * hkv + h) * page_size + slot) * d;
+            else
+                base = (((size_t)page * page_size + slot) * hkv + h) * d;
+            const uint16_t* src = rows + ((size_t)i * hkv + h) * d;
+            for (int c = 0; c < d; ++c) pool[base + c] = src[c];
+        }
+    }
+    return ORC_OK;
+}
+
 /* SM-aware CTA scheduler semantics (gpu_sim.hpp:80-131),
  * restated for checking the device role log.  Proportional ratio is the
  * gcd-reduced P:D (gpu_sim.hpp:100-105). */

@@ -59,6 +59,9 @@ def port() -> C.CDLL:
         l.orc_gqa_kv_head.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
         l.orc_gather_pages.argtypes = [C.c_void_p, C.c_int, C.c_long, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                        C.c_void_p, C.c_int, C.c_long, _dp]
+        l.orc_append_kv.argtypes = [C.c_void_p, C.c_int, C.c_long, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                    C.c_void_p, C.c_int, C.c_long, C.c_long, C.c_void_p]
+        l.orc_append_kv.restype = C.c_int
         l.orc_sched_ratio.argtypes = [C.c_int, C.c_long, C.c_long, _lp, _lp]
         l.orc_sm_aware_replay.argtypes = [C.c_long, C.c_long, C.c_long, C.c_long, C.c_int, C.c_void_p, C.c_long,
                                           C.c_void_p, C.c_void_p]
@@ -247,6 +250,23 @@ def gather_pages(pool_u16: np.ndarray, layout: int, page_indptr: np.ndarray, pag
     if st:
         raise OracleError(st, "gather_pages")
     return out
+
+
+def append_kv(pool_u16: np.ndarray, layout: int, page_indptr: np.ndarray, page_indices: np.ndarray,
+              req: int, pos0: int, rows_u16: np.ndarray) -> None:
+    """In place: rows [ntok][hkv][d] (16-bit words) -> positions pos0.. of request req."""
+    assert pool_u16.flags.c_contiguous and pool_u16.dtype == np.uint16
+    if layout == 0:
+        num_pages, hkv, ps, d = pool_u16.shape
+    else:
+        num_pages, ps, hkv, d = pool_u16.shape
+    rows = np.ascontiguousarray(rows_u16, np.uint16)
+    ip = np.ascontiguousarray(page_indptr, np.int32)
+    ix = np.ascontiguousarray(page_indices, np.int32)
+    st = port().orc_append_kv(pool_u16.ctypes.data, layout, num_pages, hkv, ps, d, ip.ctypes.data, ix.ctypes.data,
+                              req, pos0, rows.shape[0], rows.ctypes.data)
+    if st:
+        raise OracleError(st, "append_kv")
 
 
 def sched_replay(proportional: int, p_total: int, d_total: int, num_sms: int, sm_ids, which="port"):

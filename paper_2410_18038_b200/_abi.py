@@ -103,6 +103,7 @@ SYMBOLS = [
                                     _vp, _vp]),
     ("pod_attn_set_role_log", C.c_int, [_vp, _vp]),
     ("pod_attn_gather_probe", C.c_int, [_vp, _vp, C.c_int64, _vp, _vp, C.c_int32, C.c_int64, _vp, _vp]),
+    ("pod_attn_append_kv", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int64, _vp, _vp, _vp, _vp]),
     ("pod_attn_occupancy", C.c_int, [_vp, _i32p, _i32p, _i32p]),
     ("pod_status_string", C.c_char_p, [C.c_int]),
     ("pod_last_error", C.c_char_p, []),

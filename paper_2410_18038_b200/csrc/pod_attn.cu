@@ -25,6 +25,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "pod_internal.h"
 #include "sm100_ptx.cuh"
@@ -1472,6 +1473,34 @@ __global__ void gather_probe_kernel(const uint16_t* pool, int layout, int hkv, c
     }
 }
 
+// ========================================================== KV append ===
+// One warp per (new token, KV head): 16 lanes x 16 B move the K row, the other 16
+// the V row (256 B each at d = 128), from the dense new-token rows into the token's
+// page slot.  HBM-bound copy: 2 x 256 B read + 2 x 256 B written per (token, head).
+__global__ void __launch_bounds__(256) append_kv_kernel(const uint4* __restrict__ kp, const uint4* __restrict__ vp,
+                                                        const uint4* __restrict__ kd, const uint4* __restrict__ vd,
+                                                        uint4* k_pool, uint4* v_pool, const int32_t* indptr,
+                                                        const int32_t* indices, const int32_t* dec_pos, int chunk,
+                                                        int offset, int ndec, int hkv, int layout) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int rows = (chunk + ndec) * hkv;
+    if (warp >= rows) return;
+    const int tok = warp / hkv, h = warp % hkv;
+    const bool is_pf = tok < chunk;
+    const int req = is_pf ? 0 : (chunk > 0 ? 1 : 0) + (tok - chunk);
+    const int pos = is_pf ? offset + tok : __ldg(dec_pos + (tok - chunk));
+    const int phys = __ldg(indices + __ldg(indptr + req) + pos / 16);
+    const int slot = pos % 16;
+    constexpr int kVecs = kHeadDim * 2 / 16;  // 16 x uint4 per row
+    const size_t src = (static_cast<size_t>(is_pf ? tok : tok - chunk) * hkv + h) * kVecs;
+    const size_t dst = (layout == POD_KV_HND ? ((static_cast<size_t>(phys) * hkv + h) * 16 + slot)
+                                             : ((static_cast<size_t>(phys) * 16 + slot) * hkv + h)) * kVecs;
+    const int c = lane & 15;
+    const uint4* in = lane < 16 ? (is_pf ? kp : kd) : (is_pf ? vp : vd);
+    uint4* out = lane < 16 ? k_pool : v_pool;
+    out[dst + c] = __ldg(in + src + c);
+}
+
 // ================================================================ host ===
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1785,6 +1814,9 @@ pod_status pod_attn_workspace_init(const pod_plan* plan, void* workspace, void* 
     if (e == cudaSuccess && !plan->dctas.empty())
         e = cudaMemcpyAsync(ws + plan->ws.off_dctas, plan->dctas.data(), plan->dctas.size() * sizeof(DecodeCta),
                             cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && !plan->dec_pos.empty())
+        e = cudaMemcpyAsync(ws + plan->ws.off_dec_pos, plan->dec_pos.data(), plan->dec_pos.size() * sizeof(int32_t),
+                            cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && !plan->tile_splits.empty())
         e = cudaMemcpyAsync(ws + plan->ws.off_tile_splits, plan->tile_splits.data(),
                             plan->tile_splits.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
@@ -1831,6 +1863,35 @@ pod_status pod_attn_gather_probe(const pod_plan* plan, const void* kv_pool, int6
         page_indices, req, static_cast<int>(ctx), out);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "gather_probe");
+    return POD_OK;
+}
+
+pod_status pod_attn_append_kv(const pod_plan* plan, const void* k_new_prefill, const void* v_new_prefill,
+                              const void* k_new_decode, const void* v_new_decode, void* k_pool, void* v_pool,
+                              int64_t num_pages, const int32_t* page_indptr, const int32_t* page_indices,
+                              void* workspace, void* stream) {
+    (void)num_pages;
+    if (!plan || !k_pool || !v_pool || !page_indptr || !page_indices || !workspace) return POD_ERR_INVALID_ARGUMENT;
+    if (plan->shape.head_dim != kHeadDim || plan->batch.page_size != 16) {
+        set_last_error("append_kv: only head_dim 128 / page_size 16 are compiled");
+        return POD_ERR_UNSUPPORTED;
+    }
+    const int chunk = plan->batch.has_prefill ? static_cast<int>(plan->batch.prefill.chunk_size) : 0;
+    const int ndec = static_cast<int>(plan->decode_ctx.size());
+    if ((chunk > 0 && (!k_new_prefill || !v_new_prefill)) || (ndec > 0 && (!k_new_decode || !v_new_decode)))
+        return POD_ERR_INVALID_ARGUMENT;
+    if (chunk + ndec == 0) return POD_OK;
+    const int hkv = plan->shape.num_kv_heads;
+    const int rows = (chunk + ndec) * hkv;
+    const int32_t* dec_pos =
+        reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(workspace) + plan->ws.off_dec_pos);
+    append_kv_kernel<<<(rows + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(k_new_prefill), static_cast<const uint4*>(v_new_prefill),
+        static_cast<const uint4*>(k_new_decode), static_cast<const uint4*>(v_new_decode), static_cast<uint4*>(k_pool),
+        static_cast<uint4*>(v_pool), page_indptr, page_indices, dec_pos, chunk,
+        chunk > 0 ? static_cast<int>(plan->batch.prefill.position_offset) : 0, ndec, hkv, plan->batch.kv_layout);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "append_kv launch");
     return POD_OK;
 }
 

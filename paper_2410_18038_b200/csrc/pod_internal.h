@@ -65,6 +65,7 @@ struct WorkspaceLayout {
     size_t off_ppart_lse = 0;     // [max_splits][chunk][Hq]
     size_t off_dpart_o = 0;       // [num_decodes][splits][Hq][d]
     size_t off_dpart_lse = 0;     // [num_decodes][splits][Hq]
+    size_t off_dec_pos = 0;       // int32 per decode: position of its new token (context_len - 1)
     size_t total = 0;
 };
 
@@ -84,6 +85,7 @@ struct pod_plan {
     std::vector<pod::PrefillCta> pctas;
     std::vector<pod::DecodeCta> dctas;
     std::vector<int32_t> tile_splits;
+    std::vector<int32_t> dec_pos;  // context_len - 1 per decode (KV append)
     int64_t decode_splits = 1;
     int64_t prefill_ratio = 1;
     int64_t decode_ratio = 1;

@@ -428,7 +428,11 @@ void layout_workspace(pod_plan& p) {
     off = align(off + dp * s.head_dim * sizeof(float));
     p.ws.off_dpart_lse = off;
     off = align(off + dp * sizeof(float));
+    p.ws.off_dec_pos = off;
+    off = align(off + p.decode_ctx.size() * sizeof(int32_t));
     p.ws.total = off;
+    p.dec_pos.clear();
+    for (int64_t c : p.decode_ctx) p.dec_pos.push_back(static_cast<int32_t>(c - 1));
 }
 
 pod_tile_config b200_tile_config(const pod_plan& p) {

@@ -86,6 +86,16 @@ class PodAttention:
             _check(L.pod_attn_run_part(self.plan.handle, m - 2, *args), "pod_attn_run_part")
         return out
 
+    def append_kv(self, k_new_prefill, v_new_prefill, k_new_decode, v_new_decode, k_pool, v_pool, page_indptr,
+                  page_indices, stream=None) -> None:
+        """pod_attn_append_kv: scatter the batch's new K/V rows ([chunk][Hkv][d] and
+        [B][Hkv][d], pool dtype) into their page slots (before run())."""
+        st = stream or torch.cuda.current_stream(self.device)
+        _check(lib().pod_attn_append_kv(self.plan.handle, _ptr(k_new_prefill), _ptr(v_new_prefill), _ptr(k_new_decode),
+                                        _ptr(v_new_decode), _ptr(k_pool), _ptr(v_pool), C.c_int64(k_pool.shape[0]),
+                                        _ptr(page_indptr), _ptr(page_indices), _ptr(self.workspace),
+                                        C.c_void_p(st.cuda_stream)), "pod_attn_append_kv")
+
     def gather_probe(self, pool: torch.Tensor, page_indptr, page_indices, req: int, ctx: int) -> torch.Tensor:
         s = self.batch.shape
         out = torch.empty(ctx, s.num_kv_heads, s.head_dim, dtype=torch.int16, device=self.device)

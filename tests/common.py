@@ -86,3 +86,37 @@ def compare_decode(wl, o_gpu: np.ndarray, lse_gpu: np.ndarray, requests=None, kv
         eo = max(eo, rel_err(o_gpu[r, h * G:(h + 1) * G], o))
         el = max(el, float(np.abs(lse_gpu[r, h * G:(h + 1) * G] - lse).max()))
     return eo, el
+
+
+def new_token_rows(wl):
+    """The batch's new K/V rows as the KV-append step receives them (16-bit words):
+    prefill tokens = positions [offset, offset + chunk) of request 0, decode b's token
+    = position ctx_b - 1 of its request.  Returns (kp, vp, kd, vd) as uint16 arrays
+    [chunk][Hkv][d] / [B][Hkv][d] (None when absent), read from the HND pool at the
+    tokens' (page, slot) -- exactly the cached bits, for any 16-bit dtype."""
+    import torch
+
+    kb = wl.k_pool.cpu().view(torch.int16).numpy().view(np.uint16)
+    vb = wl.v_pool.cpu().view(torch.int16).numpy().view(np.uint16)
+    slots = token_slots(wl)
+    k = np.stack([kb[page, :, slot, :] for page, slot in slots])
+    v = np.stack([vb[page, :, slot, :] for page, slot in slots])
+    c = wl.batch.prefill.chunk_size if wl.batch.prefill is not None else 0
+    kp, vp = (k[:c], v[:c]) if c else (None, None)
+    kd, vd = (k[c:], v[c:]) if wl.batch.decodes else (None, None)
+    return kp, vp, kd, vd
+
+
+def token_slots(wl):
+    """(page, slot) of every new token, prefill first then decodes (HND pool indexing)."""
+    ip, ix = wl.page_indptr.cpu().tolist(), wl.page_indices.cpu().tolist()
+    b = wl.batch
+    out, base = [], 0
+    if b.prefill is not None:
+        off, c = b.prefill.position_offset, b.prefill.chunk_size
+        out += [(ix[ip[0] + t // 16], t % 16) for t in range(off, off + c)]
+        base = 1
+    for i, d in enumerate(b.decodes):
+        t = d.context_len - 1
+        out.append((ix[ip[base + i] + t // 16], t % 16))
+    return out

@@ -144,6 +144,57 @@ def test_nhd_layout():
     _check(wl, out)
 
 
+@pytest.mark.parametrize("layout", ["hnd", "nhd"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_kv_append_is_bit_exact(layout, dtype):
+    """pod_attn_append_kv scatters the chunk's and the decodes' new K/V rows into
+    their page slots: after zeroing those slots and appending, the pools equal the
+    original pools bit for bit (pages crossed mid-chunk, decode ctx 1 / 16 / 17)."""
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+    from tests.common import new_token_rows, token_slots
+
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=45, offset=27, decode_ctx=[1, 16, 17, 300])
+    wl = build_workload(batch, device="cuda", dtype=dtype)
+    kp, vp, kd, vd = (torch.from_numpy(x.astype(np.int16)).view(dtype).cuda() for x in new_token_rows(wl))
+    slots = token_slots(wl)
+    k_full, v_full = wl.k_pool.clone(), wl.v_pool.clone()
+    k_pool, v_pool = wl.k_pool.clone(), wl.v_pool.clone()
+    for page, slot in slots:
+        k_pool[page, :, slot, :] = 0
+        v_pool[page, :, slot, :] = 0
+    if layout == "nhd":
+        batch.kv_layout = POD_KV_NHD
+        k_full, v_full = (t.permute(0, 2, 1, 3).contiguous() for t in (k_full, v_full))
+        k_pool, v_pool = (t.permute(0, 2, 1, 3).contiguous() for t in (k_pool, v_pool))
+    assert not torch.equal(k_pool, k_full)
+    op = PodAttention(batch)
+    op.append_kv(kp, vp, kd, vd, k_pool, v_pool, wl.page_indptr, wl.page_indices)
+    torch.cuda.synchronize()
+    assert torch.equal(k_pool.view(torch.int16), k_full.view(torch.int16))
+    assert torch.equal(v_pool.view(torch.int16), v_full.view(torch.int16))
+
+
+def test_append_then_attend_matches_oracle():
+    """A layer step as a caller runs it: append the new tokens' K/V, then the fused
+    attention over the updated cache (same stream) -- equals the oracle."""
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+    from tests.common import new_token_rows, token_slots
+
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=96, offset=160, decode_ctx=[300, 77, 1024])
+    wl = build_workload(batch, device="cuda")
+    kp, vp, kd, vd = (torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16).cuda() for x in new_token_rows(wl))
+    for page, slot in token_slots(wl):
+        wl.k_pool[page, :, slot, :] = 0
+        wl.v_pool[page, :, slot, :] = 0
+    op = PodAttention(batch)
+    op.append_kv(kp, vp, kd, vd, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+    out = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+    torch.cuda.synchronize()
+    _check(wl, out)
+
+
 def test_causality_is_bitwise():
     _need_gpu()
     off, chunk, r = 300, 64, 20

@@ -72,3 +72,33 @@ def test_gather_out_of_range_page_is_rejected():
         assert e.status == 4
     else:
         raise AssertionError("expected out_of_range")
+
+
+def test_kv_append_oracle_round_trip_hnd_and_nhd():
+    """Oracle KV append (test infrastructure): zero the new tokens' slots, scatter the
+    rows back through the block table -> the pool is bit-identical again (both layouts),
+    and the rows are what gather_pages reads at those positions."""
+    from tests.common import new_token_rows, token_slots
+
+    shape = ModelShape(8, 2, 128, math.sqrt(128))
+    batch = make_batch(shape, chunk=20, offset=37, decode_ctx=[1, 15, 16, 17, 100])
+    wl = build_workload(batch, pad_value=7.0)
+    ip, ix = wl.page_indptr.numpy(), wl.page_indices.numpy()
+    kp, vp, kd, vd = new_token_rows(wl)
+    slots = token_slots(wl)
+    for layout in (0, 1):
+        full = _bits(wl.k_pool)
+        if layout == 1:
+            full = np.ascontiguousarray(full.transpose(0, 2, 1, 3))
+        pool = full.copy()
+        for page, slot in slots:
+            if layout == 0:
+                pool[page, :, slot, :] = 0
+            else:
+                pool[page, slot, :, :] = 0
+        assert not np.array_equal(pool, full)
+        O.append_kv(pool, layout, ip, ix, 0, batch.prefill.position_offset, kp)
+        for i, d in enumerate(batch.decodes):
+            O.append_kv(pool, layout, ip, ix, 1 + i, d.context_len - 1, kd[i:i + 1])
+        assert np.array_equal(pool, full)
+    assert kp.shape == (20, 2, 128) and kd.shape == (5, 2, 128) and vp.shape == kp.shape and vd.shape == kd.shape
