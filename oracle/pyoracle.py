@@ -99,6 +99,13 @@ def ref() -> C.CDLL:
         l.ref_run_shards.restype = C.c_double
         l.ref_sched_replay.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_int64, _i64p, _i64p,
                                        C.c_void_p, C.c_void_p]
+        l.ref_generate_trace.argtypes = [C.c_double, C.c_int64, C.c_int, C.c_double, C.c_double, C.c_int,
+                                         C.c_double, C.c_double, C.c_uint64, _dp, _i64p, _i64p]
+        l.ref_run_serving_linear.argtypes = [C.c_int64, _dp, _i64p, _i64p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                             C.c_double, C.c_double, C.c_int64, _dp, _dp, _i64p, _i64p, _i64p,
+                                             _i64p, _dp, _dp, _dp]
+        l.ref_generate_trace.restype = C.c_int
+        l.ref_run_serving_linear.restype = C.c_int
         for f in ("ref_tiled_prefill", "ref_decode_splitk", "ref_merge_partials", "ref_naive_attention",
                   "ref_decode_attention", "ref_gqa_kv_head", "ref_decompose_hybrid", "ref_select_tile_config",
                   "ref_limit_prefill_splits", "ref_make_tile_config"):
@@ -359,3 +366,40 @@ def run_shards(shards, d, scale, tile_q, tile_kv, threads):
     if st.value:
         raise OracleError(st.value, "run_shards")
     return sec
+
+
+_DIST_KIND = {"fixed": 0, "uniform": 1, "lognormal": 2}
+
+
+def ref_generate_trace(qps, n, pdist, ddist, seed):
+    """The reference's generate_trace (serving.hpp:101-118) -> (arrival, prefill, decode) arrays."""
+    arr = np.zeros(n)
+    pt = np.zeros(n, np.int64)
+    dt = np.zeros(n, np.int64)
+    st = ref().ref_generate_trace(qps, n, _DIST_KIND[pdist.kind], pdist.a, pdist.b, _DIST_KIND[ddist.kind],
+                                  ddist.a, ddist.b, seed, _d(arr), pt.ctypes.data_as(_i64p), dt.ctypes.data_as(_i64p))
+    if st:
+        raise OracleError(st, "ref_generate_trace")
+    return arr, pt, dt
+
+
+def ref_run_serving_linear(trace, policy, c0, c1):
+    """The reference's run_serving (serving.hpp:180-330) with cost c0 + c1 * tokens."""
+    n = len(trace)
+    arr = np.array([r.arrival_time for r in trace], np.float64)
+    pt = np.array([r.prefill_tokens for r in trace], np.int64)
+    dt = np.array([r.decode_tokens for r in trace], np.int64)
+    cap = 1 << 20
+    t0, t1 = np.zeros(cap), np.zeros(cap)
+    pr, ptk, nd = (np.zeros(cap, np.int64) for _ in range(3))
+    nit = np.zeros(1, np.int64)
+    ttft, lat, met = np.zeros(n), np.zeros(n), np.zeros(9)
+    i64 = lambda a: a.ctypes.data_as(_i64p)  # noqa: E731
+    st = ref().ref_run_serving_linear(n, _d(arr), i64(pt), i64(dt), 0 if policy.kind == "prefill_prioritized" else 1,
+                                      policy.chunk_size, policy.max_batch, policy.token_budget, c0, c1, cap,
+                                      _d(t0), _d(t1), i64(pr), i64(ptk), i64(nd), i64(nit), _d(ttft), _d(lat), _d(met))
+    if st:
+        raise OracleError(st, "ref_run_serving_linear")
+    k = int(nit[0])
+    its = list(zip(t0[:k], t1[:k], pr[:k], ptk[:k], nd[:k]))
+    return its, ttft, lat, met

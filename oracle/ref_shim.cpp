@@ -20,6 +20,7 @@
 #include "attnsim/gpu.hpp"
 #include "attnsim/gpu_sim.hpp"
 #include "attnsim/rng.hpp"
+#include "attnsim/serving.hpp"
 #include "attnsim/types.hpp"
 #include "attnsim/work_decomp.hpp"
 
@@ -386,6 +387,65 @@ double ref_run_shards(const ref_shard* shards, int64_t n, int d, double scale, i
     for (int x : st)
         if (x) *status = x;
     return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// Serving simulator (serving.hpp): trace generation and the iteration loop with a
+// linear cost c0 + c1 * tokens (the cost the reference's own serving tests use), for
+// pinning the Python serving-loop port (paper_2410_18038_b200/serving.py).
+static TokenDist make_dist(int kind, double a, double b) {
+    TokenDist t;
+    t.kind = kind == 0 ? TokenDist::Kind::Fixed : kind == 1 ? TokenDist::Kind::Uniform : TokenDist::Kind::LogNormal;
+    t.a = a;
+    t.b = b;
+    return t;
+}
+
+int ref_generate_trace(double qps, int64_t n, int pk, double pa, double pb, int dk, double da, double db,
+                       uint64_t seed, double* arrival, int64_t* ptok, int64_t* dtok) {
+    return guarded([&] {
+        auto tr = generate_trace(qps, n, make_dist(pk, pa, pb), make_dist(dk, da, db), seed);
+        for (int64_t i = 0; i < n; ++i) {
+            arrival[i] = tr[i].arrival_time;
+            ptok[i] = tr[i].prefill_tokens;
+            dtok[i] = tr[i].decode_tokens;
+        }
+    });
+}
+
+// metrics: ttft50, ttft99, tbt50, tbt99, lat50, lat99, throughput, stall@200, stall@500
+int ref_run_serving_linear(int64_t n, const double* arrival, const int64_t* ptok, const int64_t* dtok,
+                           int policy_kind, int64_t chunk, int64_t max_batch, int64_t token_budget, double c0,
+                           double c1, int64_t max_iters, double* it_t0, double* it_t1, int64_t* it_preq,
+                           int64_t* it_ptok, int64_t* it_ndec, int64_t* n_iters, double* ttft, double* latency,
+                           double* metrics) {
+    return guarded([&] {
+        std::vector<Request> tr(n);
+        for (int64_t i = 0; i < n; ++i) tr[i] = Request{arrival[i], ptok[i], dtok[i]};
+        SchedulerPolicy pol = policy_kind == 0 ? SchedulerPolicy::prefill_prioritized()
+                                               : SchedulerPolicy::chunked_hybrid(chunk, max_batch, token_budget);
+        auto cost = [&](const HybridBatchSpec& b, bool) {
+            long tokens = b.prefill ? b.prefill->chunk_size : 0;
+            return c0 + c1 * (tokens + (double)b.decodes.size());
+        };
+        ModelShape shape{16, 4, 128, 11.3137};
+        auto r = run_serving(tr, pol, cost, false, shape, {200.0, 500.0});
+        *n_iters = (int64_t)r.iterations.size();
+        for (size_t i = 0; i < r.iterations.size() && (int64_t)i < max_iters; ++i) {
+            it_t0[i] = r.iterations[i].t_start;
+            it_t1[i] = r.iterations[i].t_end;
+            it_preq[i] = r.iterations[i].prefill_request;
+            it_ptok[i] = r.iterations[i].prefill_tokens;
+            it_ndec[i] = r.iterations[i].decode_requests;
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            ttft[i] = r.ttft[i];
+            latency[i] = r.latency[i];
+        }
+        const Metrics& m = r.metrics;
+        double v[9] = {m.ttft_p50, m.ttft_p99, m.tbt_p50, m.tbt_p99, m.latency_p50, m.latency_p99, m.throughput,
+                       m.stall_pct_at[0].second, m.stall_pct_at[1].second};
+        std::memcpy(metrics, v, sizeof(v));
+    });
 }
 
 }  // extern "C"
