@@ -40,6 +40,10 @@ CONFIGS = {
     "c2_b32": (32, 8, 1024, 15360, 32, 16384),
     "c2_b64": (32, 8, 1024, 15360, 64, 16384),
     "c4": (32, 32, 2048, 2048, 128, 4096),
+    # one rank's share of C2 B=64 under KV-head-group TP (what each GPU runs at T = 2/4/8)
+    "c3_tp2_rank": (16, 4, 1024, 15360, 64, 16384),
+    "c3_tp4_rank": (8, 2, 1024, 15360, 64, 16384),
+    "c3_tp8_rank": (4, 1, 1024, 15360, 64, 16384),
 }
 DEFAULT_CONFIG = "c2_b64"
 
