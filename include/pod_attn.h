@@ -131,8 +131,9 @@ enum {
     POD_POLICY_WARPSPEC = 7,     /* one CTA per SM hosting a prefill engine (two 128-row
                                     M-blocks, Q/S/P/O in TMEM) and a decode warp group side
                                     by side; each binds items from its pool at runtime */
-    POD_POLICY_AUTO = 8          /* default: WARPSPEC when the decode share of the serial
-                                    time is >= 0.25 (decode-heavy batches), else COMPLEMENT
+    POD_POLICY_AUTO = 8          /* default: WARPSPEC for hybrid batches whose decode share
+                                    of the serial time is >= 0.25 with decode contexts >= 2K
+                                    on average, else COMPLEMENT
                                     (the plan records the resolved policy) */
 };
 

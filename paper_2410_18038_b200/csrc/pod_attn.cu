@@ -1033,9 +1033,18 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
     // Software pipeline over pages: the score MMAs of page i+1 are issued before the
     // softmax and P V of page i, so their latency overlaps the dependent chain of i.
     float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    // debug trace (POD_TRACE): CTA 0, items by claim order, rows 512 + k
+    int32_t* dtr = nullptr;
+    if (p.trace && blockIdx.x == 0 && p.role_log) {
+        int32_t* cnt = p.role_log + p.trace + 767 * 8 + 7;  // item counter (last row)
+        const int k = __shfl_sync(0xffffffffu, (warp == 0 && lane == 0) ? atomicAdd(cnt, 0) : 0, 0);
+        if (k < 200) dtr = p.role_log + p.trace + (512 + k) * 8;
+        if (dtr && lane == 0) dtr[warp == 0 ? 0 : 7] = static_cast<int32_t>(clock64());
+    }
     if (npg > 0) {
         const int st = dpos % kDecStages;
         ptx::mbar_wait(bars + 8 * st, (dpos / kDecStages) & 1);
+        if (dtr && lane == 0 && warp == 0) dtr[1] = static_cast<int32_t>(clock64());
         scores(ring + st * kDecStageBytes, sc);
     }
     for (int i = 0; i < npg; ++i) {
@@ -1134,6 +1143,7 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
         }
     }
     dpos += npg;
+    if (dtr && lane == 0) atomicMax(&dtr[2 + (warp == 0 ? 0 : 1)], static_cast<int32_t>(clock64()));
     if constexpr (kPack) {  // O = O_hi + O_lo (hi lanes keep the sum)
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -1183,6 +1193,7 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
             acc += red[(w * G + g) * kStride + d] * wt;
         }
         const int qhead = h * G + g;
+        if (dtr && idx == tid && tid == 0) dtr[4] = static_cast<int32_t>(clock64());
         const float out = acc / L;
         const float lse = (M + ptx::lg2(L)) * kLn2;
         if (job.n_splits == 1) {
@@ -1193,6 +1204,10 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
             p.dpart_o[row * kHeadDim + d] = out;
             if (d == 0) p.dpart_lse[row] = lse;
         }
+    }
+    if (dtr && tid == 0) {
+        dtr[5] = static_cast<int32_t>(clock64());
+        atomicAdd(p.role_log + p.trace + 767 * 8 + 7, 1);
     }
 }
 
@@ -1644,13 +1659,14 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.w_decode = static_cast<float>(plan->w_decode);
     p.p_split = plan->opts.precision == POD_PRECISION_SPLIT ? 1 : 0;
     {
-        const char* e = std::getenv("POD_GRID_PER_SM");  // experiment knob
-        p.grid_per_sm = e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+        static const char* grid_env = std::getenv("POD_GRID_PER_SM");  // experiment knob
+        p.grid_per_sm = grid_env ? std::max(1, std::min(2, std::atoi(grid_env))) : 2;
     }
     {
-        const char* e = std::getenv("POD_TRACE");  // debug knob
-        p.trace = (e && std::atoi(e)) ? static_cast<int32_t>(8 * (plan->pctas.size() + plan->dctas.size())) : 0;
-        p.trace_mode = e ? std::atoi(e) : 0;
+        static const char* trace_env = std::getenv("POD_TRACE");  // debug knob
+        const int t = trace_env ? std::atoi(trace_env) : 0;
+        p.trace = t ? static_cast<int32_t>(8 * (plan->pctas.size() + plan->dctas.size())) : 0;
+        p.trace_mode = t;
     }
     p.prefill_sms = plan->prefill_sms;
     p.num_sms = plan->dev.num_sms;
@@ -1702,7 +1718,8 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
                                                                                maps.dv);
         } else {
             int grid = std::min(items, q.grid_per_sm * nsm);  // persistent: 2 resident CTAs per SM
-            if (const char* e = std::getenv("POD_GRID_CTAS")) grid = std::min(grid, std::max(1, std::atoi(e)));
+            static const char* grid_ctas = std::getenv("POD_GRID_CTAS");  // experiment knob
+            if (grid_ctas) grid = std::min(grid, std::max(1, std::atoi(grid_ctas)));
             pod_fused_kernel<G, kFmt, false><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk,
                                                                                 maps.dv);
         }
@@ -1766,8 +1783,20 @@ pod_status run_mode(const pod_plan* plan, int mode, const void* q_prefill, const
     if (need_p && (!q_prefill || !o_prefill || !lse_prefill)) return POD_ERR_INVALID_ARGUMENT;
     if (need_d && (!q_decode || !o_decode || !lse_decode)) return POD_ERR_INVALID_ARGUMENT;
     Maps maps;
-    st = make_maps(plan, q_prefill, k_pool, v_pool, num_pages, &maps);
-    if (st != POD_OK) return st;
+    static_assert(sizeof(Maps) == sizeof(plan->map_blob), "map cache size");
+    pod_plan* mp = const_cast<pod_plan*>(plan);  // the cache is not part of the plan's semantics
+    if (mp->map_key[0] == q_prefill && mp->map_key[1] == k_pool && mp->map_key[2] == v_pool &&
+        mp->map_pages == num_pages) {
+        std::memcpy(&maps, mp->map_blob, sizeof(Maps));
+    } else {
+        st = make_maps(plan, q_prefill, k_pool, v_pool, num_pages, &maps);
+        if (st != POD_OK) return st;
+        std::memcpy(mp->map_blob, &maps, sizeof(Maps));
+        mp->map_key[0] = q_prefill;
+        mp->map_key[1] = k_pool;
+        mp->map_key[2] = v_pool;
+        mp->map_pages = num_pages;
+    }
     RunParams p = make_params(plan, q_prefill, q_decode, k_pool, v_pool, num_pages, indptr, indices, o_prefill,
                               lse_prefill, o_decode, lse_decode, workspace);
     if (mode == 2) p.num_dctas = 0;

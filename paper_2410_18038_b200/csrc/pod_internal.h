@@ -98,6 +98,11 @@ struct pod_plan {
     int32_t prefill_sms = 0; // POD_POLICY_PARTITION: SMs whose slots bind prefill first
     pod::WorkspaceLayout ws;
     int32_t* role_log = nullptr;
+    // Tensor maps of the last run (5 x CUtensorMap, 128 B each), re-encoded only when
+    // the Q / K / V pointers or the pool size change: host launch cost per run.
+    const void* map_key[3] = {nullptr, nullptr, nullptr};
+    int64_t map_pages = -1;
+    alignas(64) unsigned char map_blob[5 * 128];
 };
 
 namespace pod {

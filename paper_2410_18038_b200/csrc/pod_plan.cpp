@@ -473,7 +473,14 @@ void build(pod_plan& p) {
         // prefill-heavy batches run faster on two POD CTAs per SM
         // (C2 at B = 8/16/32/64: 508 vs 542, 554 vs 557, 592 vs 671, 738 vs 800 us;
         // C1: 82 vs 89 us -- one-CTA-per-SM vs two-CTA POD, best split caps)
-        p.opts.policy = decode_share(p) >= 0.25 ? POD_POLICY_WARPSPEC : POD_POLICY_COMPLEMENT;
+        // Decode-only and short-context batches keep the two-CTA kernel: more decode
+        // groups per SM amortise the per-item latency (64 x 2K decode-only: 107 vs
+        // 126 us; 512@1536 + 64 x 1K: 93 vs 106 us).
+        double avg_ctx = 0;
+        for (int64_t c : p.decode_ctx) avg_ctx += static_cast<double>(c);
+        avg_ctx = p.decode_ctx.empty() ? 0 : avg_ctx / static_cast<double>(p.decode_ctx.size());
+        p.opts.policy = (p.batch.has_prefill && decode_share(p) >= 0.25 && avg_ctx >= 2048) ? POD_POLICY_WARPSPEC
+                                                                                              : POD_POLICY_COMPLEMENT;
     }
     if (p.opts.tile_override) {
         p.cfg = *p.opts.tile_override;
