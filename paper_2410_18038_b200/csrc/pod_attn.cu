@@ -51,6 +51,9 @@ constexpr uint32_t kOffV = kOffK + 2 * kKvStageBytes;       // 2 stages
 #ifndef POD_DEC_WARPS
 #define POD_DEC_WARPS 4
 #endif
+#ifndef POD_DEC_SLEEP
+#define POD_DEC_SLEEP 0  // decode page waits: spin (0) or __nanosleep back-off
+#endif
 // Warps that stream one decode item (the planner's 4 virtual decode CTAs,
 // kDecodeWarps, are the item's logical split; the kernel may use more warps).
 constexpr int kDecWarpsK = POD_DEC_WARPS;
@@ -349,7 +352,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                     pk.init(p.page_indices + pbeg, npages, br.kt0 / 16);
                     pvi.init(p.page_indices + pbeg, npages, br.kt0 / 16);
                 }
-                if (qb > 0) ptx::mbar_wait(b_qempty, (qb - 1) & 1);
+                if (qb > 0) ptx::mbar_wait_relaxed<>(b_qempty, (qb - 1) & 1);
                 ptx::mbar_arrive_expect_tx_elect(b_qfull, kQBytes);
                 ptx::tma_load_3d_elect(sQ, tmq, b_qfull, 0, job.kv_head * G, br.r0);
                 ptx::tma_load_3d_elect(sQ + kMBlock * 128, tmq, b_qfull, 64, job.kv_head * G, br.r0);
@@ -357,7 +360,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                 for (int t = 0; t <= br.nt; ++t) {
                     if (t < br.nt) {  // K of tile t
                         const int gg = g + t, st = gg & 1;
-                        if (gg >= 2) ptx::mbar_wait(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
+                        if (gg >= 2) ptx::mbar_wait_relaxed<>(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t, 4);
                         ptx::mbar_arrive_expect_tx_elect(b_kfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmk, sK + st * kKvStageBytes, b_kfull + 8 * st,
@@ -366,7 +369,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                     }
                     if (t > 0) {  // V of tile t-1
                         const int gg = g + t - 1, st = gg & 1;
-                        if (gg >= 2) ptx::mbar_wait(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
+                        if (gg >= 2) ptx::mbar_wait_relaxed<>(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t - 1, 6);
                         ptx::mbar_arrive_expect_tx_elect(b_vfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
@@ -633,14 +636,14 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
                 for (int t = 0; t <= nt && nt > 0; ++t) {
                     if (t < nt) {
                         const int gg = g + t, st = gg & 1;
-                        if (gg >= 2) ptx::mbar_wait(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
+                        if (gg >= 2) ptx::mbar_wait_relaxed<>(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
                         ptx::mbar_arrive_expect_tx_elect(b_kfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmk, sK + st * kKvStageBytes, b_kfull + 8 * st,
                                              ra.kt0 + t * kKvTile, job.kv_head, pk);
                     }
                     if (t > 0) {
                         const int gg = g + t - 1, st = gg & 1;
-                        if (gg >= 2) ptx::mbar_wait(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
+                        if (gg >= 2) ptx::mbar_wait_relaxed<>(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
                         ptx::mbar_arrive_expect_tx_elect(b_vfull + 8 * st, kKvStageBytes);
                         prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
                                              ra.kt0 + (t - 1) * kKvTile, job.kv_head, pvi);
@@ -1054,7 +1057,11 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
         float scn[4] = {0.f, 0.f, 0.f, 0.f};
         if (i + 1 < npg) {
             const int st1 = (n + 1) % kDecStages;
+#if POD_DEC_SLEEP > 0
+            ptx::mbar_wait_relaxed<POD_DEC_SLEEP>(bars + 8 * st1, ((n + 1) / kDecStages) & 1);
+#else
             ptx::mbar_wait(bars + 8 * st1, ((n + 1) / kDecStages) & 1);
+#endif
             scores(ring + st1 * kDecStageBytes, scn);
         }
         // sc: (key g, head 2t), (key g, head 2t+1), (key g+8, head 2t), (key g+8, head 2t+1)

@@ -446,7 +446,8 @@ pod_tile_config b200_tile_config(const pod_plan& p) {
     pod_tile_config c = make_tile_config(2);
     const int group = p.shape.num_q_heads / p.shape.num_kv_heads;
     // slots policy: two 128-row M-blocks per prefill item (ping-pong engine)
-    const bool two_blocks = p.opts.policy == POD_POLICY_SLOTS || p.opts.policy == POD_POLICY_WARPSPEC;
+    const bool two_blocks = (p.opts.policy == POD_POLICY_SLOTS || p.opts.policy == POD_POLICY_WARPSPEC) &&
+                            !std::getenv("POD_ONE_BLOCK");  // experiment knob
     const int rows = (two_blocks ? 2 : 1) * pod::kMBlock;
     c.prefill_tile_q = std::max(1, rows / group);
     c.tile_kv = pod::kKvTile;

@@ -23,6 +23,20 @@
 // atomic tickets on the same counters (gpu_sim.hpp:114-131).
 #pragma once
 
+#ifndef POD_SM_MMA_SLEEP
+#define POD_SM_MMA_SLEEP 0
+#endif
+#ifndef POD_SM_SOFTMAX_SLEEP
+#define POD_SM_SOFTMAX_SLEEP 0
+#endif
+// wait helper: spin (try_wait) or back off with __nanosleep(kNs)
+template <int kNs>
+__device__ __forceinline__ void sm_wait(uint32_t bar, uint32_t parity) {
+    if constexpr (kNs > 0)
+        ptx::mbar_wait_relaxed<kNs>(bar, parity);
+    else
+        ptx::mbar_wait(bar, parity);
+}
 namespace sm3 {
 #ifndef POD_SM_DUAL_MMA
 #define POD_SM_DUAL_MMA 0
@@ -152,13 +166,13 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         for (int t = 0; t <= nt && nt > 0; ++t) {
             if (t < nt) {  // K of tile t
                 const int gg = s0.g + t, st = gg % kNS;
-                if (gg >= kNS) ptx::mbar_wait(bar(6 + st), ((gg / kNS) - 1) & 1);
+                if (gg >= kNS) ptx::mbar_wait_relaxed<>(bar(6 + st), ((gg / kNS) - 1) & 1);
                 ptx::mbar_arrive_expect_tx_elect(bar(2 + st), kStage);
                 load_tile32(p, tmk, sK + st * kStage, bar(2 + st), kt0 + t * kTN, job.kv_head, ids);
             }
             if (t > 0) {  // V of tile t-1
                 const int gg = s0.g + t - 1, st = gg % kNS;
-                if (gg >= kNS) ptx::mbar_wait(bar(14 + st), ((gg / kNS) - 1) & 1);
+                if (gg >= kNS) ptx::mbar_wait_relaxed<>(bar(14 + st), ((gg / kNS) - 1) & 1);
                 ptx::mbar_arrive_expect_tx_elect(bar(10 + st), kStage);
                 load_tile32(p, tmv, sV + st * kStage, bar(10 + st), kt0 + (t - 1) * kTN, job.kv_head, ids);
             }
@@ -169,11 +183,11 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         // pipe), so the softmax of tile t+1 overlaps PV_X(t) and QK_X(t+2); the two
         // blocks interleave on the tensor core.
         if (nt > 0) {
-            ptx::mbar_wait(bar(0), s0.nq[0] & 1);
-            if (hasB) ptx::mbar_wait(bar(1), s0.nq[1] & 1);
+            sm_wait<POD_SM_MMA_SLEEP>(bar(0), s0.nq[0] & 1);
+            if (hasB) sm_wait<POD_SM_MMA_SLEEP>(bar(1), s0.nq[1] & 1);
             for (int j = 0; j < 2 && j < nt; ++j) {
                 const int gg = s0.g + j, st = gg % kNS;
-                ptx::mbar_wait(bar(2 + st), (gg / kNS) & 1);
+                sm_wait<POD_SM_MMA_SLEEP>(bar(2 + st), (gg / kNS) & 1);
                 ptx::tc_fence_after();
                 const int bA = (s0.n[0] + j) & 1, bB = (s0.n[1] + j) & 1;
                 issue_qk32<kFmt>(tmem + kSA + 32 * bA, tmem + kQA, sK + st * kStage);
@@ -189,15 +203,15 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                 const int g2 = gg + 2, st2 = g2 % kNS;
                 const bool more = t + 2 < nt;
                 const int nA = s0.n[0] + t, bA = nA & 1;
-                ptx::mbar_wait(bar(22 + bA), (nA >> 1) & 1);
+                sm_wait<POD_SM_MMA_SLEEP>(bar(22 + bA), (nA >> 1) & 1);
                 trace_stamp(p, first, t, 4);
-                ptx::mbar_wait(bar(10 + st), (gg / kNS) & 1);
+                sm_wait<POD_SM_MMA_SLEEP>(bar(10 + st), (gg / kNS) & 1);
                 ptx::tc_fence_after();
                 issue_pv32<kFmt>(tmem + kOA, tmem + kSA + 32 * bA, sV + st * kStage, t > 0, p.p_split != 0);
                 ptx::umma_commit_elect(bar(26 + bA));
                 trace_stamp(p, first, t, 5);
                 if (more) {
-                    ptx::mbar_wait(bar(2 + st2), (g2 / kNS) & 1);
+                    sm_wait<POD_SM_MMA_SLEEP>(bar(2 + st2), (g2 / kNS) & 1);
                     ptx::tc_fence_after();
                     issue_qk32<kFmt>(tmem + kSA + 32 * bA, tmem + kQA, sK + st2 * kStage);
                     ptx::umma_commit_elect(bar(18 + bA));
@@ -205,7 +219,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                 trace_stamp(p, first, t, 6);
                 if (hasB) {
                     const int nB = s0.n[1] + t, bB = nB & 1;
-                    ptx::mbar_wait(bar(24 + bB), (nB >> 1) & 1);
+                    sm_wait<POD_SM_MMA_SLEEP>(bar(24 + bB), (nB >> 1) & 1);
                     ptx::tc_fence_after();
                     issue_pv32<kFmt>(tmem + kOB, tmem + kSB + 32 * bB, sV + st * kStage, t > 0, p.p_split != 0);
                     ptx::umma_commit_elect(bar(28 + bB));
@@ -325,7 +339,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             const int n = s0.n[X] + t, b = n & 1;
             const uint32_t s_addr = lane_base + (X ? kSB : kSA) + 32 * b;
             if (lane == 0 && q == 0) trace_stamp(p, first, 256 * X + t, 0);
-            ptx::mbar_wait(bar(18 + 2 * X + b), (n >> 1) & 1);
+            sm_wait<POD_SM_SOFTMAX_SLEEP>(bar(18 + 2 * X + b), (n >> 1) & 1);
             if (lane == 0 && q == 0) trace_stamp(p, first, 256 * X + t, 1);
             ptx::tc_fence_after();
             float s[kTN];

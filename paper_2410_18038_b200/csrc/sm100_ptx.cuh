@@ -59,6 +59,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+// Wait with a sleep back-off, for a warp that is not latency-critical (a TMA
+// producer running stages ahead): spinning on try_wait would take issue slots
+// from the softmax warps sharing its SM sub-partition.
+template <int kSleepNs = 128>
+__device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity)) {
+        __nanosleep(kSleepNs);
+        if (clock64() - t0 > (1ll << 34)) __trap();
+    }
+}
+
 // ------------------------------------------------------------------ TMA --
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1, int c2) {
