@@ -23,6 +23,9 @@
 // atomic tickets on the same counters (gpu_sim.hpp:114-131).
 #pragma once
 
+#ifndef POD_SM_SOFTMAX_HIGH
+#define POD_SM_SOFTMAX_HIGH 0
+#endif
 #ifndef POD_SM_MMA_SLEEP
 #define POD_SM_MMA_SLEEP 0
 #endif
@@ -441,7 +444,17 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
                   const __grid_constant__ CUtensorMap tdv) {
     using namespace sm3;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // Logical warp roles (0-7 softmax, 8 producer, 9 MMA, 10.. decode).  With
+    // POD_SM_SOFTMAX_HIGH the decode group takes the lowest hardware warp ids and the
+    // softmax warps the highest (the SMSP arbiter favours higher warp ids); TMEM lane
+    // quadrants follow the hardware id, which keeps warp % 4 for every softmax warp.
+    const int hw_warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    static_assert(!POD_SM_SOFTMAX_HIGH || (kDecWarp0 == 10 && sm3::kThreads == 512), "role remap layout");
+    const int warp = !POD_SM_SOFTMAX_HIGH ? hw_warp
+                     : hw_warp >= 8       ? hw_warp - 8    // softmax: hardware warps 8-15 (quadrant = hw % 4)
+                     : hw_warp >= 6       ? hw_warp + 2    // producer, MMA: hardware warps 6, 7
+                                          : hw_warp + 10;  // decode group: hardware warps 0-5
+    const int tid = warp * 32 + lane;
     const uint32_t sbase = ptx::smem_u32(smem);
     volatile int32_t* misc = reinterpret_cast<volatile int32_t*>(smem + kOffMisc);  // [0] tmem, [2..3] pf, [4..5] dec
     if (tid == 0) {
