@@ -98,18 +98,24 @@ def test_policies_and_reference_tiles(policy):
         _check(wl, out)
 
 
-def test_peaky_queries():
+# the two POD kernels: two CTAs per SM (COMPLEMENT) and one warp-specialised CTA per SM
+KERNELS = [POD_POLICY_COMPLEMENT, POD_POLICY_WARPSPEC]
+
+
+@pytest.mark.parametrize("policy", KERNELS)
+def test_peaky_queries(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=64, offset=900, decode_ctx=[1000, 333])
-    wl, _, out = _run(batch, q_scale=8.0)
+    wl, _, out = _run(batch, q_scale=8.0, options=pkg.PlanOptions(policy=policy))
     _check(wl, out)
 
 
-def test_fp16_inputs():
+@pytest.mark.parametrize("policy", KERNELS)
+def test_fp16_inputs(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=64, offset=100, decode_ctx=[200, 45])
     batch.dtype = POD_DTYPE_FP16
-    wl, _, out = _run(batch, dtype=torch.float16)
+    wl, _, out = _run(batch, dtype=torch.float16, options=pkg.PlanOptions(policy=policy))
     # the oracle regenerates bf16-rounded values; compare against fp16-rounded ones instead
     s = batch.shape
     G = s.group_size()
@@ -195,11 +201,12 @@ def test_append_then_attend_matches_oracle():
     _check(wl, out)
 
 
-def test_causality_is_bitwise():
+@pytest.mark.parametrize("policy", KERNELS)
+def test_causality_is_bitwise(policy):
     _need_gpu()
     off, chunk, r = 300, 64, 20
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=chunk, offset=off, decode_ctx=[100])
-    wl, op, out1 = _run(batch)
+    wl, op, out1 = _run(batch, options=pkg.PlanOptions(policy=policy))
     before = out1.o_prefill[: r + 1].clone()
     ix = wl.page_indices.cpu().tolist()
     for t in range(off + r + 1, off + chunk):  # keys no row <= r can see
@@ -211,14 +218,16 @@ def test_causality_is_bitwise():
     assert not torch.equal(out2.o_prefill[r + 1:], out1.o_prefill[r + 1:])
 
 
-def test_split_invariance():
+@pytest.mark.parametrize("policy", KERNELS)
+def test_split_invariance(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=128, offset=1000, decode_ctx=[3000, 1500])
     wl = build_workload(batch, device="cuda")
     outs = []
     for ds in (1, 2, 3, 5):
         for cap in (1, 2, 4):
-            _, _, out = _run(batch, options=pkg.PlanOptions(decode_splits=ds, split_wave_cap=cap), wl=wl)
+            _, _, out = _run(batch, options=pkg.PlanOptions(policy=policy, decode_splits=ds, split_wave_cap=cap),
+                             wl=wl)
             outs.append(out)
             _check(wl, out, kv_heads=[0, 5])
     base = outs[0]
@@ -228,10 +237,11 @@ def test_split_invariance():
         assert d <= O_TOL and p <= O_TOL
 
 
-def test_deterministic_and_fused_equals_serial_bitwise():
+@pytest.mark.parametrize("policy", KERNELS)
+def test_deterministic_and_fused_equals_serial_bitwise(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=256, offset=700, decode_ctx=[900] * 6)
-    wl, op, a = _run(batch)
+    wl, op, a = _run(batch, options=pkg.PlanOptions(policy=policy))
     b = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
     c = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, mode="serial")
     torch.cuda.synchronize()
@@ -240,13 +250,14 @@ def test_deterministic_and_fused_equals_serial_bitwise():
         assert torch.equal(a.o_decode, x.o_decode) and torch.equal(a.lse_decode, x.lse_decode)
 
 
-def test_cuda_graph_replay():
+@pytest.mark.parametrize("policy", KERNELS)
+def test_cuda_graph_replay(policy):
     _need_gpu()
     from paper_2410_18038_b200.hybrid import PodAttention
 
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=96, offset=100, decode_ctx=[400, 80])
     wl = build_workload(batch, device="cuda")
-    op = PodAttention(batch)
+    op = PodAttention(batch, options=pkg.PlanOptions(policy=policy))
     out = op.alloc_outputs()
     ref = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
     s = torch.cuda.Stream()
