@@ -297,8 +297,11 @@ struct PrefillState {
 };
 
 // Debug trace (RunParams::trace): CTA 0, first prefill item, first 256 tiles.
+#ifndef POD_TRACE_STAMPS
+#define POD_TRACE_STAMPS 0  // debug builds: -DPOD_TRACE_STAMPS=1 enables the per-tile cycle stamps
+#endif
 __device__ __forceinline__ void trace_stamp(const RunParams& p, int items, int t, int k) {
-    if (p.trace && blockIdx.x == 0 && items == 0 && t < 768 && p.role_log) {
+    if (POD_TRACE_STAMPS && p.trace && blockIdx.x == 0 && items == 0 && t < 768 && p.role_log) {
         int32_t* tr = p.role_log + p.trace;
         tr[t * 8 + k] = static_cast<int32_t>(clock64());
     }

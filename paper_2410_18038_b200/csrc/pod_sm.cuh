@@ -26,6 +26,9 @@
 #ifndef POD_SM_SOFTMAX_HIGH
 #define POD_SM_SOFTMAX_HIGH 0
 #endif
+#ifndef POD_SM_MERGED_EMPTY
+#define POD_SM_MERGED_EMPTY 1
+#endif
 #ifndef POD_SM_MMA_SLEEP
 #define POD_SM_MMA_SLEEP 0
 #endif
@@ -71,7 +74,9 @@ constexpr uint32_t kOffDec = 2 * kNS * kStage;                 // decode rings (
 constexpr uint32_t kOffBars = kOffDec + kDW * kDS * kDecStageBytes;
 // prefill mbarriers: 0 qA, 1 qB, 2-5 k_full, 6-9 k_empty, 10-13 v_full, 14-17 v_empty,
 // 18-19 sA[2], 20-21 sB[2], 22-23 pA[2], 24-25 pB[2], 26-27 pvA[2], 28-29 pvB[2]
-// (k_empty / v_empty take two arrivals: one commit per block's issuing thread)
+// (single MMA issuer: bars 6-9 are per-stage kv_empty, committed once both K and V of a
+//  tile are consumed; bars 14-17 unused.  POD_SM_DUAL_MMA: k_empty / v_empty take two
+//  arrivals, one commit per block's issuing thread)
 // (pv per S buffer: a waiter is never more than one completion behind on a
 // barrier, so parity waits stay unambiguous even when the softmax skips them)
 constexpr int kNumBars = 30;
@@ -173,9 +178,10 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                 ptx::mbar_arrive_expect_tx_elect(bar(2 + st), kStage);
                 load_tile32(p, tmk, sK + st * kStage, bar(2 + st), kt0 + t * kTN, job.kv_head, ids);
             }
-            if (t > 0) {  // V of tile t-1
+            if (t > 0) {  // V of tile t-1 (single issuer: its stage was freed with K's)
                 const int gg = s0.g + t - 1, st = gg % kNS;
-                if (gg >= kNS) ptx::mbar_wait_relaxed<>(bar(14 + st), ((gg / kNS) - 1) & 1);
+                if ((kDualMma || !POD_SM_MERGED_EMPTY) && gg >= kNS)
+                    ptx::mbar_wait_relaxed<>(bar(14 + st), ((gg / kNS) - 1) & 1);
                 ptx::mbar_arrive_expect_tx_elect(bar(10 + st), kStage);
                 load_tile32(p, tmv, sV + st * kStage, bar(10 + st), kt0 + (t - 1) * kTN, job.kv_head, ids);
             }
@@ -199,7 +205,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                     issue_qk32<kFmt>(tmem + kSB + 32 * bB, tmem + kQB, sK + st * kStage);
                     ptx::umma_commit_elect(bar(20 + bB));
                 }
-                ptx::umma_commit_elect(bar(6 + st));
+                if (!POD_SM_MERGED_EMPTY) ptx::umma_commit_elect(bar(6 + st));
             }
             for (int t = 0; t < nt; ++t) {
                 const int gg = s0.g + t, st = gg % kNS;
@@ -209,12 +215,15 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                 sm_wait<POD_SM_MMA_SLEEP>(bar(22 + bA), (nA >> 1) & 1);
                 trace_stamp(p, first, t, 4);
                 sm_wait<POD_SM_MMA_SLEEP>(bar(10 + st), (gg / kNS) & 1);
+                trace_stamp(p, first, t < 128 ? 384 + t : 9999, 4);
                 ptx::tc_fence_after();
                 issue_pv32<kFmt>(tmem + kOA, tmem + kSA + 32 * bA, sV + st * kStage, t > 0, p.p_split != 0);
+                trace_stamp(p, first, t < 128 ? 384 + t : 9999, 5);
                 ptx::umma_commit_elect(bar(26 + bA));
                 trace_stamp(p, first, t, 5);
                 if (more) {
                     sm_wait<POD_SM_MMA_SLEEP>(bar(2 + st2), (g2 / kNS) & 1);
+                    trace_stamp(p, first, t < 128 ? 384 + t : 9999, 6);
                     ptx::tc_fence_after();
                     issue_qk32<kFmt>(tmem + kSA + 32 * bA, tmem + kQA, sK + st2 * kStage);
                     ptx::umma_commit_elect(bar(18 + bA));
@@ -223,6 +232,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                 if (hasB) {
                     const int nB = s0.n[1] + t, bB = nB & 1;
                     sm_wait<POD_SM_MMA_SLEEP>(bar(24 + bB), (nB >> 1) & 1);
+                    trace_stamp(p, first, t < 128 ? 384 + t : 9999, 7);
                     ptx::tc_fence_after();
                     issue_pv32<kFmt>(tmem + kOB, tmem + kSB + 32 * bB, sV + st * kStage, t > 0, p.p_split != 0);
                     ptx::umma_commit_elect(bar(28 + bB));
@@ -231,8 +241,14 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                         ptx::umma_commit_elect(bar(20 + bB));
                     }
                 }
-                ptx::umma_commit_elect(bar(14 + st));
-                if (more) ptx::umma_commit_elect(bar(6 + st2));
+                if (POD_SM_MERGED_EMPTY) {
+                    // K and V of tile t are both consumed (QK(t) ran before PV(t)): one
+                    // commit frees the stage for the producer
+                    ptx::umma_commit_elect(bar(6 + st));
+                } else {
+                    ptx::umma_commit_elect(bar(14 + st));
+                    if (more) ptx::umma_commit_elect(bar(6 + st2));
+                }
             }
         }
     } else if (kDualMma && (warp == kMmaWarp || warp == kMmaWarpB)) {
@@ -266,19 +282,19 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                 const bool more = t + 2 < nt;
                 const int n = s0.n[X] + t, bx = n & 1;
                 ptx::mbar_wait(bar(22 + 2 * X + bx), (n >> 1) & 1);
-                trace_stamp(p, first, 256 * X + t, 4);
+                trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 4);
                 ptx::mbar_wait(bar(10 + st), (gg / kNS) & 1);
                 ptx::tc_fence_after();
                 issue_pv32<kFmt>(tO, tS + 32 * bx, sV + st * kStage, t > 0, p.p_split != 0);
                 ptx::umma_commit_elect(bar(26 + 2 * X + bx));
-                trace_stamp(p, first, 256 * X + t, 5);
+                trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 5);
                 if (more) {
                     ptx::mbar_wait(bar(2 + st2), (g2 / kNS) & 1);
                     ptx::tc_fence_after();
                     issue_qk32<kFmt>(tS + 32 * bx, tQ, sK + st2 * kStage);
                     ptx::umma_commit_elect(bar(18 + 2 * X + bx));
                 }
-                trace_stamp(p, first, 256 * X + t, 6);
+                trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 6);
                 release(bar(14 + st));
                 if (more) release(bar(6 + st2));
             }
@@ -341,9 +357,9 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         for (int t = 0; t < nt; ++t) {
             const int n = s0.n[X] + t, b = n & 1;
             const uint32_t s_addr = lane_base + (X ? kSB : kSA) + 32 * b;
-            if (lane == 0 && q == 0) trace_stamp(p, first, 256 * X + t, 0);
+            if (lane == 0 && q == 0) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 0);
             sm_wait<POD_SM_SOFTMAX_SLEEP>(bar(18 + 2 * X + b), (n >> 1) & 1);
-            if (lane == 0 && q == 0) trace_stamp(p, first, 256 * X + t, 1);
+            if (lane == 0 && q == 0) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 1);
             ptx::tc_fence_after();
             float s[kTN];
             ptx::tmem_ld32(s_addr, s);
@@ -392,8 +408,8 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0 && q == 0) trace_stamp(p, first, 256 * X + t, 2);
-            if (lane == 0 && q == 3) trace_stamp(p, first, 256 * X + t, 3);
+            if (lane == 0 && q == 0) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 2);
+            if (lane == 0 && q == 3) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 3);
             if (lane == 0) ptx::mbar_arrive(bar(22 + 2 * X + b));
         }
         // ------------------------------------------------- epilogue --

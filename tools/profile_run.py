@@ -58,10 +58,10 @@ def main():
         tr = allrec[nrec:].tolist()
         print("trace words nonzero:", int((allrec[nrec:] != 0).sum()), "policy", a.policy)
         if any(any(x) for x in tr) and op.info.policy == 7:
-            print("trace (warpspec): t | A: swait, sok, w0 done, w3 done, mma pA seen, PV_A issued, QK_A issued | B: same")
+            print("trace (warpspec): t | A: swait, sok, w0 done, w3 done, mma pA seen, PV_A committed, QK_A committed | B: swait, sok, w0 done, w3 done | mma: vfull ok, PV_A issued, kfull ok, pB seen")
             base = tr[0][0]
             for t in list(range(0, 10)) + list(range(100, 104)):
-                row = tr[t][:7] + tr[256 + t][:7]
+                row = tr[t][:7] + tr[384 + t][:4] + tr[384 + t][4:8]
                 print(t, [((x - base) & 0xffffffff) if x else None for x in row])
         elif any(any(x) for x in tr):
             import os
