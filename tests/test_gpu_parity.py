@@ -314,8 +314,13 @@ def test_role_log_scheduler_contract(policy):
     for sm in np.unique(sms):
         mine = rec[sms == sm]
         if policy != POD_POLICY_COMPLEMENT:
-            # per-SM tickets are the SM counter's values 0..k-1, each used once
-            assert sorted(mine[:, 1].tolist()) == list(range(len(mine)))
+            # per-SM tickets are distinct values of the SM counter; a ticket whose claim
+            # found both pools drained leaves no record, and two CTAs share an SM, so
+            # a CTA that drew ticket k can lose the last item to the one that drew k+1:
+            # at most one gap per resident CTA, and only at the tail
+            t = sorted(mine[:, 1].tolist())
+            assert len(set(t)) == len(t)
+            assert t[-1] < len(t) + 2
             pr, dr = op.info.prefill_ratio, op.info.decode_ratio
             # in ticket order the ops follow sm_aware_assign's pattern until the first
             # switch; a switch means the wanted pool ran dry, so every later claim on
