@@ -341,6 +341,26 @@ def ref_decompose_hybrid(shape, prefill, decode_ctx, gpu, cfg=None):
         [dt[i] for i in range(nd_.value)] if not st else []
 
 
+DES_FIELDS = ("serial", "fused_best", "oracle_runtime", "prefill_alone", "decode_alone", "ctas_per_sm",
+              "streams", "fused_selected")
+
+
+def ref_des_predict(shape, prefill, decode_ctx, gpu):
+    """The reference's discrete-event model of one hybrid batch (gpu_sim.hpp:781-816):
+    dict of DES_FIELDS (times in the GpuSpec's time unit)."""
+    hq, hkv, d, scale = shape
+    nd = len(decode_ctx)
+    ctx = (C.c_int64 * max(1, nd))(*decode_ctx)
+    has = 1 if prefill is not None else 0
+    ch, pr, off = prefill if prefill is not None else (0, 0, 0)
+    out = (C.c_double * 8)()
+    st = ref().ref_des_predict(hq, hkv, d, C.c_double(scale), has, C.c_int64(ch), C.c_int64(pr),
+                               C.c_int64(off), C.c_int64(nd), ctx, C.byref(gpu), out)
+    if st:
+        raise OracleError(f"ref_des_predict: status {st}")
+    return dict(zip(DES_FIELDS, list(out)))
+
+
 def ref_limit_prefill_splits(natural, gpu, cfg):
     out = C.c_int64(0)
     st = ref().ref_limit_prefill_splits(C.c_int64(natural), C.byref(gpu), C.byref(cfg), C.byref(out))

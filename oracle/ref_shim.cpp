@@ -448,4 +448,38 @@ int ref_run_serving_linear(int64_t n, const double* arrival, const int64_t* ptok
     });
 }
 
+// ------------------------------------------------- DES predictor (N3) --
+
+// The reference's discrete-event model of one hybrid batch on `gpu`
+// (gpu_sim.hpp:781-816, work_decomp.hpp:139-145,249-261), for cross-validation
+// against measured B200 times.  out[8] =
+//   {serial makespan (select_tile_config decomposition, Strategy::Serial),
+//    best fused makespan (best_fused_makespan: {2,4} CTAs/SM x {5050, prop}),
+//    oracle_runtime (combined roofline of the same tasks),
+//    prefill-alone makespan, decode-alone makespan (Serial, same config),
+//    selected ctas_per_sm, streams makespan, fused makespan at the selected config (5050)}
+int ref_des_predict(int hq, int hkv, int d, double scale, int has_prefill, int64_t chunk,
+                    int64_t prompt, int64_t offset, int64_t n_dec, const int64_t* dec_ctx,
+                    const ref_gpu_spec* gpu, double* out) {
+    return guarded([&] {
+        auto b = make_batch(hq, hkv, d, scale, has_prefill, chunk, prompt, offset, n_dec, dec_ctx);
+        const GpuSpec g = to_gpu(gpu);
+        SimOptions opt;
+        opt.record_trace = false;
+        const TileConfig cfg = select_tile_config(b, g);
+        const auto launches = make_attention_launches(decompose_hybrid(b, g, cfg));
+        out[0] = simulate(g, launches, ExecutionStrategy::serial(), 0, opt).makespan;
+        out[1] = best_fused_makespan(g, b, 0);
+        out[2] = oracle_runtime(g, launches);
+        out[3] = out[4] = 0;
+        for (size_t i = 0; i < launches.size(); ++i) {
+            const double t = simulate(g, {launches[i]}, ExecutionStrategy::serial(), 0, opt).makespan;
+            out[launches[i].stream_id == 0 ? 3 : 4] = t;
+        }
+        out[5] = cfg.ctas_per_sm;
+        out[6] = simulate(g, launches, ExecutionStrategy::streams(), 0, opt).makespan;
+        out[7] = simulate(g, launches, ExecutionStrategy::sm_aware(SmPolicy::FiftyFifty), 0, opt).makespan;
+    });
+}
+
 }  // extern "C"
