@@ -228,7 +228,8 @@ def run_pod(args, rank, world, local_rank):
     batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
     wl = build_workload(batch, device=dev, seed_q=42 + 1000 * rank, seed_kv=43 + 1000 * rank)
     opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode, precision=args.precision,
-                           decode_splits=args.decode_splits, split_wave_cap=args.split_wave_cap)
+                           decode_splits=args.decode_splits, split_wave_cap=args.split_wave_cap,
+                           out_dtype={"f32": 0, "bf16": 1}[args.out_dtype])
     op = PodAttention(batch, options=opts, device=local_rank)
     out = op.alloc_outputs()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -315,7 +316,7 @@ def run_pod(args, rank, world, local_rank):
 
     host_out = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in _dev_out(o)] for o in outs]
     h2d = (qp_h.numel() * 2 if qp_h is not None else 0) + (qd_h.numel() * 2 if qd_h is not None else 0)
-    d2h = sum(t.numel() * 4 for t in _dev_out(out))
+    d2h = sum(t.numel() * t.element_size() for t in _dev_out(out))
     s_c = torch.cuda.current_stream(dev)
     s_h, s_d = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ev_h = [torch.cuda.Event() for _ in range(2)]
@@ -387,6 +388,8 @@ def main():
     ap.add_argument("--policy", type=int, default=8, help="POD_POLICY_*: 8 = AUTO (default), 7 = WARPSPEC, 3 = COMPLEMENT")
     ap.add_argument("--tile-mode", type=int, default=1)
     ap.add_argument("--precision", type=int, default=0, help="0: prefill P as bf16 hi+lo (default), 1: single bf16")
+    ap.add_argument("--out-dtype", default="f32", choices=["f32", "bf16"],
+                    help="element type of the attention outputs (LSE stays fp32); f32 = the reference's")
     ap.add_argument("--decode-splits", type=int, default=0)
     ap.add_argument("--split-wave-cap", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="wall seconds of the CPU reference sample")
@@ -490,7 +493,7 @@ def main():
         "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
                  "prefill_splits": info.prefill_splits, "decode_splits": info.decode_splits,
                  "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
-                 "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_p": {0: "bf16 hi+lo", 1: "bf16"}[args.precision]},
+                 "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_p": {0: "bf16 hi+lo", 1: "bf16"}[args.precision], "out_dtype": args.out_dtype},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": {7: "pod_sm_kernel (+merge)"}.get(r["info"].policy, "pod_fused_kernel (+merge)"),

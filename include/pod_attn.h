@@ -151,7 +151,14 @@ typedef struct pod_options {
     int32_t decode_splits;   /* 0 = auto (fill the machine), else splits per (request, kv head) */
     const pod_tile_config* tile_override; /* non-NULL: use this TileConfig verbatim */
     int32_t precision;       /* POD_PRECISION_* for the prefill P operand            */
+    int32_t out_dtype;       /* POD_OUT_*: element type of o_prefill / o_decode (LSE stays fp32) */
 } pod_options;
+
+enum {
+    POD_OUT_F32 = 0,  /* fp32 outputs (default; the reference's AttentionPartial.o, attention.hpp:86-93) */
+    POD_OUT_BF16 = 1, /* bf16 outputs, RNE of the fp32 result: half the HBM / PCIe / all-gather bytes */
+    POD_OUT_F16 = 2   /* fp16 outputs, RNE of the fp32 result */
+};
 
 enum {
     POD_PRECISION_SPLIT = 0, /* P = bf16 hi + bf16 lo (two PV MMAs): ~16-bit P, default */
@@ -213,28 +220,28 @@ pod_status pod_attn_workspace_init(const pod_plan* plan, void* workspace, void* 
  *   q_decode   [num_decodes][Hq][d]                   (attention.hpp:71-84)
  *   k_pool, v_pool  HND [num_pages][Hkv][page_size][d] or NHD [num_pages][page_size][Hkv][d]
  *   page_indptr [num_requests + 1], page_indices [...] (int32, device)
- *   o_prefill  [chunk][Hq][d] fp32,  lse_prefill [chunk][Hq] fp32 (natural log)
- *   o_decode   [num_decodes][Hq][d] fp32, lse_decode [num_decodes][Hq] fp32
+ *   o_prefill  [chunk][Hq][d] fp32 (or bf16/fp16 per options.out_dtype), lse_prefill [chunk][Hq] fp32 (natural log)
+ *   o_decode   [num_decodes][Hq][d] (same element type), lse_decode [num_decodes][Hq] fp32
  * Unused outputs may be NULL when the batch has no such part. */
 pod_status pod_attn_run(const pod_plan* plan, const void* q_prefill, const void* q_decode,
                         const void* k_pool, const void* v_pool, int64_t num_pages,
-                        const int32_t* page_indptr, const int32_t* page_indices, float* o_prefill,
-                        float* lse_prefill, float* o_decode, float* lse_decode, void* workspace,
+                        const int32_t* page_indptr, const int32_t* page_indices, void* o_prefill,
+                        float* lse_prefill, void* o_decode, float* lse_decode, void* workspace,
                         void* stream);
 /* Serial comparator (gpu_sim.hpp:496-506): the same prefill and decode device
  * code as two back-to-back launches on one stream, then the merge. */
 pod_status pod_attn_run_serial(const pod_plan* plan, const void* q_prefill, const void* q_decode,
                                const void* k_pool, const void* v_pool, int64_t num_pages,
                                const int32_t* page_indptr, const int32_t* page_indices,
-                               float* o_prefill, float* lse_prefill, float* o_decode,
+                               void* o_prefill, float* lse_prefill, void* o_decode,
                                float* lse_decode, void* workspace, void* stream);
 /* Standalone halves (prefill-alone / decode-alone timings and unit tests).
  * which: 0 = prefill only, 1 = decode only.  Includes that part's merge. */
 pod_status pod_attn_run_part(const pod_plan* plan, int which, const void* q_prefill,
                              const void* q_decode, const void* k_pool, const void* v_pool,
                              int64_t num_pages, const int32_t* page_indptr,
-                             const int32_t* page_indices, float* o_prefill, float* lse_prefill,
-                             float* o_decode, float* lse_decode, void* workspace, void* stream);
+                             const int32_t* page_indices, void* o_prefill, float* lse_prefill,
+                             void* o_decode, float* lse_decode, void* workspace, void* stream);
 
 /* Optional device-side role log of the fused kernel (the GPU analogue of
  * SmAssignment, gpu_sim.hpp:141-148): when set (non-NULL, device memory of

@@ -24,6 +24,7 @@ POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_
     POD_POLICY_BALANCED, POD_POLICY_PARTITION, POD_POLICY_WARPSPEC, POD_POLICY_AUTO = 0, 1, 2, 3, 4, 5, 6, 7, 8
 POD_TILE_REFERENCE, POD_TILE_B200 = 0, 1
 POD_PRECISION_SPLIT, POD_PRECISION_FAST = 0, 1
+POD_OUT_F32, POD_OUT_BF16, POD_OUT_F16 = 0, 1, 2
 
 
 class pod_shape(C.Structure):
@@ -68,7 +69,7 @@ class pod_options(C.Structure):
     _fields_ = [("policy", C.c_int32), ("tile_mode", C.c_int32), ("ctas_per_sm", C.c_int32),
                 ("virtual_decode", C.c_int32), ("split_wave_cap", C.c_int32),
                 ("decode_splits", C.c_int32), ("tile_override", C.POINTER(pod_tile_config)),
-                ("precision", C.c_int32)]
+                ("precision", C.c_int32), ("out_dtype", C.c_int32)]
 
 
 class pod_plan_info(C.Structure):

@@ -87,9 +87,10 @@ struct RunParams {
     const void* v_pool;
     const int32_t* page_indptr;
     const int32_t* page_indices;
-    float* o_prefill;
+    void* o_prefill;
     float* lse_prefill;
-    float* o_decode;
+    void* o_decode;
+    int out_fmt;  // POD_OUT_*: element type of o_prefill / o_decode
     float* lse_decode;
     float* ppart_o;
     float* ppart_lse;
@@ -300,6 +301,39 @@ struct PrefillState {
 #ifndef POD_TRACE_STAMPS
 #define POD_TRACE_STAMPS 0  // debug builds: -DPOD_TRACE_STAMPS=1 enables the per-tile cycle stamps
 #endif
+// Final-output rows: fp32, or 16-bit (POD_OUT_BF16 / POD_OUT_F16) = RNE of the same
+// fp32 value, so a 16-bit run equals the rounded fp32 run bit for bit.  Split
+// partials always stay fp32 (fmt 0).
+struct ORow {
+    char* ptr;
+    int fmt;
+};
+__device__ __forceinline__ ORow out_row(void* base, size_t elem, int fmt) {
+    return {static_cast<char*>(base) + elem * (fmt ? 2u : 4u), fmt};
+}
+__device__ __forceinline__ uint32_t pack16(int fmt, float a, float b) {
+    if (fmt == 1) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<const uint32_t*>(&h);
+    }
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ void store4(const ORow& o, int c, float4 v) {
+    if (o.fmt == 0)
+        *reinterpret_cast<float4*>(o.ptr + 4 * c) = v;
+    else
+        *reinterpret_cast<uint2*>(o.ptr + 2 * c) = make_uint2(pack16(o.fmt, v.x, v.y), pack16(o.fmt, v.z, v.w));
+}
+__device__ __forceinline__ void store1(const ORow& o, int c, float v) {
+    if (o.fmt == 0)
+        reinterpret_cast<float*>(o.ptr)[c] = v;
+    else if (o.fmt == 1)
+        reinterpret_cast<__nv_bfloat16*>(o.ptr)[c] = __float2bfloat16_rn(v);
+    else
+        reinterpret_cast<__half*>(o.ptr)[c] = __float2half_rn(v);
+}
+
 __device__ __forceinline__ void trace_stamp(const RunParams& p, int items, int t, int k) {
     if (POD_TRACE_STAMPS && p.trace && blockIdx.x == 0 && items == 0 && t < 768 && p.role_log) {
         int32_t* tr = p.role_log + p.trace;
@@ -448,20 +482,19 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
             const bool row_ok = (m / G) < br.nrows;
             const int vis = p.offset + my_r;  // last visible key (inclusive)
             const int qhead = job.kv_head * G + my_g;
-            float* orow;
+            ORow orow;
             float* lrow;
             if (job.n_splits == 1) {
-                orow = p.o_prefill + (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim;
+                orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim, p.out_fmt);
                 lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
             } else {
                 const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
-                orow = p.ppart_o + row * kHeadDim;
+                orow = out_row(p.ppart_o, row * kHeadDim, 0);
                 lrow = p.ppart_lse + row;
             }
             if (br.nt == 0) {
                 if (row_ok) {
-                    for (int c = 0; c < kHeadDim; c += 4)
-                        *reinterpret_cast<float4*>(orow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int c = 0; c < kHeadDim; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
                     *lrow = -INFINITY;
                 }
                 continue;
@@ -552,8 +585,8 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                 if (row_ok) {
 #pragma unroll
                     for (int c = 0; c < 32; c += 4)
-                        *reinterpret_cast<float4*>(orow + ch * 32 + c) =
-                            make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv);
+                        store4(orow, ch * 32 + c,
+                               make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
                 }
             }
             if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
@@ -727,7 +760,7 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
             const int nblk = hasB ? 2 : 1;
             int my_r[2], vis[2];
             bool row_ok[2];
-            float* orow[2];
+            ORow orow[2];
             float* lrow[2];
             const int qhead = job.kv_head * G + m % G;
 #pragma unroll
@@ -736,11 +769,11 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
                 row_ok[bi] = bi < nblk && (m / G) < br[bi].nrows;
                 vis[bi] = p.offset + my_r[bi];
                 if (job.n_splits == 1) {
-                    orow[bi] = p.o_prefill + (static_cast<size_t>(my_r[bi]) * p.hq + qhead) * kHeadDim;
+                    orow[bi] = out_row(p.o_prefill, (static_cast<size_t>(my_r[bi]) * p.hq + qhead) * kHeadDim, p.out_fmt);
                     lrow[bi] = p.lse_prefill + static_cast<size_t>(my_r[bi]) * p.hq + qhead;
                 } else {
                     const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r[bi]) * p.hq + qhead;
-                    orow[bi] = p.ppart_o + row * kHeadDim;
+                    orow[bi] = out_row(p.ppart_o, row * kHeadDim, 0);
                     lrow[bi] = p.ppart_lse + row;
                 }
             }
@@ -748,8 +781,7 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
 #pragma unroll
                 for (int bi = 0; bi < 2; ++bi)
                     if (row_ok[bi]) {
-                        for (int c = 0; c < kHeadDim; c += 4)
-                            *reinterpret_cast<float4*>(orow[bi] + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int c = 0; c < kHeadDim; c += 4) store4(orow[bi], c, make_float4(0.f, 0.f, 0.f, 0.f));
                         *lrow[bi] = -INFINITY;
                     }
                 continue;
@@ -868,8 +900,8 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
                     if (row_ok[bi]) {
 #pragma unroll
                         for (int c = 0; c < 32; c += 4)
-                            *reinterpret_cast<float4*>(orow[bi] + ch * 32 + c) =
-                                make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv);
+                            store4(orow[bi], ch * 32 + c,
+                                   make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
                     }
                 }
                 if (row_ok[bi])
@@ -1207,7 +1239,8 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
         const float out = acc / L;
         const float lse = (M + ptx::lg2(L)) * kLn2;
         if (job.n_splits == 1) {
-            p.o_decode[(static_cast<size_t>(job.request) * p.hq + qhead) * kHeadDim + d] = out;
+            store1(out_row(p.o_decode, (static_cast<size_t>(job.request) * p.hq + qhead) * kHeadDim, p.out_fmt), d,
+                   out);
             if (d == 0) p.lse_decode[static_cast<size_t>(job.request) * p.hq + qhead] = lse;
         } else {
             const size_t row = (static_cast<size_t>(job.request) * p.decode_splits + job.split) * p.hq + qhead;
@@ -1236,7 +1269,7 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
     const float* po;
     const float* pl;
     size_t stride_o, stride_l;
-    float* out_o;
+    ORow out_o;
     float* out_l;
     if (mode == 0) {
         n = tile_splits[r / tile_q];
@@ -1246,7 +1279,7 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
         pl = p.ppart_lse + row;
         stride_l = static_cast<size_t>(p.chunk) * p.hq;
         stride_o = stride_l * kHeadDim;
-        out_o = p.o_prefill + row * kHeadDim;
+        out_o = out_row(p.o_prefill, row * kHeadDim, p.out_fmt);
         out_l = p.lse_prefill + row;
     } else {
         n = p.decode_splits;  // uniform per plan (clamped to the shortest context)
@@ -1256,7 +1289,7 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
         pl = p.dpart_lse + row;
         stride_l = p.hq;
         stride_o = stride_l * kHeadDim;
-        out_o = p.o_decode + (static_cast<size_t>(r) * p.hq + qh) * kHeadDim;
+        out_o = out_row(p.o_decode, (static_cast<size_t>(r) * p.hq + qh) * kHeadDim, p.out_fmt);
         out_l = p.lse_decode + static_cast<size_t>(r) * p.hq + qh;
     }
     float M = -INFINITY;
@@ -1273,7 +1306,7 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
         acc.z += w * v.z;
         acc.w += w * v.w;
     }
-    *reinterpret_cast<float4*>(out_o + lane * 4) = acc;
+    store4(out_o, lane * 4, acc);
     if (lane == 0) *out_l = lse_tot;
 }
 
@@ -1631,8 +1664,8 @@ pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_
 }
 
 RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q_decode, const void* k_pool, const void* v_pool,
-                      int64_t num_pages, const int32_t* indptr, const int32_t* indices, float* o_prefill,
-                      float* lse_prefill, float* o_decode, float* lse_decode, void* workspace) {
+                      int64_t num_pages, const int32_t* indptr, const int32_t* indices, void* o_prefill,
+                      float* lse_prefill, void* o_decode, float* lse_decode, void* workspace) {
     RunParams p{};
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     p.q_prefill = q_prefill;
@@ -1668,6 +1701,7 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.w_prefill = static_cast<float>(plan->w_prefill);
     p.w_decode = static_cast<float>(plan->w_decode);
     p.p_split = plan->opts.precision == POD_PRECISION_SPLIT ? 1 : 0;
+    p.out_fmt = plan->opts.out_dtype;
     {
         static const char* grid_env = std::getenv("POD_GRID_PER_SM");  // experiment knob
         p.grid_per_sm = grid_env ? std::max(1, std::min(2, std::atoi(grid_env))) : 2;
@@ -1783,7 +1817,7 @@ pod_status dispatch_g(const pod_plan* plan, int mode, const RunParams& p, const 
 
 pod_status run_mode(const pod_plan* plan, int mode, const void* q_prefill, const void* q_decode,
                     const void* k_pool, const void* v_pool, int64_t num_pages, const int32_t* indptr,
-                    const int32_t* indices, float* o_prefill, float* lse_prefill, float* o_decode,
+                    const int32_t* indices, void* o_prefill, float* lse_prefill, void* o_decode,
                     float* lse_decode, void* workspace, void* stream) {
     if (!plan || !k_pool || !v_pool || !indptr || !indices || !workspace) return POD_ERR_INVALID_ARGUMENT;
     pod_status st = check_supported(plan);
@@ -1866,7 +1900,7 @@ pod_status pod_attn_workspace_init(const pod_plan* plan, void* workspace, void* 
 
 pod_status pod_attn_run(const pod_plan* plan, const void* q_prefill, const void* q_decode, const void* k_pool,
                         const void* v_pool, int64_t num_pages, const int32_t* page_indptr,
-                        const int32_t* page_indices, float* o_prefill, float* lse_prefill, float* o_decode,
+                        const int32_t* page_indices, void* o_prefill, float* lse_prefill, void* o_decode,
                         float* lse_decode, void* workspace, void* stream) {
     return run_mode(plan, 0, q_prefill, q_decode, k_pool, v_pool, num_pages, page_indptr, page_indices, o_prefill,
                     lse_prefill, o_decode, lse_decode, workspace, stream);
@@ -1874,8 +1908,8 @@ pod_status pod_attn_run(const pod_plan* plan, const void* q_prefill, const void*
 
 pod_status pod_attn_run_serial(const pod_plan* plan, const void* q_prefill, const void* q_decode,
                                const void* k_pool, const void* v_pool, int64_t num_pages,
-                               const int32_t* page_indptr, const int32_t* page_indices, float* o_prefill,
-                               float* lse_prefill, float* o_decode, float* lse_decode, void* workspace,
+                               const int32_t* page_indptr, const int32_t* page_indices, void* o_prefill,
+                               float* lse_prefill, void* o_decode, float* lse_decode, void* workspace,
                                void* stream) {
     return run_mode(plan, 1, q_prefill, q_decode, k_pool, v_pool, num_pages, page_indptr, page_indices, o_prefill,
                     lse_prefill, o_decode, lse_decode, workspace, stream);
@@ -1883,8 +1917,8 @@ pod_status pod_attn_run_serial(const pod_plan* plan, const void* q_prefill, cons
 
 pod_status pod_attn_run_part(const pod_plan* plan, int which, const void* q_prefill, const void* q_decode,
                              const void* k_pool, const void* v_pool, int64_t num_pages,
-                             const int32_t* page_indptr, const int32_t* page_indices, float* o_prefill,
-                             float* lse_prefill, float* o_decode, float* lse_decode, void* workspace,
+                             const int32_t* page_indptr, const int32_t* page_indices, void* o_prefill,
+                             float* lse_prefill, void* o_decode, float* lse_decode, void* workspace,
                              void* stream) {
     if (which != 0 && which != 1) return POD_ERR_INVALID_ARGUMENT;
     return run_mode(plan, which == 0 ? 2 : 3, q_prefill, q_decode, k_pool, v_pool, num_pages, page_indptr,

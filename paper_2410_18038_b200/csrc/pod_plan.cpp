@@ -556,6 +556,7 @@ void pod_options_default(pod_options* out) {
     out->decode_splits = 0;
     out->tile_override = nullptr;
     out->precision = POD_PRECISION_SPLIT;
+    out->out_dtype = POD_OUT_F32;
 }
 
 pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const pod_device* dev,
@@ -578,6 +579,8 @@ pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const p
             p->opts = *opts;
         else
             pod_options_default(&p->opts);
+        if (p->opts.out_dtype < POD_OUT_F32 || p->opts.out_dtype > POD_OUT_F16)
+            fail(POD_ERR_INVALID_ARGUMENT, "pod_options: out_dtype must be a POD_OUT_* value");
         build(*p);
         p->opts.tile_override = nullptr;  // do not keep caller pointers
         *out = p;

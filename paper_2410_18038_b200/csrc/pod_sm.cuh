@@ -312,20 +312,19 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         const int qhead = job.kv_head * G + m % G;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
         const uint32_t o_addr = lane_base + (X ? kOB : kOA);
-        float* orow;
+        ORow orow;
         float* lrow;
         if (job.n_splits == 1) {
-            orow = p.o_prefill + (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim;
+            orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim, p.out_fmt);
             lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
         } else {
             const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
-            orow = p.ppart_o + row * kHeadDim;
+            orow = out_row(p.ppart_o, row * kHeadDim, 0);
             lrow = p.ppart_lse + row;
         }
         if (nt == 0) {
             if (row_ok) {
-                for (int c = 0; c < kHeadDim; c += 4)
-                    *reinterpret_cast<float4*>(orow + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int c = 0; c < kHeadDim; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
                 *lrow = -INFINITY;
             }
             return;
@@ -427,8 +426,8 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             if (row_ok) {
 #pragma unroll
                 for (int c = 0; c < 32; c += 4)
-                    *reinterpret_cast<float4*>(orow + ch * 32 + c) =
-                        make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv);
+                    store4(orow, ch * 32 + c,
+                           make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
             }
         }
         if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;

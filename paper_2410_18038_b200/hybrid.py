@@ -54,17 +54,24 @@ class PodAttention:
         _check(lib().pod_attn_set_role_log(self.plan.handle, _ptr(self.role_log)), "set_role_log")
         return self.role_log
 
+    @property
+    def out_dtype(self) -> torch.dtype:
+        """Element type of o_prefill / o_decode (PlanOptions.out_dtype); LSE is always fp32."""
+        return {_abi.POD_OUT_F32: torch.float32, _abi.POD_OUT_BF16: torch.bfloat16,
+                _abi.POD_OUT_F16: torch.float16}[self.plan.options.out_dtype]
+
     def alloc_outputs(self) -> HybridOutputs:
         s = self.batch.shape
         dev = self.device
+        odt = self.out_dtype
         op = lp = od = ld = None
         if self.batch.prefill is not None:
             c = self.batch.prefill.chunk_size
-            op = torch.empty(c, s.num_q_heads, s.head_dim, dtype=torch.float32, device=dev)
+            op = torch.empty(c, s.num_q_heads, s.head_dim, dtype=odt, device=dev)
             lp = torch.empty(c, s.num_q_heads, dtype=torch.float32, device=dev)
         if self.batch.decodes:
             b = len(self.batch.decodes)
-            od = torch.empty(b, s.num_q_heads, s.head_dim, dtype=torch.float32, device=dev)
+            od = torch.empty(b, s.num_q_heads, s.head_dim, dtype=odt, device=dev)
             ld = torch.empty(b, s.num_q_heads, dtype=torch.float32, device=dev)
         return HybridOutputs(op, lp, od, ld)
 

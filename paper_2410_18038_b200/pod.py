@@ -224,6 +224,7 @@ class PlanOptions:
     decode_splits: int = 0
     tile_override: Optional[TileConfig] = None
     precision: int = _abi.POD_PRECISION_SPLIT
+    out_dtype: int = _abi.POD_OUT_F32
 
 
 def _task(t) -> CtaTask:
@@ -246,6 +247,7 @@ class Plan:
         o.virtual_decode, o.split_wave_cap, o.decode_splits = (options.virtual_decode, options.split_wave_cap,
                                                               options.decode_splits)
         o.precision = options.precision
+        o.out_dtype = options.out_dtype
         tc = None
         if options.tile_override is not None:
             tc = options.tile_override._c()

@@ -70,6 +70,9 @@ def test_error_codes_cross_the_boundary_as_statuses():
         Plan(HybridBatchSpec(shape=ModelShape(32, 8, 128, 1.0)), GpuSpec.b200())
     with pytest.raises(pkg.InvalidArgument):
         Plan(HybridBatchSpec(decodes=[DecodeSpec(5)], shape=ModelShape(32, 8, 128, 1.0)), GpuSpec(num_sms=0))
+    with pytest.raises(pkg.InvalidArgument):  # out_dtype outside POD_OUT_*
+        Plan(HybridBatchSpec(decodes=[DecodeSpec(5)], shape=ModelShape(32, 8, 128, 1.0)), GpuSpec.b200(),
+             PlanOptions(out_dtype=3))
     # run entry points validate arguments before touching CUDA
     st = _abi.lib().pod_attn_run(None, None, None, None, None, 0, None, None, None, None, None, None, None, None)
     assert st == 1

@@ -238,6 +238,26 @@ def test_split_invariance(policy):
 
 
 @pytest.mark.parametrize("policy", KERNELS)
+@pytest.mark.parametrize("out_dtype", [pkg._abi.POD_OUT_BF16, pkg._abi.POD_OUT_F16])
+def test_16bit_outputs_are_rounded_fp32_outputs(policy, out_dtype):
+    """16-bit outputs (half the output bytes) are the RNE rounding of
+    the fp32 result of the same plan, bit for bit, through every store path: the
+    prefill epilogue, the unsplit decode reduction and both split merges."""
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=200, offset=900, decode_ctx=[1700, 1100, 600])
+    wl = build_workload(batch, device="cuda")
+    want = {pkg._abi.POD_OUT_BF16: torch.bfloat16, pkg._abi.POD_OUT_F16: torch.float16}[out_dtype]
+    for ds, cap in ((1, 1), (3, 4)):
+        kw = dict(policy=policy, decode_splits=ds, split_wave_cap=cap)
+        _, _, ref = _run(batch, options=pkg.PlanOptions(**kw), wl=wl)
+        _, op, out = _run(batch, options=pkg.PlanOptions(out_dtype=out_dtype, **kw), wl=wl)
+        assert out.o_prefill.dtype == want and out.o_decode.dtype == want
+        assert torch.equal(out.o_prefill, ref.o_prefill.to(want))
+        assert torch.equal(out.o_decode, ref.o_decode.to(want))
+        assert torch.equal(out.lse_prefill, ref.lse_prefill) and torch.equal(out.lse_decode, ref.lse_decode)
+
+
+@pytest.mark.parametrize("policy", KERNELS)
 def test_deterministic_and_fused_equals_serial_bitwise(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=256, offset=700, decode_ctx=[900] * 6)
