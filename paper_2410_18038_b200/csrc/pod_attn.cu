@@ -28,6 +28,20 @@
 #include <vector>
 
 #include "pod_internal.h"
+
+// timing experiments only (tools/micro/build_variant.sh); both 0 in the product
+#ifndef POD_EXP_FAKE
+#define POD_EXP_FAKE 0
+#endif
+#ifndef POD_SOFTMAX_SKIP
+#define POD_SOFTMAX_SKIP 0
+#endif
+#ifndef POD_SM_NOLOAD
+#define POD_SM_NOLOAD 0
+#endif
+#ifndef POD_SM_NOMMA
+#define POD_SM_NOMMA 0
+#endif
 #include "sm100_ptx.cuh"
 
 namespace pod {
@@ -204,7 +218,11 @@ __device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, 
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
             const float2 x = ffma2(make_float2(s[32 * hf + c], s[32 * hf + c + 1]), sl2v, nm2);
+#if POD_EXP_FAKE  // timing experiment only: exp2 replaced by one FMA-pipe op
+            const float p0 = x.x * 0.5f, p1 = x.y * 0.5f;
+#else
             const float p0 = ptx::ex2(x.x), p1 = ptx::ex2(x.y);
+#endif
             lsum2 = fadd2(lsum2, make_float2(p0, p1));
             if constexpr (kMode == 1) {
                 const uint32_t u0 = __float_as_uint(p0), u1 = __float_as_uint(p1);

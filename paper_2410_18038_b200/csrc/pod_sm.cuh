@@ -66,7 +66,16 @@ constexpr int kThreads = (kDecWarp0 + kDW) * 32;
 // Prefill K/V tiles of 32 keys (2 pages): S is double-buffered per block inside
 // the block's 64 TMEM columns, so QK_X(t+1) runs while the softmax of tile t does.
 constexpr int kTN = 32;
-constexpr int kNS = 4;                                         // K and V ring stages
+#ifndef POD_SM_PROD_SLEEP
+#define POD_SM_PROD_SLEEP 128  // producer back-off (ns) while waiting for a free stage
+#endif
+#ifndef POD_SM_LAZY_PV
+#define POD_SM_LAZY_PV 1
+#endif
+#ifndef POD_SM_STAGES
+#define POD_SM_STAGES 4
+#endif
+constexpr int kNS = POD_SM_STAGES;                             // K and V ring stages
 constexpr uint32_t kStage = kTN * kHeadDim * 2;                // 8 KB: [d-half][32 keys][64 d], SW128
 constexpr uint32_t kOffKs = 0;
 constexpr uint32_t kOffVs = kNS * kStage;
@@ -79,7 +88,9 @@ constexpr uint32_t kOffBars = kOffDec + kDW * kDS * kDecStageBytes;
 //  arrivals, one commit per block's issuing thread)
 // (pv per S buffer: a waiter is never more than one completion behind on a
 // barrier, so parity waits stay unambiguous even when the softmax skips them)
-constexpr int kNumBars = 30;
+constexpr int kBarKF = 2, kBarKE = kBarKF + kNS, kBarVF = kBarKE + kNS, kBarVE = kBarVF + kNS;
+constexpr int kBarS = kBarVE + kNS, kBarP = kBarS + 4, kBarPV = kBarP + 4;
+constexpr int kNumBars = kBarPV + 4;
 constexpr uint32_t kOffDecBars = kOffBars + kNumBars * 8;
 constexpr uint32_t kOffMisc = kOffDecBars + kDW * kDS * 8;     // tmem slot, claim slots
 constexpr uint32_t kSmem = kOffMisc + 64;
@@ -92,12 +103,14 @@ struct PfState {
     int g = 0;            // K/V tiles issued (stage = g % kNS, phase = (g / kNS) & 1)
     int n[2] = {0, 0};    // tiles per block (S buffer = n & 1; s/p/pv phases (n >> 1) & 1)
     int nq[2] = {0, 0};   // Q loads per block (q_full phases)
+    int npv[2][2] = {{0, 0}, {0, 0}};  // pv commits per (block, S buffer) (POD_SM_LAZY_PV)
 };
 
 // S = Q K^T for one 32-key tile: A = Q (TMEM, 128 rows x 128 d), B = K (smem,
 // K-major SW128 [d-half][32 keys][64 d]), N = 32.
 template <int kFmt>
 __device__ __forceinline__ void issue_qk32(uint32_t tmem_s, uint32_t tmem_q, uint32_t sK) {
+    if (POD_SM_NOMMA) return;  // timing experiment only
     constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kTN, 0);
     ptx::umma_ts_k128_elect<kTN * 128>(tmem_s, tmem_q, ptx::sw128_desc(sK, 16, 1024), idesc);
 }
@@ -106,6 +119,7 @@ __device__ __forceinline__ void issue_qk32(uint32_t tmem_s, uint32_t tmem_q, uin
 template <int kFmt>
 __device__ __forceinline__ void issue_pv32(uint32_t tmem_o, uint32_t tmem_p, uint32_t sV, bool accumulate,
                                            bool split) {
+    if (POD_SM_NOMMA) return;  // timing experiment only
     constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);
     static_assert(kTN == 32, "umma_pv32_elect: two K-steps, lo part 16 columns after hi");
     const uint64_t b = ptx::sw128_desc(sV, kTN * 128, 1024);
@@ -159,7 +173,16 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             ps.n[1] += nt;
             ps.nq[1] += 1;
         }
+        // pv commits (see pv_commit below): tiles max(0, nt-2) .. nt-1, one per S buffer
+        for (int t = max(0, nt - 2); t < nt; ++t) {
+            ps.npv[0][(s0.n[0] + t) & 1] += 1;
+            if (hasB) ps.npv[1][(s0.n[1] + t) & 1] += 1;
+        }
     }
+    // POD_SM_LAZY_PV: PV_X(t) gets its own commit only for the last two tiles.  Earlier,
+    // "PV_X(t-1) done" is implied by S_X(t+1)'s commit (issued after PV_X(t-1) by the same
+    // thread, in-order pipe), which the softmax waits for anyway.
+    auto pv_commit = [&](int t) { return !POD_SM_LAZY_PV || t + 2 >= nt; };
     const int pbeg = p.page_indptr[0];
     const int npages = p.page_indptr[1] - pbeg;
     const uint32_t bar0 = sbase + kOffBars;
@@ -174,16 +197,24 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         for (int t = 0; t <= nt && nt > 0; ++t) {
             if (t < nt) {  // K of tile t
                 const int gg = s0.g + t, st = gg % kNS;
-                if (gg >= kNS) ptx::mbar_wait_relaxed<>(bar(6 + st), ((gg / kNS) - 1) & 1);
-                ptx::mbar_arrive_expect_tx_elect(bar(2 + st), kStage);
-                load_tile32(p, tmk, sK + st * kStage, bar(2 + st), kt0 + t * kTN, job.kv_head, ids);
+                if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarKE + st), ((gg / kNS) - 1) & 1);
+                if (POD_SM_NOLOAD && gg >= kNS) {  // timing experiment: stale K, no TMA
+                    if (lane == 0) ptx::mbar_arrive(bar(kBarKF + st));
+                } else {
+                    ptx::mbar_arrive_expect_tx_elect(bar(kBarKF + st), kStage);
+                    load_tile32(p, tmk, sK + st * kStage, bar(kBarKF + st), kt0 + t * kTN, job.kv_head, ids);
+                }
             }
             if (t > 0) {  // V of tile t-1 (single issuer: its stage was freed with K's)
                 const int gg = s0.g + t - 1, st = gg % kNS;
-                if ((kDualMma || !POD_SM_MERGED_EMPTY) && gg >= kNS)
-                    ptx::mbar_wait_relaxed<>(bar(14 + st), ((gg / kNS) - 1) & 1);
-                ptx::mbar_arrive_expect_tx_elect(bar(10 + st), kStage);
-                load_tile32(p, tmv, sV + st * kStage, bar(10 + st), kt0 + (t - 1) * kTN, job.kv_head, ids);
+                if (!POD_SM_MERGED_EMPTY && gg >= kNS)
+                    ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarVE + st), ((gg / kNS) - 1) & 1);
+                if (POD_SM_NOLOAD && gg >= kNS) {
+                    if (lane == 0) ptx::mbar_arrive(bar(kBarVF + st));
+                } else {
+                    ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
+                    load_tile32(p, tmv, sV + st * kStage, bar(kBarVF + st), kt0 + (t - 1) * kTN, job.kv_head, ids);
+                }
             }
         }
     } else if (!kDualMma && warp == kMmaWarp) {
@@ -196,58 +227,58 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             if (hasB) sm_wait<POD_SM_MMA_SLEEP>(bar(1), s0.nq[1] & 1);
             for (int j = 0; j < 2 && j < nt; ++j) {
                 const int gg = s0.g + j, st = gg % kNS;
-                sm_wait<POD_SM_MMA_SLEEP>(bar(2 + st), (gg / kNS) & 1);
+                sm_wait<POD_SM_MMA_SLEEP>(bar(kBarKF + st), (gg / kNS) & 1);
                 ptx::tc_fence_after();
                 const int bA = (s0.n[0] + j) & 1, bB = (s0.n[1] + j) & 1;
                 issue_qk32<kFmt>(tmem + kSA + 32 * bA, tmem + kQA, sK + st * kStage);
-                ptx::umma_commit_elect(bar(18 + bA));
+                ptx::umma_commit_elect(bar(kBarS + bA));
                 if (hasB) {
                     issue_qk32<kFmt>(tmem + kSB + 32 * bB, tmem + kQB, sK + st * kStage);
-                    ptx::umma_commit_elect(bar(20 + bB));
+                    ptx::umma_commit_elect(bar(kBarS + 2 + bB));
                 }
-                if (!POD_SM_MERGED_EMPTY) ptx::umma_commit_elect(bar(6 + st));
+                if (!POD_SM_MERGED_EMPTY) ptx::umma_commit_elect(bar(kBarKE + st));
             }
             for (int t = 0; t < nt; ++t) {
                 const int gg = s0.g + t, st = gg % kNS;
                 const int g2 = gg + 2, st2 = g2 % kNS;
                 const bool more = t + 2 < nt;
                 const int nA = s0.n[0] + t, bA = nA & 1;
-                sm_wait<POD_SM_MMA_SLEEP>(bar(22 + bA), (nA >> 1) & 1);
+                sm_wait<POD_SM_MMA_SLEEP>(bar(kBarP + bA), (nA >> 1) & 1);
                 trace_stamp(p, first, t, 4);
-                sm_wait<POD_SM_MMA_SLEEP>(bar(10 + st), (gg / kNS) & 1);
+                sm_wait<POD_SM_MMA_SLEEP>(bar(kBarVF + st), (gg / kNS) & 1);
                 trace_stamp(p, first, t < 128 ? 384 + t : 9999, 4);
                 ptx::tc_fence_after();
                 issue_pv32<kFmt>(tmem + kOA, tmem + kSA + 32 * bA, sV + st * kStage, t > 0, p.p_split != 0);
                 trace_stamp(p, first, t < 128 ? 384 + t : 9999, 5);
-                ptx::umma_commit_elect(bar(26 + bA));
+                if (pv_commit(t)) ptx::umma_commit_elect(bar(kBarPV + bA));
                 trace_stamp(p, first, t, 5);
                 if (more) {
-                    sm_wait<POD_SM_MMA_SLEEP>(bar(2 + st2), (g2 / kNS) & 1);
+                    sm_wait<POD_SM_MMA_SLEEP>(bar(kBarKF + st2), (g2 / kNS) & 1);
                     trace_stamp(p, first, t < 128 ? 384 + t : 9999, 6);
                     ptx::tc_fence_after();
                     issue_qk32<kFmt>(tmem + kSA + 32 * bA, tmem + kQA, sK + st2 * kStage);
-                    ptx::umma_commit_elect(bar(18 + bA));
+                    ptx::umma_commit_elect(bar(kBarS + bA));
                 }
                 trace_stamp(p, first, t, 6);
                 if (hasB) {
                     const int nB = s0.n[1] + t, bB = nB & 1;
-                    sm_wait<POD_SM_MMA_SLEEP>(bar(24 + bB), (nB >> 1) & 1);
+                    sm_wait<POD_SM_MMA_SLEEP>(bar(kBarP + 2 + bB), (nB >> 1) & 1);
                     trace_stamp(p, first, t < 128 ? 384 + t : 9999, 7);
                     ptx::tc_fence_after();
                     issue_pv32<kFmt>(tmem + kOB, tmem + kSB + 32 * bB, sV + st * kStage, t > 0, p.p_split != 0);
-                    ptx::umma_commit_elect(bar(28 + bB));
+                    if (pv_commit(t)) ptx::umma_commit_elect(bar(kBarPV + 2 + bB));
                     if (more) {
                         issue_qk32<kFmt>(tmem + kSB + 32 * bB, tmem + kQB, sK + st2 * kStage);
-                        ptx::umma_commit_elect(bar(20 + bB));
+                        ptx::umma_commit_elect(bar(kBarS + 2 + bB));
                     }
                 }
                 if (POD_SM_MERGED_EMPTY) {
                     // K and V of tile t are both consumed (QK(t) ran before PV(t)): one
                     // commit frees the stage for the producer
-                    ptx::umma_commit_elect(bar(6 + st));
+                    ptx::umma_commit_elect(bar(kBarKE + st));
                 } else {
-                    ptx::umma_commit_elect(bar(14 + st));
-                    if (more) ptx::umma_commit_elect(bar(6 + st2));
+                    ptx::umma_commit_elect(bar(kBarVE + st));
+                    if (more) ptx::umma_commit_elect(bar(kBarKE + st2));
                 }
             }
         }
@@ -269,34 +300,38 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             ptx::mbar_wait(bar(X), s0.nq[X] & 1);
             for (int j = 0; j < 2 && j < nt; ++j) {
                 const int gg = s0.g + j, st = gg % kNS;
-                ptx::mbar_wait(bar(2 + st), (gg / kNS) & 1);
+                ptx::mbar_wait(bar(kBarKF + st), (gg / kNS) & 1);
                 ptx::tc_fence_after();
                 const int bx = (s0.n[X] + j) & 1;
                 issue_qk32<kFmt>(tS + 32 * bx, tQ, sK + st * kStage);
-                ptx::umma_commit_elect(bar(18 + 2 * X + bx));
-                release(bar(6 + st));
+                ptx::umma_commit_elect(bar(kBarS + 2 * X + bx));
+                if (!POD_SM_MERGED_EMPTY) release(bar(kBarKE + st));
             }
             for (int t = 0; t < nt; ++t) {
                 const int gg = s0.g + t, st = gg % kNS;
                 const int g2 = gg + 2, st2 = g2 % kNS;
                 const bool more = t + 2 < nt;
                 const int n = s0.n[X] + t, bx = n & 1;
-                ptx::mbar_wait(bar(22 + 2 * X + bx), (n >> 1) & 1);
+                ptx::mbar_wait(bar(kBarP + 2 * X + bx), (n >> 1) & 1);
                 trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 4);
-                ptx::mbar_wait(bar(10 + st), (gg / kNS) & 1);
+                ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
                 ptx::tc_fence_after();
                 issue_pv32<kFmt>(tO, tS + 32 * bx, sV + st * kStage, t > 0, p.p_split != 0);
-                ptx::umma_commit_elect(bar(26 + 2 * X + bx));
+                if (pv_commit(t)) ptx::umma_commit_elect(bar(kBarPV + 2 * X + bx));
                 trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 5);
                 if (more) {
-                    ptx::mbar_wait(bar(2 + st2), (g2 / kNS) & 1);
+                    ptx::mbar_wait(bar(kBarKF + st2), (g2 / kNS) & 1);
                     ptx::tc_fence_after();
                     issue_qk32<kFmt>(tS + 32 * bx, tQ, sK + st2 * kStage);
-                    ptx::umma_commit_elect(bar(18 + 2 * X + bx));
+                    ptx::umma_commit_elect(bar(kBarS + 2 * X + bx));
                 }
                 trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 6);
-                release(bar(14 + st));
-                if (more) release(bar(6 + st2));
+                if (POD_SM_MERGED_EMPTY) {
+                    release(bar(kBarKE + st));  // K(t) and V(t) both consumed by this thread
+                } else {
+                    release(bar(kBarVE + st));
+                    if (more) release(bar(kBarKE + st2));
+                }
             }
         }
     } else {
@@ -357,9 +392,14 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             const int n = s0.n[X] + t, b = n & 1;
             const uint32_t s_addr = lane_base + (X ? kSB : kSA) + 32 * b;
             if (lane == 0 && q == 0) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 0);
-            sm_wait<POD_SM_SOFTMAX_SLEEP>(bar(18 + 2 * X + b), (n >> 1) & 1);
+            sm_wait<POD_SM_SOFTMAX_SLEEP>(bar(kBarS + 2 * X + b), (n >> 1) & 1);
             if (lane == 0 && q == 0) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 1);
             ptx::tc_fence_after();
+            if (POD_SOFTMAX_SKIP) {  // timing experiment only: P = S bits, no softmax work
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(bar(kBarP + 2 * X + b));
+                continue;
+            }
             float s[kTN];
             ptx::tmem_ld32(s_addr, s);
             ptx::tmem_wait_ld();
@@ -383,7 +423,12 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             // O is rescaled only when the reference max moved: then wait for
             // PV_X(t-1), the newest MMA writing O_X (PV_X(t) needs our arrival).
             if (t > 0 && __any_sync(0xffffffffu, need)) {
-                ptx::mbar_wait(bar(26 + 2 * X + ((n - 1) & 1)), ((n - 1) >> 1) & 1);
+                if (!POD_SM_LAZY_PV)
+                    ptx::mbar_wait(bar(kBarPV + 2 * X + ((n - 1) & 1)), ((n - 1) >> 1) & 1);
+                else if (t + 1 < nt)  // S_X(t+1) complete => PV_X(t-1) complete
+                    ptx::mbar_wait(bar(kBarS + 2 * X + ((n + 1) & 1)), ((n + 1) >> 1) & 1);
+                else
+                    ptx::mbar_wait(bar(kBarPV + 2 * X + ((n - 1) & 1)), s0.npv[X][(n - 1) & 1] & 1);
                 ptx::tc_fence_after();
 #pragma unroll 1
                 for (int ch = 0; ch < kHeadDim / 32; ++ch) {
@@ -409,12 +454,12 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             __syncwarp();
             if (lane == 0 && q == 0) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 2);
             if (lane == 0 && q == 3) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 3);
-            if (lane == 0) ptx::mbar_arrive(bar(22 + 2 * X + b));
+            if (lane == 0) ptx::mbar_arrive(bar(kBarP + 2 * X + b));
         }
         // ------------------------------------------------- epilogue --
         {  // the last PV's commit covers every earlier MMA of this thread
             const int nl = s0.n[X] + nt - 1;
-            ptx::mbar_wait(bar(26 + 2 * X + (nl & 1)), (nl >> 1) & 1);
+            ptx::mbar_wait(bar(kBarPV + 2 * X + (nl & 1)), POD_SM_LAZY_PV ? s0.npv[X][nl & 1] & 1 : (nl >> 1) & 1);
         }
         ptx::tc_fence_after();
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -476,8 +521,8 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
         if (sbase & 1023u) __trap();
         // q_full (0, 1) and p_full (22-25): one arrival per softmax warp of the block
         for (int i = 0; i < kNumBars; ++i)
-            ptx::mbar_init(sbase + kOffBars + 8 * i, (i <= 1 || (i >= 22 && i <= 25)) ? kPrefillWarps
-                                                     : (kDualMma && ((i >= 6 && i <= 9) || (i >= 14 && i <= 17))) ? 2 : 1);
+            ptx::mbar_init(sbase + kOffBars + 8 * i, (i <= 1 || (i >= kBarP && i < kBarP + 4)) ? kPrefillWarps
+                                                     : (kDualMma && i >= kBarKE && i < kBarVE + kNS && !(i >= kBarVF && i < kBarVE)) ? 2 : 1);
         for (int i = 0; i < kDW * kDS; ++i) ptx::mbar_init(sbase + kOffDecBars + 8 * i, 1);
         ptx::fence_mbar_init();
     }
