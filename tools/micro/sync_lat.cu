@@ -127,6 +127,86 @@ __global__ void __launch_bounds__(128, 1) sync_lat(int n, long long* out) {
     if (warp == 0) ptx::tmem_dealloc(tmem, 512);
 }
 
+// Replica of the pair engine's single-issuer loop (pod_sm.cuh prefill_item_sm) with the
+// softmax replaced by one responder warp per block (wait S, arrive P), no TMA:
+// cycles per tile-pair.  order as the kernel: PV_A, QK_A(t+2), PV_B, QK_B(t+2).
+template <int kNoMma, int kResp, int kProd>
+__global__ void __launch_bounds__(512, 1) pipe_replica(int n, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t bars[16];  // s[X][b] 2X+b, p[X][b] 4+2X+b, kfull 8+st, kvempty 12+st
+    const int warp = threadIdx.x / 32;
+    const uint32_t sb = ptx::smem_u32(smem);
+    auto bar = [&](int i) { return ptx::smem_u32(&bars[i]); };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 16; ++i) ptx::mbar_init(bar(i), (i >= 4 && i < 8) ? kResp : 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) {
+        ptx::tmem_alloc(ptx::smem_u32(&tmem_slot), 512);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    constexpr uint32_t idesc_qk = ptx::idesc_f16(1, 128, 32, 0);
+    constexpr uint32_t idesc_pv = ptx::idesc_f16(1, 128, 128, 1);
+    const uint64_t bk = ptx::sw128_desc(sb, 16, 1024);
+    const uint64_t bv = ptx::sw128_desc(sb + 65536, 32 * 128, 1024);
+    const uint32_t kQ[2] = {0, 64}, kS[2] = {128, 192}, kO[2] = {256, 384};
+    if (warp == 1) {
+        const long long t0 = clock64();
+        for (int j = 0; j < 2; ++j)
+            for (int X = 0; X < 2; ++X) {
+                if (kProd && X == 0) ptx::mbar_wait(bar(8 + j), 0);
+                if (!kNoMma) ptx::umma_ts_k128_elect<32 * 128>(tmem + kS[X] + 32 * j, tmem + kQ[X], bk, idesc_qk);
+                ptx::umma_commit_elect(bar(2 * X + j));
+            }
+        for (int t = 0; t < n; ++t) {
+            const int b = t & 1;
+            const bool more = t + 2 < n;
+            for (int X = 0; X < 2; ++X) {
+                ptx::mbar_wait(bar(4 + 2 * X + b), (t >> 1) & 1);
+                ptx::tc_fence_after();
+                if (!kNoMma) ptx::umma_pv32_elect<true>(tmem + kO[X], tmem + kS[X] + 32 * b, bv, idesc_pv, 1u);
+                if (more) {
+                    if (kProd && X == 0) {
+                        const int g2 = t + 2;
+                        ptx::mbar_wait(bar(8 + (g2 & 3)), (g2 >> 2) & 1);
+                        ptx::tc_fence_after();
+                    }
+                    if (!kNoMma) ptx::umma_ts_k128_elect<32 * 128>(tmem + kS[X] + 32 * b, tmem + kQ[X], bk, idesc_qk);
+                    ptx::umma_commit_elect(bar(2 * X + b));
+                }
+            }
+            if (kProd) ptx::umma_commit_elect(bar(12 + (t & 3)));  // stage of tile t free
+        }
+        ptx::umma_commit_elect(bar(2));  // spare: wait for the tail via a last commit on s_B[0]...
+        const long long t1 = clock64();
+        if (threadIdx.x == 32) out[blockIdx.x] = t1 - t0;
+    } else if (kProd && warp == 12) {  // producer: stage ring of 4, arrive instead of TMA
+        for (int g = 0; g < n; ++g) {
+            if (g >= 4) ptx::mbar_wait_relaxed<>(bar(12 + (g & 3)), ((g >> 2) - 1) & 1);
+            if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(bar(8 + (g & 3)));
+        }
+    } else if (warp >= 2 && warp < 2 + 2 * kResp) {
+        const int X = (warp - 2) / kResp;
+        for (int t = 0; t < n; ++t) {
+            const int b = t & 1;
+            ptx::mbar_wait(bar(2 * X + b), (t >> 1) & 1);
+            ptx::tc_fence_after();
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(bar(4 + 2 * X + b));
+        }
+    }
+    __nanosleep(20000);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 0) ptx::tmem_dealloc(tmem, 512);
+}
+
 int main() {
     long long* d;
     cudaMalloc(&d, 1024 * 8);
@@ -153,6 +233,27 @@ int main() {
         long long mx = 0;
         for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
         printf("%-45s %.1f cycles/iter\n", names[test], double(mx) / n);
+    }
+    {
+      for (int v = 0; v < 6; ++v) {
+        auto k = v == 0 ? pipe_replica<0, 1, 0> : v == 1 ? pipe_replica<1, 1, 0> : v == 2 ? pipe_replica<0, 4, 0>
+               : v == 3 ? pipe_replica<0, 4, 1> : v == 4 ? pipe_replica<1, 4, 1> : pipe_replica<0, 1, 1>;
+        const char* vn[6] = {"replica: MMAs, 1 responder/block", "replica: no MMAs, 1 responder/block",
+                             "replica: MMAs, 4 responders/block", "replica: MMAs, 4 resp, producer ring",
+                             "replica: no MMAs, 4 resp, producer ring", "replica: MMAs, 1 resp, producer ring"};
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        const int n = 1000;
+        for (int rep = 0; rep < 2; ++rep) k<<<148, 512, 200 * 1024>>>(n, d);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            printf("err %s\n", cudaGetErrorString(e));
+            return 1;
+        }
+        cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
+        long long mx = 0;
+        for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+        printf("%-45s %.1f cycles/tile-pair\n", vn[v], double(mx) / n);
+      }
     }
     return 0;
 }
