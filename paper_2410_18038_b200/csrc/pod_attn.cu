@@ -37,6 +37,9 @@
 #ifndef POD_SOFTMAX_SKIP
 #define POD_SOFTMAX_SKIP 0
 #endif
+#ifndef POD_UNIFORM_WARP
+#define POD_UNIFORM_WARP 1  // two-CTA kernel: see uniform_warp()
+#endif
 #ifndef POD_SM_NOLOAD
 #define POD_SM_NOLOAD 0
 #endif
@@ -353,6 +356,13 @@ __device__ __forceinline__ void store1(const ORow& o, int c, float v) {
         reinterpret_cast<__half*>(o.ptr)[c] = __float2half_rn(v);
 }
 
+// Warp index broadcast from lane 0, so the compiler treats it (and the role loops
+// derived from it) as warp-uniform and keeps MMA / TMA operands on the uniform datapath.
+__device__ __forceinline__ int uniform_warp() {
+    return POD_UNIFORM_WARP ? __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0)
+                            : static_cast<int>(threadIdx.x >> 5);
+}
+
 __device__ __forceinline__ void trace_stamp(const RunParams& p, int items, int t, int k) {
     if (POD_TRACE_STAMPS && p.trace && blockIdx.x == 0 && items == 0 && t < 768 && p.role_log) {
         int32_t* tr = p.role_log + p.trace;
@@ -366,7 +376,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                              PrefillState& ps) {
     const PrefillCta job = p.pctas[cta_id];
     const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
+    const int warp = uniform_warp(), lane = tid & 31;
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t sQ = sbase + kOffQ, sK = sbase + kOffK, sV = sbase + kOffV;
     const uint32_t bar0 = sbase + kOffBar;
@@ -648,7 +658,7 @@ __device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const 
                               uint8_t* smem, uint32_t tmem, Prefill2State& ps) {
     const PrefillCta job = p.pctas[cta_id];
     const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
+    const int warp = uniform_warp(), lane = tid & 31;
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t sK = sbase + kOffK2, sV = sbase + kOffV2;
     const uint32_t bar0 = sbase + kOffBar;
@@ -1409,7 +1419,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     extern __shared__ __align__(1024) uint8_t smem[];
     int* role = reinterpret_cast<int*>(smem + kOffRole);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmemSlot);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = uniform_warp(), lane = tid & 31;
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t sm = ptx::smid();
     constexpr bool slots = kSlots;  // POD_POLICY_SLOTS (engine 2) vs ticket policies (engine 1)
