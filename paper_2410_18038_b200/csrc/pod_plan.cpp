@@ -249,13 +249,14 @@ void lower(pod_plan& p) {
     if (splits <= 0) {
         if (warpspec) {
             // one decode group per SM: items of <= ~4 MB of K/V (the per-item latency
-            // stays a small share) and at least 2 items per SM (a short tail);
-            // measured at C2 B=64 (2 splits) and the C3 TP8 rank (4-5 splits)
+            // stays a small share) and at least 1.5 items per SM (a short tail);
+            // measured sweep: C2 B=64 / B=32 / B=16 -> 2, C3 TP4 rank -> 2,
+            // C3 TP8 rank -> 4 (2 x nsm / parents gave 3 and 5: 2-7 % slower)
             int64_t max_ctx = 0;
             for (int64_t c : p.decode_ctx) max_ctx = std::max(max_ctx, c);
             const int64_t parent_bytes = max_ctx * 4 * s.head_dim;  // bf16 K + V of one KV head
             const int64_t by_size = ceil_div(parent_bytes, int64_t(4) << 20);
-            const int64_t by_count = parents == 0 ? 1 : ceil_div(2 * static_cast<int64_t>(p.dev.num_sms), parents);
+            const int64_t by_count = parents == 0 ? 1 : ceil_div(3 * static_cast<int64_t>(p.dev.num_sms), 2 * parents);
             splits = std::max<int64_t>(1, std::max(by_size, by_count));
         } else {
             const int64_t slots = static_cast<int64_t>(p.dev.num_sms) * 2;
