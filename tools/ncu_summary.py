@@ -84,7 +84,8 @@ def launches(path):
     print("| # | kernel | duration (us) |\n|---|---|---|")
     n = 0
     for r in rows[start + 1:]:
-        if len(r) != len(hdr) or r[iM] != "gpu__time_duration.sum" or "pod::" not in r[iK]:
+        if len(r) != len(hdr) or r[iM] != "gpu__time_duration.sum" or not re.search(
+                r"pod::|pod_sm_kernel|pod_fused_kernel|merge_kernel|append_kv_kernel", r[iK]):
             continue
         n += 1
         print(f"| {n} | {r[iK][:70]} | {float(r[iV].replace(',', '')) / 1000:.1f} |")
