@@ -128,7 +128,9 @@ struct RunParams {
     int32_t chunk;
     int32_t offset;
     int32_t kv_layout;
-    int32_t decode_splits;
+    int32_t decode_splits;   // largest split count = partials' stride
+    int32_t dec_split_base;  // splits of requests below dec_tail_start
+    int32_t dec_tail_start;
     int32_t policy;
     float w_prefill;  // POD_POLICY_BALANCED: estimated slot-us per prefill / decode item
     float w_decode;
@@ -1311,7 +1313,7 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
         out_o = out_row(p.o_prefill, row * kHeadDim, p.out_fmt);
         out_l = p.lse_prefill + row;
     } else {
-        n = p.decode_splits;  // uniform per plan (clamped to the shortest context)
+        n = r >= p.dec_tail_start ? p.decode_splits : p.dec_split_base;  // per request (whole waves)
         if (n <= 1) return;
         const size_t row = static_cast<size_t>(r) * p.decode_splits * p.hq + qh;
         po = p.dpart_o + row * kHeadDim;
@@ -1726,6 +1728,8 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.offset = plan->batch.has_prefill ? static_cast<int32_t>(plan->batch.prefill.position_offset) : 0;
     p.kv_layout = plan->batch.kv_layout;
     p.decode_splits = static_cast<int32_t>(plan->decode_splits);
+    p.dec_split_base = static_cast<int32_t>(plan->dec_split_base);
+    p.dec_tail_start = static_cast<int32_t>(plan->dec_tail_start);
     p.policy = plan->opts.policy;
     p.w_prefill = static_cast<float>(plan->w_prefill);
     p.w_decode = static_cast<float>(plan->w_decode);

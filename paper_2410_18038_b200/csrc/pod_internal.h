@@ -86,7 +86,9 @@ struct pod_plan {
     std::vector<pod::DecodeCta> dctas;
     std::vector<int32_t> tile_splits;
     std::vector<int32_t> dec_pos;  // context_len - 1 per decode (KV append)
-    int64_t decode_splits = 1;
+    int64_t decode_splits = 1;     // largest split count (partials' stride)
+    int64_t dec_split_base = 1;    // splits of requests [0, dec_tail_start)
+    int64_t dec_tail_start = 0;    // first request with decode_splits splits
     int64_t prefill_ratio = 1;
     int64_t decode_ratio = 1;
     int32_t max_prefill_splits = 1;

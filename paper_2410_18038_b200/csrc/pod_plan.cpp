@@ -22,6 +22,10 @@
 
 #include "pod_internal.h"
 
+#ifndef POD_WHOLE_WAVES
+#define POD_WHOLE_WAVES 1  // warp-specialised decode items rounded up to whole waves
+#endif
+
 namespace {
 
 struct Status : std::exception {
@@ -214,6 +218,8 @@ void decompose_prefill(pod_plan& p) {
 }
 
 // Lower tasks to the kernels' physical CTA tables.
+double decode_share(const pod_plan& p);
+
 void lower(pod_plan& p) {
     const pod_shape& s = p.shape;
     p.pctas.clear();
@@ -272,10 +278,37 @@ void lower(pod_plan& p) {
         if (p.opts.decode_splits <= 0) splits = std::min(splits, cap);
     }
     p.decode_splits = std::max<int64_t>(1, splits);
+    // Whole waves (warp-specialised kernel): the decode items are claimed in id order
+    // (request-major) by one decode group per SM, so a count that is not a multiple of
+    // the SM count leaves SMs idle for the last item's duration.  The last requests get
+    // one split more, lifting the item count to the next multiple of num_sms (the items
+    // claimed last are the smaller ones).  decode_splits becomes the largest count (the
+    // partials' stride); dec_split_base is the count of requests below dec_tail_start.
+    p.dec_split_base = p.decode_splits;
+    p.dec_tail_start = static_cast<int64_t>(p.decode_ctx.size());
+    // (decode-dominant batches only: when the prefill role is the longer one the decode
+    // balance does not set the makespan and the extra merge rows cost ~1 %, C2 B=16)
+    if (warpspec && p.opts.decode_splits <= 0 && !p.decode_ctx.empty() && POD_WHOLE_WAVES &&
+        decode_share(p) >= 0.5) {
+        int64_t min_ctx = INT64_MAX;
+        for (int64_t c : p.decode_ctx) min_ctx = std::min(min_ctx, c);
+        const int64_t cap = std::max<int64_t>(1, min_ctx / (pod::kSmDecodeWarps * 16));
+        const int64_t nb = static_cast<int64_t>(p.decode_ctx.size());
+        const int64_t items = parents * p.decode_splits, nsm = p.dev.num_sms;
+        const int64_t extra = ceil_div(items, nsm) * nsm - items;   // parents needing one more split
+        const int64_t ntail = std::min<int64_t>(nb, extra / s.num_kv_heads);
+        if (ntail > 0 && p.decode_splits + 1 <= cap) {
+            p.dec_tail_start = nb - ntail;
+            p.decode_splits += 1;
+        }
+    }
+    auto splits_of = [&](size_t r) {
+        return static_cast<int64_t>(r) >= p.dec_tail_start ? p.decode_splits : p.dec_split_base;
+    };
     const int page_row0 = p.batch.has_prefill ? 1 : 0;
     for (size_t r = 0; r < p.decode_ctx.size(); ++r) {
         const long ctx = p.decode_ctx[r];
-        const long sp_n = std::min<long>(p.decode_splits, ctx);
+        const long sp_n = std::min<long>(splits_of(r), ctx);
         const long base = ctx / sp_n, rem = ctx % sp_n;
         for (int h = 0; h < s.num_kv_heads; ++h) {
             long pos = 0;
@@ -304,8 +337,8 @@ void lower(pod_plan& p) {
                 p.merge_rows_prefill += static_cast<int32_t>(rows * s.num_q_heads);
             }
     p.merge_rows_decode = 0;
-    for (int64_t c : p.decode_ctx)
-        if (std::min<int64_t>(p.decode_splits, c) > 1)
+    for (size_t r = 0; r < p.decode_ctx.size(); ++r)
+        if (std::min<int64_t>(splits_of(r), p.decode_ctx[r]) > 1)
             p.merge_rows_decode += s.num_q_heads;
 }
 

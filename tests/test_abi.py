@@ -51,11 +51,13 @@ def test_reference_default_device_matches_gpuspec():
 def test_plan_info_and_workspace():
     shape = ModelShape(32, 8, 128, 128 ** 0.5)
     b = HybridBatchSpec(prefill=PrefillSpec(1024, 16384, 15360), decodes=[DecodeSpec(16384)] * 64, shape=shape)
-    # default: warp-specialised one-CTA-per-SM kernel (two-block prefill items, decode
-    # parents split for ~6 items per SM)
+    # default: warp-specialised one-CTA-per-SM kernel (two-block prefill items; decode
+    # parents split in 2; the last request's 8 parents in 3, filling the 7th wave of 148
+    # items as far as whole requests allow: 1032 of 1036)
     p = Plan(b, GpuSpec.b200())
     i = p.info()
-    assert i.num_prefill_ctas == 128 and i.num_decode_ctas == 1024 and i.decode_splits == 2
+    assert i.num_prefill_ctas == 128 and i.num_decode_ctas == 1032 and i.decode_splits == 3
+    assert 6 * 148 < i.num_decode_ctas <= 7 * 148
     assert i.smem_bytes > 0 and p.workspace_bytes() == i.workspace_bytes > 0
     assert i.smem_bytes + 1024 <= 233472  # one CTA per SM
     # the two-CTA-per-SM POD kernel

@@ -237,6 +237,17 @@ def test_split_invariance(policy):
         assert d <= O_TOL and p <= O_TOL
 
 
+def test_whole_wave_split_mix_matches_oracle():
+    """Warp-specialised plan of a decode-dominant batch: the last requests get one KV
+    split more so the decode items fill whole waves of SMs (pod_plan.cpp); the merge
+    uses each request's own split count."""
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(4, 1, 128, SCALE), chunk=16, offset=100, decode_ctx=[2048] * 64)
+    wl, op, out = _run(batch, options=pkg.PlanOptions(policy=POD_POLICY_WARPSPEC))
+    assert op.info.num_decode_ctas == 296 and op.info.decode_splits == 5  # 24 x 4 + 40 x 5 splits
+    _check(wl, out, requests=[0, 23, 24, 25, 63])
+
+
 @pytest.mark.parametrize("policy", KERNELS)
 @pytest.mark.parametrize("out_dtype", [pkg._abi.POD_OUT_BF16, pkg._abi.POD_OUT_F16])
 def test_16bit_outputs_are_rounded_fp32_outputs(policy, out_dtype):
