@@ -181,7 +181,7 @@ typedef struct pod_plan_info {
     int32_t num_merge_rows_prefill; /* (row, q head) pairs needing a split merge */
     int32_t num_merge_rows_decode;
     int32_t policy;             /* the POD_POLICY_* the plan runs (POD_POLICY_AUTO resolved) */
-    int32_t pad_;
+    int32_t prefill_tile_keys;  /* keys per prefill K/V tile of the warp-specialised pair engine (32 or 64; 0 otherwise) */
 } pod_plan_info;
 
 typedef struct pod_plan pod_plan;

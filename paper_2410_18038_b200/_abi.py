@@ -79,7 +79,7 @@ class pod_plan_info(C.Structure):
                 ("decode_splits", C.c_int64), ("prefill_ratio", C.c_int64),
                 ("decode_ratio", C.c_int64), ("smem_bytes", C.c_int64),
                 ("workspace_bytes", C.c_int64), ("num_merge_rows_prefill", C.c_int32),
-                ("num_merge_rows_decode", C.c_int32), ("policy", C.c_int32), ("pad_", C.c_int32)]
+                ("num_merge_rows_decode", C.c_int32), ("policy", C.c_int32), ("prefill_tile_keys", C.c_int32)]
 
 
 # (name, restype, argtypes) for every symbol include/pod_attn.h declares.

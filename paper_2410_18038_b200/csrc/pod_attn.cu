@@ -135,6 +135,7 @@ struct RunParams {
     float w_prefill;  // POD_POLICY_BALANCED: estimated slot-us per prefill / decode item
     float w_decode;
     int32_t p_split;  // prefill P as bf16 hi + lo (two PV MMAs)
+    int32_t pf_tn64;  // warp-specialised kernel: 64-key single-S pair engine (prefill-dominant plans)
     int32_t grid_per_sm;   // resident CTAs per SM of the persistent launch (1 or 2)
     int32_t trace;         // debug: per-tile cycle stamps of CTA 0's first prefill item after the role log
     int32_t trace_mode;    // debug: 2 = serialise MMA issue with completion (execution latency probe)
@@ -1734,6 +1735,7 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.w_prefill = static_cast<float>(plan->w_prefill);
     p.w_decode = static_cast<float>(plan->w_decode);
     p.p_split = plan->opts.precision == POD_PRECISION_SPLIT ? 1 : 0;
+    p.pf_tn64 = plan->pf_tn64 ? 1 : 0;
     p.out_fmt = plan->opts.out_dtype;
     {
         static const char* grid_env = std::getenv("POD_GRID_PER_SM");  // experiment knob

@@ -86,6 +86,7 @@ struct pod_plan {
     std::vector<pod::DecodeCta> dctas;
     std::vector<int32_t> tile_splits;
     std::vector<int32_t> dec_pos;  // context_len - 1 per decode (KV append)
+    bool pf_tn64 = false;          // warp-specialised: 64-key pair engine (see pod_plan.cpp)
     int64_t decode_splits = 1;     // largest split count (partials' stride)
     int64_t dec_split_base = 1;    // splits of requests [0, dec_tail_start)
     int64_t dec_tail_start = 0;    // first request with decode_splits splits

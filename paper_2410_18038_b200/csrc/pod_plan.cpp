@@ -278,6 +278,15 @@ void lower(pod_plan& p) {
         if (p.opts.decode_splits <= 0) splits = std::min(splits, cap);
     }
     p.decode_splits = std::max<int64_t>(1, splits);
+    // Pair-engine tile width (warp-specialised kernel): 64-key tiles with one S buffer
+    // per block issue a third fewer MMAs and half the barrier hops per key (prefill
+    // -6 %, prefill-dominant fused C2 B=16/32 -6 %) but slowed the decode-dominant fused
+    // batches (C2 B=64 +9 %), so they serve prefill-dominant batches only.
+    {
+        static const char* tn_env = std::getenv("POD_TN64");  // experiment knob: 0 / 1 forces
+        p.pf_tn64 = warpspec && p.batch.has_prefill &&
+                    (tn_env ? std::atoi(tn_env) != 0 : decode_share(p) < 0.5);
+    }
     // Whole waves (warp-specialised kernel): the decode items are claimed in id order
     // (request-major) by one decode group per SM, so a count that is not a multiple of
     // the SM count leaves SMs idle for the last item's duration.  The last requests get
@@ -649,6 +658,7 @@ pod_status pod_attn_plan_get_info(const pod_plan* p, pod_plan_info* out) {
     out->num_merge_rows_prefill = p->merge_rows_prefill;
     out->num_merge_rows_decode = p->merge_rows_decode;
     out->policy = p->opts.policy;
+    out->prefill_tile_keys = p->opts.policy == POD_POLICY_WARPSPEC && p->batch.has_prefill ? (p->pf_tn64 ? 64 : 32) : 0;
     return POD_OK;
 }
 

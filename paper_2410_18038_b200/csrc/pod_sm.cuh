@@ -503,6 +503,267 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// The pair engine over 64-key K/V tiles with ONE S buffer per block (plans with
+// pf_tn64: prefill-dominant batches, pod_plan.cpp).
+// TMEM keeps the same columns (Q_A | Q_B | S_A | S_B | O_A | O_B, S now 64 keys
+// wide): per 64 keys a block issues 8 QK (N = 64) + 8 PV MMAs instead of 2 x 12,
+// and half the barrier hops.  With S single-buffered, QK_X(t+1) follows PV_X(t)
+// in the in-order pipe, and S_X(t) complete implies PV_X(t-1) complete, so the
+// lazy O rescale needs no extra wait.  K and V rings: 2 stages of 16 KB each with
+// separate empty barriers (K freed after both QKs, V after both PVs).
+namespace sm64 {
+constexpr int kTN = 64;
+constexpr int kNS = 2;
+constexpr uint32_t kStage = kTN * kHeadDim * 2;  // 16 KB: [d-half][64 keys][64 d], SW128
+static_assert(2 * kNS * kStage <= 2 * sm3::kNS * sm3::kStage, "same ring bytes as the 32-key engine");
+__device__ __forceinline__ void load_tile64(const RunParams& p, const CUtensorMap* tm, uint32_t dst, uint32_t bar,
+                                            int kt, int kv_head, const PageIds& ids) {
+    int ph[4];
+#pragma unroll
+    for (int pg = 0; pg < 4; ++pg) ph[pg] = ids.get(min(kt / 16 + pg, ids.n - 1));
+#pragma unroll
+    for (int pg = 0; pg < 4; ++pg) {
+#pragma unroll
+        for (int dh = 0; dh < 2; ++dh) {
+            const uint32_t d = dst + dh * (kTN * 128) + pg * 2048;
+            if (p.kv_layout == POD_KV_HND)
+                ptx::tma_load_4d_elect(d, tm, bar, dh * 64, 0, kv_head, ph[pg]);
+            else
+                ptx::tma_load_4d_elect(d, tm, bar, dh * 64, kv_head, 0, ph[pg]);
+        }
+    }
+}
+template <int kFmt>
+__device__ __forceinline__ void issue_qk64(uint32_t tmem_s, uint32_t tmem_q, uint32_t sK) {
+    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kTN, 0);
+    ptx::umma_ts_k128_elect<kTN * 128>(tmem_s, tmem_q, ptx::sw128_desc(sK, 16, 1024), idesc);
+}
+}  // namespace sm64
+
+template <int kFmt>
+__device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv, int item,
+                                  uint32_t sbase, uint32_t tmem, sm3::PfState& ps, int warp, int lane) {
+    using namespace sm3;
+    using sm64::kTN;
+    using sm64::kNS;
+    using sm64::kStage;
+    const PrefillCta job = p.pctas[item];
+    const int G = p.group;
+    const int rpb = kMBlock / G;
+    const int nblocks = (job.rows + rpb - 1) / rpb;  // 1 or 2
+    const bool hasB = nblocks > 1;
+    const BlockRange rA = prefill_block(p, job, 0);
+    const BlockRange rB = hasB ? prefill_block(p, job, 1) : rA;
+    const int kv_hi = min(job.kv_end, p.offset + (hasB ? rB.r0 + rB.nrows : rA.r0 + rA.nrows));
+    const int kt0 = rA.kt0;
+    const int nt = kv_hi > job.kv_begin ? (kv_hi - kt0 + kTN - 1) / kTN : 0;
+    const PfState s0 = ps;
+    if (nt > 0) {  // g: tiles through the rings; n: S / P completions; npv[X][0]: PV commits
+        ps.g += nt;
+        ps.n[0] += nt;
+        ps.nq[0] += 1;
+        ps.npv[0][0] += 1;
+        if (hasB) {
+            ps.n[1] += nt;
+            ps.nq[1] += 1;
+            ps.npv[1][0] += 1;
+        }
+    }
+    const int pbeg = p.page_indptr[0];
+    const int npages = p.page_indptr[1] - pbeg;
+    const uint32_t bar0 = sbase + kOffBars;
+    auto bar = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
+    const uint32_t sK = sbase + kOffKs, sV = sbase + kOffKs + kNS * kStage;
+
+    if (warp == kProdWarp) {
+        // ------------------------------------------------ TMA producer --
+        PageIds ids;
+        ids.init(p.page_indices + pbeg, npages, kt0 / 16);
+        for (int t = 0; t < nt; ++t) {
+            const int gg = s0.g + t, st = gg % kNS;
+            if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarKE + st), ((gg / kNS) - 1) & 1);
+            ptx::mbar_arrive_expect_tx_elect(bar(kBarKF + st), kStage);
+            sm64::load_tile64(p, tmk, sK + st * kStage, bar(kBarKF + st), kt0 + t * kTN, job.kv_head, ids);
+            if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarVE + st), ((gg / kNS) - 1) & 1);
+            ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
+            sm64::load_tile64(p, tmv, sV + st * kStage, bar(kBarVF + st), kt0 + t * kTN, job.kv_head, ids);
+        }
+    } else if (warp == kMmaWarp) {
+        // -------------------------------------------------- MMA issuer --
+        auto mma_issuer = [&](auto split_c) {
+            constexpr bool kSplit = decltype(split_c)::value;
+            if (nt == 0) return;
+            ptx::mbar_wait(bar(0), s0.nq[0] & 1);
+            if (hasB) ptx::mbar_wait(bar(1), s0.nq[1] & 1);
+            {
+                const int gg = s0.g, st = gg % kNS;
+                ptx::mbar_wait(bar(kBarKF + st), (gg / kNS) & 1);
+                ptx::tc_fence_after();
+                sm64::issue_qk64<kFmt>(tmem + kSA, tmem + kQA, sK + st * kStage);
+                ptx::umma_commit_elect(bar(kBarS + 0));
+                if (hasB) {
+                    sm64::issue_qk64<kFmt>(tmem + kSB, tmem + kQB, sK + st * kStage);
+                    ptx::umma_commit_elect(bar(kBarS + 1));
+                }
+                ptx::umma_commit_elect(bar(kBarKE + st));
+            }
+            for (int t = 0; t < nt; ++t) {
+                const int gg = s0.g + t, st = gg % kNS;
+                const int g1 = gg + 1, st1 = g1 % kNS;
+                const bool more = t + 1 < nt, last = t + 1 == nt;
+#pragma unroll
+                for (int X = 0; X < 2; ++X) {
+                    if (X == 1 && !hasB) break;
+                    const int n = s0.n[X] + t;
+                    ptx::mbar_wait(bar(kBarP + X), n & 1);
+                    if (X == 0) ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
+                    ptx::tc_fence_after();
+                    prefill_issue_pv<kFmt>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA), sV + st * kStage, t > 0,
+                                           kSplit);
+                    if (last) ptx::umma_commit_elect(bar(kBarPV + X));
+                    if (more) {
+                        if (X == 0) {
+                            ptx::mbar_wait(bar(kBarKF + st1), (g1 / kNS) & 1);
+                            ptx::tc_fence_after();
+                        }
+                        sm64::issue_qk64<kFmt>(tmem + (X ? kSB : kSA), tmem + (X ? kQB : kQA), sK + st1 * kStage);
+                        ptx::umma_commit_elect(bar(kBarS + X));
+                    }
+                }
+                ptx::umma_commit_elect(bar(kBarVE + st));          // V(t): both PVs issued above
+                if (more) ptx::umma_commit_elect(bar(kBarKE + st1));  // K(t+1): both QKs
+            }
+        };
+        if (p.p_split != 0)
+            mma_issuer(std::true_type{});
+        else
+            mma_issuer(std::false_type{});
+    } else if (warp < kProdWarp) {
+        // ------------------------------------ softmax (4 warps per block) --
+        const int X = warp >> 2;  // block
+        if (X == 1 && !hasB) return;
+        const int q = warp & 3;   // TMEM lane quadrant
+        const BlockRange br = X ? rB : rA;
+        const int m = q * 32 + lane;
+        const int my_r = br.r0 + m / G;
+        const bool row_ok = (m / G) < br.nrows;
+        const int vis = p.offset + my_r;
+        const int qhead = job.kv_head * G + m % G;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        const uint32_t o_addr = lane_base + (X ? kOB : kOA);
+        const uint32_t s_addr = lane_base + (X ? kSB : kSA);
+        ORow orow;
+        float* lrow;
+        if (job.n_splits == 1) {
+            orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim, p.out_fmt);
+            lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
+        } else {
+            const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
+            orow = out_row(p.ppart_o, row * kHeadDim, 0);
+            lrow = p.ppart_lse + row;
+        }
+        if (nt == 0) {
+            if (row_ok) {
+                for (int c = 0; c < kHeadDim; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
+                *lrow = -INFINITY;
+            }
+            return;
+        }
+        {  // Q row -> TMEM (A operand of QK^T); rows past the chunk are zero
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(static_cast<const uint16_t*>(p.q_prefill) +
+                                                                    (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                float qv[32];
+#pragma unroll
+                for (int c = 0; c < 32; c += 4) {
+                    const uint4 v = row_ok ? __ldg(reinterpret_cast<const uint4*>(src + 32 * hf + c))
+                                           : make_uint4(0u, 0u, 0u, 0u);
+                    qv[c] = __uint_as_float(v.x);
+                    qv[c + 1] = __uint_as_float(v.y);
+                    qv[c + 2] = __uint_as_float(v.z);
+                    qv[c + 3] = __uint_as_float(v.w);
+                }
+                ptx::tmem_st32(lane_base + (X ? kQB : kQA) + 32 * hf, qv);
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(bar(X));
+        }
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int t = 0; t < nt; ++t) {
+            const int n = s0.n[X] + t;
+            ptx::mbar_wait(bar(kBarS + X), n & 1);  // also: PV_X(t-1) complete
+            ptx::tc_fence_after();
+            float s[kTN];
+            ptx::tmem_ld32(s_addr, *reinterpret_cast<float(*)[32]>(&s[0]));
+            ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+            ptx::tmem_wait_ld();
+            const int kb = kt0 + t * kTN;
+            const int lo = max(job.kv_begin - kb, 0);
+            const int hi = row_ok ? min(min(job.kv_end, vis + 1) - kb, kTN) : 0;
+            if (!__all_sync(0xffffffffu, lo == 0 && hi == kTN)) {
+#pragma unroll
+                for (int c = 0; c < kTN; ++c)
+                    if (c < lo || c >= hi) s[c] = -INFINITY;
+            }
+            float tmax = s[0];
+#pragma unroll
+            for (int c = 1; c < kTN; c += 2) tmax = fmaxf(tmax, fmaxf(s[c], s[min(c + 1, kTN - 1)]));
+            const float m_new = fmaxf(m_run, tmax * p.sl2);
+            const bool need = m_new > m_run + 8.f;  // lazy rescale (see prefill_item)
+            const float m_use = need ? m_new : m_run;
+            const float factor = need ? ptx::ex2(m_run - m_new) : 1.f;
+            l_run *= factor;
+            m_run = m_use;
+            if (t > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll 1
+                for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+                    float o[32];
+                    ptx::tmem_ld32(o_addr + ch * 32, o);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) o[c] *= factor;
+                    ptx::tmem_st32(o_addr + ch * 32, o);
+                }
+            }
+            const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
+            float lsum;
+            if (kFmt == 1 && p.p_split)
+                lsum = softmax_p_row<kFmt, 1, kTN>(s, p.sl2, neg_m, s_addr);
+            else if (p.p_split)
+                lsum = softmax_p_row<kFmt, 2, kTN>(s, p.sl2, neg_m, s_addr);
+            else
+                lsum = softmax_p_row<kFmt, 0, kTN>(s, p.sl2, neg_m, s_addr);
+            l_run += lsum;
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(bar(kBarP + X));
+        }
+        ptx::mbar_wait(bar(kBarPV + X), s0.npv[X][0] & 1);  // the last PV (commit covers all)
+        ptx::tc_fence_after();
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll 1
+        for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+            float o[32];
+            ptx::tmem_ld32(o_addr + ch * 32, o);
+            ptx::tmem_wait_ld();
+            if (row_ok) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 4)
+                    store4(orow, ch * 32 + c,
+                           make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
+            }
+        }
+        if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
+        ptx::tc_fence_before();
+    }
+}
+
 __device__ __forceinline__ void sm_log_claim(const RunParams& p, int op, int id, int32_t* slot_out) {
     *slot_out = -1;
     if (!p.role_log || id < 0) return;
@@ -590,7 +851,10 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
             const int id = misc[2];
             prev_slot = misc[3];
             if (id < 0) break;
-            prefill_item_sm<kFmt>(p, &tmk, &tmv, id, sbase, tmem, ps, warp, lane);
+            if (p.pf_tn64)
+                prefill_item_sm64<kFmt>(p, &tmk, &tmv, id, sbase, tmem, ps, warp, lane);
+            else
+                prefill_item_sm<kFmt>(p, &tmk, &tmv, id, sbase, tmem, ps, warp, lane);
         }
         ptx::tc_fence_before();
         ptx::named_bar_sync(1, kPrefillThreads);

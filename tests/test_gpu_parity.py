@@ -237,6 +237,19 @@ def test_split_invariance(policy):
         assert d <= O_TOL and p <= O_TOL
 
 
+@pytest.mark.parametrize("chunk,offset,ctx,keys", [(256, 1000, [300, 90], 64), (16, 100, [4096] * 8, 32)])
+def test_pair_engine_tile_widths_match_oracle(chunk, offset, ctx, keys):
+    """Warp-specialised kernel: prefill-dominant plans run the 64-key single-S pair
+    engine, decode-dominant ones the 32-key double-S engine; both against the oracle,
+    including peaky queries (online-softmax rescales)."""
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=chunk, offset=offset, decode_ctx=ctx)
+    for q_scale in (1.0, 8.0):
+        wl, op, out = _run(batch, q_scale=q_scale, options=pkg.PlanOptions(policy=POD_POLICY_WARPSPEC))
+        assert op.info.prefill_tile_keys == keys
+        _check(wl, out)
+
+
 def test_whole_wave_split_mix_matches_oracle():
     """Warp-specialised plan of a decode-dominant batch: the last requests get one KV
     split more so the decode items fill whole waves of SMs (pod_plan.cpp); the merge
