@@ -517,18 +517,18 @@ double decode_share(const pod_plan& p) {
 void build(pod_plan& p) {
     validate_batch(p);
     if (p.opts.policy == POD_POLICY_AUTO) {
-        // measured on B200: the one-CTA-per-SM kernel wins once the
-        // decode stream dominates (it keeps HBM saturated next to the prefill);
-        // prefill-heavy batches run faster on two POD CTAs per SM
-        // (C2 at B = 8/16/32/64: 508 vs 542, 554 vs 557, 592 vs 671, 738 vs 800 us;
-        // C1: 82 vs 89 us -- one-CTA-per-SM vs two-CTA POD, best split caps)
+        // measured on B200: the one-CTA-per-SM kernel wins unless the
+        // prefill dominates almost entirely (decode share < 0.1: chunks >= 2K next to a
+        // few decodes, e.g. 2048@16K + 8 x 16K: 835 vs 783 us, 4096@4K + 8 x 4K: 302 vs
+        // 280 us); with the 64-key pair engine it wins C2 B = 8 (462 vs 493 us) and
+        // 512@4K + 8 x 4K (106 vs 147 us)
         // Decode-only and short-context batches keep the two-CTA kernel: more decode
         // groups per SM amortise the per-item latency (64 x 2K decode-only: 107 vs
         // 126 us; 512@1536 + 64 x 1K: 93 vs 106 us).
         double avg_ctx = 0;
         for (int64_t c : p.decode_ctx) avg_ctx += static_cast<double>(c);
         avg_ctx = p.decode_ctx.empty() ? 0 : avg_ctx / static_cast<double>(p.decode_ctx.size());
-        p.opts.policy = (p.batch.has_prefill && decode_share(p) >= 0.25 && avg_ctx >= 2048) ? POD_POLICY_WARPSPEC
+        p.opts.policy = (p.batch.has_prefill && decode_share(p) >= 0.1 && avg_ctx >= 2048) ? POD_POLICY_WARPSPEC
                                                                                               : POD_POLICY_COMPLEMENT;
     }
     if (p.opts.tile_override) {

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--batches", default="8,64,256")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--max-kv-gb", type=float, default=80.0)
+    ap.add_argument("--policy", type=int, default=8, help="POD_POLICY_* (8 = AUTO)")
     a = ap.parse_args()
     pk = peaks()
     shape = pkg.ModelShape(32, 8, 128, math.sqrt(128))
@@ -44,7 +45,7 @@ def main():
                 off = ctx - chunk
                 batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
                 wl = build_workload(batch, device="cuda")
-                op = PodAttention(batch)
+                op = PodAttention(batch, options=pkg.PlanOptions(policy=a.policy))
                 out = op.alloc_outputs()
                 res = {}
                 for mode in ("fused", "serial", "prefill", "decode"):
