@@ -16,6 +16,9 @@
 // needs only 64 KB of K/V stages, and the decode group gets 144 KB of rings.  The
 // prefill engine runs two 128-row M-blocks over the same K/V tiles (half the K/V
 // traffic per row), ping-ponging the tensor core between the blocks' softmax.
+// Two tile widths share the layout: 32-key tiles with double-buffered S
+// (prefill_item_sm, decode-dominant plans) and 64-key tiles with one S buffer per
+// block (prefill_item_sm64, prefill-dominant plans; RunParams::pf_tn64).
 //
 // Role binding is still SM-aware and dynamic: every SM hosts both roles for as
 // long as both pools have work (the placement the POD scheduler aims for,
