@@ -152,6 +152,7 @@ typedef struct pod_options {
     const pod_tile_config* tile_override; /* non-NULL: use this TileConfig verbatim */
     int32_t precision;       /* POD_PRECISION_* for the prefill P operand            */
     int32_t out_dtype;       /* POD_OUT_*: element type of o_prefill / o_decode (LSE stays fp32) */
+    int32_t prefill_tile_keys; /* warp-specialised pair engine: 0 = by decode share, 32 or 64 forces */
 } pod_options;
 
 enum {

@@ -69,7 +69,7 @@ class pod_options(C.Structure):
     _fields_ = [("policy", C.c_int32), ("tile_mode", C.c_int32), ("ctas_per_sm", C.c_int32),
                 ("virtual_decode", C.c_int32), ("split_wave_cap", C.c_int32),
                 ("decode_splits", C.c_int32), ("tile_override", C.POINTER(pod_tile_config)),
-                ("precision", C.c_int32), ("out_dtype", C.c_int32)]
+                ("precision", C.c_int32), ("out_dtype", C.c_int32), ("prefill_tile_keys", C.c_int32)]
 
 
 class pod_plan_info(C.Structure):

@@ -284,8 +284,9 @@ void lower(pod_plan& p) {
     // batches (C2 B=64 +9 %), so they serve prefill-dominant batches only.
     {
         static const char* tn_env = std::getenv("POD_TN64");  // experiment knob: 0 / 1 forces
-        p.pf_tn64 = warpspec && p.batch.has_prefill &&
-                    (tn_env ? std::atoi(tn_env) != 0 : decode_share(p) < 0.5);
+        const int32_t keys = p.opts.prefill_tile_keys;
+        const bool auto64 = tn_env ? std::atoi(tn_env) != 0 : decode_share(p) < 0.5;
+        p.pf_tn64 = warpspec && p.batch.has_prefill && (keys == 64 || (keys == 0 && auto64));
     }
     // Whole waves (warp-specialised kernel): the decode items are claimed in id order
     // (request-major) by one decode group per SM, so a count that is not a multiple of
@@ -600,6 +601,7 @@ void pod_options_default(pod_options* out) {
     out->tile_override = nullptr;
     out->precision = POD_PRECISION_SPLIT;
     out->out_dtype = POD_OUT_F32;
+    out->prefill_tile_keys = 0;
 }
 
 pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const pod_device* dev,
@@ -624,6 +626,8 @@ pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const p
             pod_options_default(&p->opts);
         if (p->opts.out_dtype < POD_OUT_F32 || p->opts.out_dtype > POD_OUT_F16)
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: out_dtype must be a POD_OUT_* value");
+        if (p->opts.prefill_tile_keys != 0 && p->opts.prefill_tile_keys != 32 && p->opts.prefill_tile_keys != 64)
+            fail(POD_ERR_INVALID_ARGUMENT, "pod_options: prefill_tile_keys must be 0, 32 or 64");
         build(*p);
         p->opts.tile_override = nullptr;  // do not keep caller pointers
         *out = p;

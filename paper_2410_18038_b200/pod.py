@@ -225,6 +225,7 @@ class PlanOptions:
     tile_override: Optional[TileConfig] = None
     precision: int = _abi.POD_PRECISION_SPLIT
     out_dtype: int = _abi.POD_OUT_F32
+    prefill_tile_keys: int = 0  # warp-specialised pair engine: 0 = auto, 32 or 64
 
 
 def _task(t) -> CtaTask:
@@ -248,6 +249,7 @@ class Plan:
                                                               options.decode_splits)
         o.precision = options.precision
         o.out_dtype = options.out_dtype
+        o.prefill_tile_keys = options.prefill_tile_keys
         tc = None
         if options.tile_override is not None:
             tc = options.tile_override._c()

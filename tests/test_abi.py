@@ -60,6 +60,9 @@ def test_plan_info_and_workspace():
     assert 6 * 148 < i.num_decode_ctas <= 7 * 148
     assert i.smem_bytes > 0 and p.workspace_bytes() == i.workspace_bytes > 0
     assert i.smem_bytes + 1024 <= 233472  # one CTA per SM
+    # the pair engine's tile width: 32 keys for this decode-dominant batch, forceable
+    assert i.prefill_tile_keys == 32
+    assert Plan(b, GpuSpec.b200(), PlanOptions(prefill_tile_keys=64)).info().prefill_tile_keys == 64
     # the two-CTA-per-SM POD kernel
     p = Plan(b, GpuSpec.b200(), PlanOptions(policy=_abi.POD_POLICY_COMPLEMENT))
     i = p.info()
@@ -72,6 +75,9 @@ def test_error_codes_cross_the_boundary_as_statuses():
         Plan(HybridBatchSpec(shape=ModelShape(32, 8, 128, 1.0)), GpuSpec.b200())
     with pytest.raises(pkg.InvalidArgument):
         Plan(HybridBatchSpec(decodes=[DecodeSpec(5)], shape=ModelShape(32, 8, 128, 1.0)), GpuSpec(num_sms=0))
+    with pytest.raises(pkg.InvalidArgument):  # pair-engine tile width other than 0 / 32 / 64
+        Plan(HybridBatchSpec(decodes=[DecodeSpec(5)], shape=ModelShape(32, 8, 128, 1.0)), GpuSpec.b200(),
+             PlanOptions(prefill_tile_keys=48))
     with pytest.raises(pkg.InvalidArgument):  # out_dtype outside POD_OUT_*
         Plan(HybridBatchSpec(decodes=[DecodeSpec(5)], shape=ModelShape(32, 8, 128, 1.0)), GpuSpec.b200(),
              PlanOptions(out_dtype=3))

@@ -98,15 +98,23 @@ def test_policies_and_reference_tiles(policy):
         _check(wl, out)
 
 
-# the two POD kernels: two CTAs per SM (COMPLEMENT) and one warp-specialised CTA per SM
-KERNELS = [POD_POLICY_COMPLEMENT, POD_POLICY_WARPSPEC]
+# the POD kernels: two CTAs per SM (COMPLEMENT) and one warp-specialised CTA per SM with
+# its 32-key (double-S) or 64-key (single-S) pair engine
+KERNELS = [POD_POLICY_COMPLEMENT, (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64)]
+
+
+def _kopts(kernel, **kw):
+    """PlanOptions for one entry of KERNELS."""
+    if isinstance(kernel, tuple):
+        return pkg.PlanOptions(policy=kernel[0], prefill_tile_keys=kernel[1], **kw)
+    return pkg.PlanOptions(policy=kernel, **kw)
 
 
 @pytest.mark.parametrize("policy", KERNELS)
 def test_peaky_queries(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=64, offset=900, decode_ctx=[1000, 333])
-    wl, _, out = _run(batch, q_scale=8.0, options=pkg.PlanOptions(policy=policy))
+    wl, _, out = _run(batch, q_scale=8.0, options=_kopts(policy))
     _check(wl, out)
 
 
@@ -115,7 +123,7 @@ def test_fp16_inputs(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=64, offset=100, decode_ctx=[200, 45])
     batch.dtype = POD_DTYPE_FP16
-    wl, _, out = _run(batch, dtype=torch.float16, options=pkg.PlanOptions(policy=policy))
+    wl, _, out = _run(batch, dtype=torch.float16, options=_kopts(policy))
     # the oracle regenerates bf16-rounded values; compare against fp16-rounded ones instead
     s = batch.shape
     G = s.group_size()
@@ -206,7 +214,7 @@ def test_causality_is_bitwise(policy):
     _need_gpu()
     off, chunk, r = 300, 64, 20
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=chunk, offset=off, decode_ctx=[100])
-    wl, op, out1 = _run(batch, options=pkg.PlanOptions(policy=policy))
+    wl, op, out1 = _run(batch, options=_kopts(policy))
     before = out1.o_prefill[: r + 1].clone()
     ix = wl.page_indices.cpu().tolist()
     for t in range(off + r + 1, off + chunk):  # keys no row <= r can see
@@ -226,7 +234,7 @@ def test_split_invariance(policy):
     outs = []
     for ds in (1, 2, 3, 5):
         for cap in (1, 2, 4):
-            _, _, out = _run(batch, options=pkg.PlanOptions(policy=policy, decode_splits=ds, split_wave_cap=cap),
+            _, _, out = _run(batch, options=_kopts(policy, decode_splits=ds, split_wave_cap=cap),
                              wl=wl)
             outs.append(out)
             _check(wl, out, kv_heads=[0, 5])
@@ -272,9 +280,9 @@ def test_16bit_outputs_are_rounded_fp32_outputs(policy, out_dtype):
     wl = build_workload(batch, device="cuda")
     want = {pkg._abi.POD_OUT_BF16: torch.bfloat16, pkg._abi.POD_OUT_F16: torch.float16}[out_dtype]
     for ds, cap in ((1, 1), (3, 4)):
-        kw = dict(policy=policy, decode_splits=ds, split_wave_cap=cap)
-        _, _, ref = _run(batch, options=pkg.PlanOptions(**kw), wl=wl)
-        _, op, out = _run(batch, options=pkg.PlanOptions(out_dtype=out_dtype, **kw), wl=wl)
+        kw = dict(decode_splits=ds, split_wave_cap=cap)
+        _, _, ref = _run(batch, options=_kopts(policy, **kw), wl=wl)
+        _, op, out = _run(batch, options=_kopts(policy, out_dtype=out_dtype, **kw), wl=wl)
         assert out.o_prefill.dtype == want and out.o_decode.dtype == want
         assert torch.equal(out.o_prefill, ref.o_prefill.to(want))
         assert torch.equal(out.o_decode, ref.o_decode.to(want))
@@ -285,7 +293,7 @@ def test_16bit_outputs_are_rounded_fp32_outputs(policy, out_dtype):
 def test_deterministic_and_fused_equals_serial_bitwise(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=256, offset=700, decode_ctx=[900] * 6)
-    wl, op, a = _run(batch, options=pkg.PlanOptions(policy=policy))
+    wl, op, a = _run(batch, options=_kopts(policy))
     b = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
     c = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, mode="serial")
     torch.cuda.synchronize()
@@ -301,7 +309,7 @@ def test_cuda_graph_replay(policy):
 
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=96, offset=100, decode_ctx=[400, 80])
     wl = build_workload(batch, device="cuda")
-    op = PodAttention(batch, options=pkg.PlanOptions(policy=policy))
+    op = PodAttention(batch, options=_kopts(policy))
     out = op.alloc_outputs()
     ref = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
     s = torch.cuda.Stream()
@@ -346,7 +354,7 @@ def test_role_log_scheduler_contract(policy):
 
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=512, offset=1536, decode_ctx=[2048] * 8)
     wl = build_workload(batch, device="cuda")
-    op = PodAttention(batch, options=pkg.PlanOptions(policy=policy))
+    op = PodAttention(batch, options=_kopts(policy))
     log = op.enable_role_log()
     op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
     torch.cuda.synchronize()
