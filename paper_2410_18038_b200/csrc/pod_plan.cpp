@@ -280,12 +280,13 @@ void lower(pod_plan& p) {
     p.decode_splits = std::max<int64_t>(1, splits);
     // Pair-engine tile width (warp-specialised kernel): 64-key tiles with one S buffer
     // per block issue a third fewer MMAs and half the barrier hops per key (prefill
-    // -6 %, prefill-dominant fused C2 B=16/32 -6 %) but slowed the decode-dominant fused
-    // batches (C2 B=64 +9 %), so they serve prefill-dominant batches only.
+    // -6 %, fused -5..11 % up to a decode share of 0.52 in the C5 sweep) but slow the
+    // decode-dominant fused batches (+2..9 % from a share of 0.62, C2 B=64 among them),
+    // so they serve batches with a decode share below 0.57.
     {
         static const char* tn_env = std::getenv("POD_TN64");  // experiment knob: 0 / 1 forces
         const int32_t keys = p.opts.prefill_tile_keys;
-        const bool auto64 = tn_env ? std::atoi(tn_env) != 0 : decode_share(p) < 0.5;
+        const bool auto64 = tn_env ? std::atoi(tn_env) != 0 : decode_share(p) < 0.57;
         p.pf_tn64 = warpspec && p.batch.has_prefill && (keys == 64 || (keys == 0 && auto64));
     }
     // Whole waves (warp-specialised kernel): the decode items are claimed in id order
