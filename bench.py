@@ -467,7 +467,7 @@ def main():
         if caps:
             traffic = json.loads(caps[-1].read_text()).get("dram_bytes_per_launch")
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the CPU baseline runs on rank 0 at N = 1 only
         try:
             # ~cpu_seconds of wall time on all host threads (cpu_seconds x threads core-seconds)
             cus, thr, desc, _ = cpu_reference_sample(hq, hkv, chunk, off, b, ctx,
