@@ -1,7 +1,7 @@
 """Debug driver: runs hybrid-batch cases in subprocesses and prints oracle errors."""
 import json, subprocess, sys, time
 from pathlib import Path
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 
 CASES = {
