@@ -95,7 +95,13 @@ constexpr int kNS = POD_SM_STAGES;                             // K and V ring s
 constexpr uint32_t kStage = kTN * kHeadDim * 2;                // 8 KB: [d-half][32 keys][64 d], SW128
 constexpr uint32_t kOffKs = 0;
 constexpr uint32_t kOffVs = kNS * kStage;
-constexpr uint32_t kOffDec = 2 * kNS * kStage;                 // decode rings (64 KB in)
+#ifndef POD_SM64_KSTAGES
+#define POD_SM64_KSTAGES 2  // K ring stages of the 64-key pair engine (V: 2)
+#endif
+// the prefill rings: 32-key engine K + V (64 KB), or the 64-key engine's K + V stages
+constexpr uint32_t kPfRingBytes = (POD_SM64_KSTAGES + 2) * 16384u > 2 * kNS * kStage ? (POD_SM64_KSTAGES + 2) * 16384u
+                                                                                      : 2 * kNS * kStage;
+constexpr uint32_t kOffDec = kPfRingBytes;                     // decode rings (64 KB in)
 constexpr uint32_t kOffBars = kOffDec + kDW * kDS * kDecStageBytes;
 // prefill mbarriers: 0 qA, 1 qB, 2-5 k_full, 6-9 k_empty, 10-13 v_full, 14-17 v_empty,
 // 18-19 sA[2], 20-21 sB[2], 22-23 pA[2], 24-25 pB[2], 26-27 pvA[2], 28-29 pvB[2]
@@ -518,9 +524,11 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
 // separate empty barriers (K freed after both QKs, V after both PVs).
 namespace sm64 {
 constexpr int kTN = 64;
-constexpr int kNS = 2;
+constexpr int kNS = 2;                      // V stages
+constexpr int kNSK = POD_SM64_KSTAGES;      // K stages
 constexpr uint32_t kStage = kTN * kHeadDim * 2;  // 16 KB: [d-half][64 keys][64 d], SW128
-static_assert(2 * kNS * kStage <= 2 * sm3::kNS * sm3::kStage, "same ring bytes as the 32-key engine");
+static_assert((kNS + kNSK) * kStage <= sm3::kPfRingBytes, "the prefill ring region holds both rings");
+static_assert(kNSK <= sm3::kNS, "K stage barriers");
 __device__ __forceinline__ void load_tile64(const RunParams& p, const CUtensorMap* tm, uint32_t dst, uint32_t bar,
                                             int kt, int kv_head, const PageIds& ids) {
     int ph[4];
@@ -552,6 +560,7 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
     using sm64::kTN;
     using sm64::kNS;
     using sm64::kStage;
+    using sm64::kNSK;
     const PrefillCta job = p.pctas[item];
     const int G = p.group;
     const int rpb = kMBlock / G;
@@ -578,17 +587,17 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
     const int npages = p.page_indptr[1] - pbeg;
     const uint32_t bar0 = sbase + kOffBars;
     auto bar = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
-    const uint32_t sK = sbase + kOffKs, sV = sbase + kOffKs + kNS * kStage;
+    const uint32_t sK = sbase + kOffKs, sV = sbase + kOffKs + kNSK * kStage;
 
     if (warp == kProdWarp) {
         // ------------------------------------------------ TMA producer --
         PageIds ids;
         ids.init(p.page_indices + pbeg, npages, kt0 / 16);
         for (int t = 0; t < nt; ++t) {
-            const int gg = s0.g + t, st = gg % kNS;
-            if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarKE + st), ((gg / kNS) - 1) & 1);
-            ptx::mbar_arrive_expect_tx_elect(bar(kBarKF + st), kStage);
-            sm64::load_tile64(p, tmk, sK + st * kStage, bar(kBarKF + st), kt0 + t * kTN, job.kv_head, ids);
+            const int gg = s0.g + t, st = gg % kNS, sk = gg % kNSK;
+            if (gg >= kNSK) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarKE + sk), ((gg / kNSK) - 1) & 1);
+            ptx::mbar_arrive_expect_tx_elect(bar(kBarKF + sk), kStage);
+            sm64::load_tile64(p, tmk, sK + sk * kStage, bar(kBarKF + sk), kt0 + t * kTN, job.kv_head, ids);
             if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarVE + st), ((gg / kNS) - 1) & 1);
             ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
             sm64::load_tile64(p, tmv, sV + st * kStage, bar(kBarVF + st), kt0 + t * kTN, job.kv_head, ids);
@@ -601,20 +610,20 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             ptx::mbar_wait(bar(0), s0.nq[0] & 1);
             if (hasB) ptx::mbar_wait(bar(1), s0.nq[1] & 1);
             {
-                const int gg = s0.g, st = gg % kNS;
-                ptx::mbar_wait(bar(kBarKF + st), (gg / kNS) & 1);
+                const int gg = s0.g, sk = gg % kNSK;
+                ptx::mbar_wait(bar(kBarKF + sk), (gg / kNSK) & 1);
                 ptx::tc_fence_after();
-                sm64::issue_qk64<kFmt>(tmem + kSA, tmem + kQA, sK + st * kStage);
+                sm64::issue_qk64<kFmt>(tmem + kSA, tmem + kQA, sK + sk * kStage);
                 ptx::umma_commit_elect(bar(kBarS + 0));
                 if (hasB) {
-                    sm64::issue_qk64<kFmt>(tmem + kSB, tmem + kQB, sK + st * kStage);
+                    sm64::issue_qk64<kFmt>(tmem + kSB, tmem + kQB, sK + sk * kStage);
                     ptx::umma_commit_elect(bar(kBarS + 1));
                 }
-                ptx::umma_commit_elect(bar(kBarKE + st));
+                ptx::umma_commit_elect(bar(kBarKE + sk));
             }
             for (int t = 0; t < nt; ++t) {
                 const int gg = s0.g + t, st = gg % kNS;
-                const int g1 = gg + 1, st1 = g1 % kNS;
+                const int g1 = gg + 1, sk1 = g1 % kNSK;
                 const bool more = t + 1 < nt, last = t + 1 == nt;
 #pragma unroll
                 for (int X = 0; X < 2; ++X) {
@@ -628,15 +637,15 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
                     if (last) ptx::umma_commit_elect(bar(kBarPV + X));
                     if (more) {
                         if (X == 0) {
-                            ptx::mbar_wait(bar(kBarKF + st1), (g1 / kNS) & 1);
+                            ptx::mbar_wait(bar(kBarKF + sk1), (g1 / kNSK) & 1);
                             ptx::tc_fence_after();
                         }
-                        sm64::issue_qk64<kFmt>(tmem + (X ? kSB : kSA), tmem + (X ? kQB : kQA), sK + st1 * kStage);
+                        sm64::issue_qk64<kFmt>(tmem + (X ? kSB : kSA), tmem + (X ? kQB : kQA), sK + sk1 * kStage);
                         ptx::umma_commit_elect(bar(kBarS + X));
                     }
                 }
                 ptx::umma_commit_elect(bar(kBarVE + st));          // V(t): both PVs issued above
-                if (more) ptx::umma_commit_elect(bar(kBarKE + st1));  // K(t+1): both QKs
+                if (more) ptx::umma_commit_elect(bar(kBarKE + sk1));  // K(t+1): both QKs
             }
         };
         if (p.p_split != 0)
