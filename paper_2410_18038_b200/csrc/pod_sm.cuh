@@ -95,6 +95,9 @@ constexpr int kNS = POD_SM_STAGES;                             // K and V ring s
 constexpr uint32_t kStage = kTN * kHeadDim * 2;                // 8 KB: [d-half][32 keys][64 d], SW128
 constexpr uint32_t kOffKs = 0;
 constexpr uint32_t kOffVs = kNS * kStage;
+#ifndef POD_SM64_BATCHED_PV
+#define POD_SM64_BATCHED_PV 1  // 64-key engine: the 8 PV MMAs of a tile in one elected asm block
+#endif
 #ifndef POD_SM64_KSTAGES
 #define POD_SM64_KSTAGES 2  // K ring stages of the 64-key pair engine (V: 2)
 #endif
@@ -632,8 +635,15 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
                     ptx::mbar_wait(bar(kBarP + X), n & 1);
                     if (X == 0) ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
                     ptx::tc_fence_after();
-                    prefill_issue_pv<kFmt>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA), sV + st * kStage, t > 0,
-                                           kSplit);
+                    if (POD_SM64_BATCHED_PV) {
+                        constexpr uint32_t idesc_pv = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);
+                        ptx::umma_pv64_elect<kSplit>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA),
+                                                     ptx::sw128_desc(sV + st * kStage, kTN * 128, 1024), idesc_pv,
+                                                     t > 0 ? 1u : 0u);
+                    } else {
+                        prefill_issue_pv<kFmt>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA), sV + st * kStage,
+                                               t > 0, kSplit);
+                    }
                     if (last) ptx::umma_commit_elect(bar(kBarPV + X));
                     if (more) {
                         if (X == 0) {

@@ -322,6 +322,41 @@ __device__ __forceinline__ void umma_pv32_elect(uint32_t d_tmem, uint32_t p_tmem
             "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
             : "memory");
 }
+// O (+)= P V over 64 keys (4 K-steps of 16) in one asm block: P hi in A columns
+// +0/+8/+16/+24, lo (if kSplit) in +32..+56; B MN-major SW128, K-steps 2 KB apart.
+template <bool kSplit>
+__device__ __forceinline__ void umma_pv64_elect(uint32_t d_tmem, uint32_t p_tmem, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+    if constexpr (kSplit)
+        asm volatile(
+            "{\n\t.reg .pred e, acc;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 a1, a2, a3, l0, l1, l2, l3;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 acc, %4, 0;\n\t"
+            "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\t"
+            "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+            "add.u32 l0, %1, 32;\n\tadd.u32 l1, %1, 40;\n\tadd.u32 l2, %1, 48;\n\tadd.u32 l3, %1, 56;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, acc;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l0], %2, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l1], b1, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l2], b2, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l3], b3, %3, 1;\n\t}" ::"r"(d_tmem),
+            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred e, acc;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 a1, a2, a3;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 acc, %4, 0;\n\t"
+            "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\t"
+            "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, acc;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, 1;\n\t}" ::"r"(d_tmem),
+            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+}
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
