@@ -12,7 +12,9 @@
  * Plain C types only; CUDA streams are passed as `void*` (a cudaStream_t).
  * All device pointers are caller-owned; pod_attn_run* allocate nothing, so a
  * (plan, workspace) pair can be captured in a CUDA graph.  One (plan,
- * workspace) pair must not run on two streams at once.
+ * workspace) pair must not run on two streams at once; one plan may be run from
+ * several host threads with distinct workspaces (its tensor-map cache is locked).
+ * Launches go to the calling thread's current CUDA device.
  */
 #ifndef POD_ATTN_H_
 #define POD_ATTN_H_
@@ -119,22 +121,17 @@ enum {
     POD_POLICY_CLAMPED = 2,      /* proportional, rounded to the per-SM slot count     */
     POD_POLICY_COMPLEMENT = 3,   /* bind from the roles resident on the SM:
                                     prefill while < prefill_ratio prefill CTAs run there */
-    POD_POLICY_SLOTS = 4,        /* 2 CTAs/SM, fixed 1:1: the first CTA resident on an SM
-                                    is the prefill slot (all 512 TMEM columns, two-block
-                                    ping-pong engine), the second streams decode */
-    POD_POLICY_BALANCED = 5,     /* bind the role with more estimated remaining slot-time
-                                    (planner per-item costs), so both pools drain together;
-                                    ties go to the role not resident on the SM */
-    POD_POLICY_PARTITION = 6,    /* SM-aware spatial split: prefill_sms SMs (spread evenly
-                                    over the SM ids) bind prefill on both slots, the others
-                                    decode; an exhausted pool switches to the other */
+    /* 4-6 retired (two-block slot engine, greedy balance, spatial partition): all
+       measured slower than COMPLEMENT / WARPSPEC; pod_attn_plan rejects them */
     POD_POLICY_WARPSPEC = 7,     /* one CTA per SM hosting a prefill engine (two 128-row
                                     M-blocks, Q/S/P/O in TMEM) and a decode warp group side
                                     by side; each binds items from its pool at runtime */
     POD_POLICY_AUTO = 8          /* default: WARPSPEC for hybrid batches whose decode share
-                                    of the serial time is >= 0.25 with decode contexts >= 2K
-                                    on average, else COMPLEMENT
-                                    (the plan records the resolved policy) */
+                                    of the serial time (algorithmic work at measured B200
+                                    rates) is >= 0.1 and whose decode contexts average >= 2K,
+                                    else COMPLEMENT; inside WARPSPEC the pair engine runs
+                                    64-key tiles below a decode share of 0.57, 32-key tiles
+                                    above (the plan records the resolved policy and width) */
 };
 
 enum {

@@ -20,8 +20,9 @@ STATUS_NAMES = {
 
 POD_KV_HND, POD_KV_NHD = 0, 1
 POD_DTYPE_BF16, POD_DTYPE_FP16 = 0, 1
-POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT, POD_POLICY_SLOTS, \
-    POD_POLICY_BALANCED, POD_POLICY_PARTITION, POD_POLICY_WARPSPEC, POD_POLICY_AUTO = 0, 1, 2, 3, 4, 5, 6, 7, 8
+POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT = 0, 1, 2, 3
+# 4-6 retired (measured slower; pod_attn_plan rejects them)
+POD_POLICY_WARPSPEC, POD_POLICY_AUTO = 7, 8
 POD_TILE_REFERENCE, POD_TILE_B200 = 0, 1
 POD_PRECISION_SPLIT, POD_PRECISION_FAST = 0, 1
 POD_OUT_F32, POD_OUT_BF16, POD_OUT_F16 = 0, 1, 2

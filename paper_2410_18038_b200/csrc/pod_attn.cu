@@ -83,9 +83,6 @@ constexpr uint32_t kDecWarpBytes = kDecStages * kDecStageBytes;
 constexpr uint32_t kPrefillBytes = kOffV + 2 * kKvStageBytes;
 constexpr uint32_t kOffBar = kPrefillBytes > kDecWarpsK * kDecWarpBytes ? kPrefillBytes
                                                                           : kDecWarpsK * kDecWarpBytes;  // 16 mbarriers
-// engine 2 keeps Q in TMEM: K/V stages only
-constexpr uint32_t kOffK2 = 0;
-constexpr uint32_t kOffV2 = kOffK2 + 2 * kKvStageBytes;
 constexpr uint32_t kOffTmemSlot = kOffBar + 128;
 constexpr uint32_t kOffDecBar = kOffBar + 160;              // 4 warps x kDecStages decode mbarriers
 constexpr uint32_t kOffRole = kOffTmemSlot + 16;          // role[0..3]
@@ -132,15 +129,11 @@ struct RunParams {
     int32_t dec_split_base;  // splits of requests below dec_tail_start
     int32_t dec_tail_start;
     int32_t policy;
-    float w_prefill;  // POD_POLICY_BALANCED: estimated slot-us per prefill / decode item
-    float w_decode;
     int32_t p_split;  // prefill P as bf16 hi + lo (two PV MMAs)
     int32_t pf_tn64;  // warp-specialised kernel: 64-key single-S pair engine (prefill-dominant plans)
-    int32_t grid_per_sm;   // resident CTAs per SM of the persistent launch (1 or 2)
-    int32_t trace;         // debug: per-tile cycle stamps of CTA 0's first prefill item after the role log
-    int32_t trace_mode;    // debug: 2 = serialise MMA issue with completion (execution latency probe)
-    int32_t prefill_sms;   // POD_POLICY_PARTITION: SMs that bind prefill first
-    int32_t num_sms;
+    const int32_t* dec_nsplit;  // KV splits of each decode request (min(splits, ctx), pod_plan.cpp)
+    int32_t trace;         // debug builds (POD_TRACE_STAMPS): per-tile cycle stamps after the role log
+    int32_t trace_mode;    // debug builds: 2 = serialise MMA issue with completion (execution latency probe)
     int64_t num_pages;
     float sl2;  // log2(e) / scale  (scale is the reference's divisor)
 };
@@ -628,324 +621,6 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
     }
 }
 
-// ================================================== prefill engine (2) ===
-// The prefill-slot CTA of an SM owns all 512 TMEM columns and runs two M-blocks
-// (A, B: 2 x 128 packed rows) in ping-pong over the same K/V tiles:
-//   TMEM  Q_A [0,64)  Q_B [64,128)  S_A [128,192)  S_B [192,256)  O_A [256,384)  O_B [384,512)
-// Q lives in TMEM (loaded once per item by the softmax threads), so both QK^T
-// and PV are TS-MMAs and shared memory only streams K/V (read once for 256 rows).
-// While the softmax warps work on block B the tensor core runs PV_A + QK_A of the
-// next tile, and vice versa.
-constexpr uint32_t kT2QA = 0, kT2QB = 64, kT2SA = 128, kT2SB = 192, kT2OA = 256, kT2OB = 384;
-constexpr uint32_t kTmemCols2 = 512;
-
-struct Prefill2State {
-    int g = 0;      // KV tiles issued (K/V stage = g & 1, phase = (g >> 1) & 1)
-    int na = 0;     // A-block tiles (s_full_A / p_full_A / pv_A phases)
-    int nb = 0;     // B-block tiles
-    int pairs = 0;  // block pairs (q_full phases)
-};
-
-template <int kFmt>
-__device__ __forceinline__ void issue_qk_ts(uint32_t tmem_s, uint32_t tmem_q, uint32_t sK) {
-    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kKvTile, 0);
-#pragma unroll
-    for (int kk = 0; kk < kHeadDim / 16; ++kk) {
-        const uint64_t b = ptx::sw128_desc(sK + (kk >> 2) * (kKvTile * 128) + (kk & 3) * 32u, 16, 1024);
-        ptx::umma_f16_ts_elect(tmem_s, tmem_q + kk * 8, b, idesc, kk > 0 ? 1u : 0u);
-    }
-}
-
-template <int kFmt>
-__device__ void prefill_item2(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv, int cta_id,
-                              uint8_t* smem, uint32_t tmem, Prefill2State& ps) {
-    const PrefillCta job = p.pctas[cta_id];
-    const int tid = threadIdx.x;
-    const int warp = uniform_warp(), lane = tid & 31;
-    const uint32_t sbase = ptx::smem_u32(smem);
-    const uint32_t sK = sbase + kOffK2, sV = sbase + kOffV2;
-    const uint32_t bar0 = sbase + kOffBar;
-    const uint32_t b_qfull = bar0 + 0;
-    const uint32_t b_kfull = bar0 + 16, b_kempty = bar0 + 32;  // [2]
-    const uint32_t b_vfull = bar0 + 48, b_vempty = bar0 + 64;  // [2]
-    const uint32_t b_sfull = bar0 + 80;                        // [A, B]
-    const uint32_t b_pfull = bar0 + 96;                        // [A, B], 4 arrivals
-    const uint32_t b_pv = bar0 + 112;                          // [A, B]
-    const int G = p.group;
-    const int rpb = kMBlock / G;
-    const int nblocks = (job.rows + rpb - 1) / rpb;
-    const int npairs = (nblocks + 1) / 2;
-    const int pbeg = p.page_indptr[0];
-    const int npages = p.page_indptr[1] - pbeg;
-    const Prefill2State s0 = ps;
-    // all threads advance the shared counters identically
-    for (int pr = 0; pr < npairs; ++pr) {
-        const bool hasB = 2 * pr + 1 < nblocks;
-        const BlockRange ra = prefill_block(p, job, 2 * pr);
-        const int nt = hasB ? prefill_block(p, job, 2 * pr + 1).nt : ra.nt;
-        if (nt == 0) continue;
-        ps.g += nt;
-        ps.na += nt;
-        ps.nb += hasB ? nt : 0;
-        ps.pairs += 1;
-    }
-
-    if (warp == 4) {
-        // ------------------------------------------------ TMA producer --
-        {  // warp-uniform; single-thread instructions are elect-predicated
-            int g = s0.g;
-            for (int pr = 0; pr < npairs; ++pr) {
-                const bool hasB = 2 * pr + 1 < nblocks;
-                const BlockRange ra = prefill_block(p, job, 2 * pr);
-                const int nt = hasB ? prefill_block(p, job, 2 * pr + 1).nt : ra.nt;
-                PageIds pk, pvi;
-                pk.init(p.page_indices + pbeg, npages, ra.kt0 / 16);
-                pvi.init(p.page_indices + pbeg, npages, ra.kt0 / 16);
-                for (int t = 0; t <= nt && nt > 0; ++t) {
-                    if (t < nt) {
-                        const int gg = g + t, st = gg & 1;
-                        if (gg >= 2) ptx::mbar_wait_relaxed<>(b_kempty + 8 * st, ((gg >> 1) - 1) & 1);
-                        ptx::mbar_arrive_expect_tx_elect(b_kfull + 8 * st, kKvStageBytes);
-                        prefill_load_kv_tile(p, tmk, sK + st * kKvStageBytes, b_kfull + 8 * st,
-                                             ra.kt0 + t * kKvTile, job.kv_head, pk);
-                    }
-                    if (t > 0) {
-                        const int gg = g + t - 1, st = gg & 1;
-                        if (gg >= 2) ptx::mbar_wait_relaxed<>(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
-                        ptx::mbar_arrive_expect_tx_elect(b_vfull + 8 * st, kKvStageBytes);
-                        prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
-                                             ra.kt0 + (t - 1) * kKvTile, job.kv_head, pvi);
-                    }
-                }
-                g += nt;
-            }
-        }
-    } else if (warp == 5) {
-        // -------------------------------------------------- MMA issuer --
-        {  // warp-uniform; single-thread instructions are elect-predicated
-            int g = s0.g, na = s0.na, nb = s0.nb, pq = s0.pairs;
-            for (int pr = 0; pr < npairs; ++pr) {
-                const bool hasB = 2 * pr + 1 < nblocks;
-                const BlockRange ra = prefill_block(p, job, 2 * pr);
-                const int nt = hasB ? prefill_block(p, job, 2 * pr + 1).nt : ra.nt;
-                if (nt == 0) continue;
-                ptx::mbar_wait(b_qfull, pq & 1);
-                {  // tile 0: QK_A, QK_B
-                    const int st = g & 1;
-                    ptx::mbar_wait(b_kfull + 8 * st, (g >> 1) & 1);
-                    ptx::tc_fence_after();
-                    issue_qk_ts<kFmt>(tmem + kT2SA, tmem + kT2QA, sK + st * kKvStageBytes);
-                    ptx::umma_commit_elect(b_sfull);
-                    if (hasB) {
-                        issue_qk_ts<kFmt>(tmem + kT2SB, tmem + kT2QB, sK + st * kKvStageBytes);
-                        ptx::umma_commit_elect(b_sfull + 8);
-                    }
-                    ptx::umma_commit_elect(b_kempty + 8 * st);
-                }
-                for (int t = 0; t < nt; ++t) {
-                    const int gg = g + t, st = gg & 1, s1 = (gg + 1) & 1;
-                    const bool more = t + 1 < nt;
-                    // block A: PV_A(t), then QK_A(t+1) into the same S/P columns (in-order pipe)
-                    ptx::mbar_wait(b_pfull, (na + t) & 1);
-                    ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
-                    ptx::tc_fence_after();
-                    prefill_issue_pv<kFmt>(tmem + kT2OA, tmem + kT2SA, sV + st * kKvStageBytes, t > 0,
-                                           p.p_split != 0);
-                    ptx::umma_commit_elect(b_pv);
-                    if (more) {
-                        ptx::mbar_wait(b_kfull + 8 * s1, ((gg + 1) >> 1) & 1);
-                        ptx::tc_fence_after();
-                        issue_qk_ts<kFmt>(tmem + kT2SA, tmem + kT2QA, sK + s1 * kKvStageBytes);
-                        ptx::umma_commit_elect(b_sfull);
-                    }
-                    if (hasB) {
-                        ptx::mbar_wait(b_pfull + 8, (nb + t) & 1);
-                        ptx::tc_fence_after();
-                        prefill_issue_pv<kFmt>(tmem + kT2OB, tmem + kT2SB, sV + st * kKvStageBytes, t > 0,
-                                               p.p_split != 0);
-                        ptx::umma_commit_elect(b_pv + 8);
-                        if (more) {
-                            issue_qk_ts<kFmt>(tmem + kT2SB, tmem + kT2QB, sK + s1 * kKvStageBytes);
-                            ptx::umma_commit_elect(b_sfull + 8);
-                        }
-                    }
-                    ptx::umma_commit_elect(b_vempty + 8 * st);
-                    if (more) ptx::umma_commit_elect(b_kempty + 8 * s1);
-                }
-                g += nt;
-                na += nt;
-                nb += hasB ? nt : 0;
-                ++pq;
-            }
-        }
-    } else {
-        // ------------------------------------------ softmax (128 threads) --
-        const int m = tid;  // TMEM lane == M row of both blocks
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-        int na = s0.na, nb = s0.nb;
-        const uint16_t* qsrc = static_cast<const uint16_t*>(p.q_prefill);
-        for (int pr = 0; pr < npairs; ++pr) {
-            const bool hasB = 2 * pr + 1 < nblocks;
-            const BlockRange br[2] = {prefill_block(p, job, 2 * pr),
-                                      hasB ? prefill_block(p, job, 2 * pr + 1) : prefill_block(p, job, 2 * pr)};
-            const int nt = hasB ? br[1].nt : br[0].nt;
-            const int nblk = hasB ? 2 : 1;
-            int my_r[2], vis[2];
-            bool row_ok[2];
-            ORow orow[2];
-            float* lrow[2];
-            const int qhead = job.kv_head * G + m % G;
-#pragma unroll
-            for (int bi = 0; bi < 2; ++bi) {
-                my_r[bi] = br[bi].r0 + m / G;
-                row_ok[bi] = bi < nblk && (m / G) < br[bi].nrows;
-                vis[bi] = p.offset + my_r[bi];
-                if (job.n_splits == 1) {
-                    orow[bi] = out_row(p.o_prefill, (static_cast<size_t>(my_r[bi]) * p.hq + qhead) * kHeadDim, p.out_fmt);
-                    lrow[bi] = p.lse_prefill + static_cast<size_t>(my_r[bi]) * p.hq + qhead;
-                } else {
-                    const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r[bi]) * p.hq + qhead;
-                    orow[bi] = out_row(p.ppart_o, row * kHeadDim, 0);
-                    lrow[bi] = p.ppart_lse + row;
-                }
-            }
-            if (nt == 0) {
-#pragma unroll
-                for (int bi = 0; bi < 2; ++bi)
-                    if (row_ok[bi]) {
-                        for (int c = 0; c < kHeadDim; c += 4) store4(orow[bi], c, make_float4(0.f, 0.f, 0.f, 0.f));
-                        *lrow[bi] = -INFINITY;
-                    }
-                continue;
-            }
-            // ---- Q rows -> TMEM (A operand of QK^T), zero rows past the chunk
-#pragma unroll
-            for (int bi = 0; bi < 2; ++bi) {
-                if (bi >= nblk) break;
-                const uint32_t* src = reinterpret_cast<const uint32_t*>(
-                    qsrc + (static_cast<size_t>(my_r[bi]) * p.hq + qhead) * kHeadDim);
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    float qv[32];
-#pragma unroll
-                    for (int c = 0; c < 32; c += 4) {
-                        const uint4 v = row_ok[bi] ? __ldg(reinterpret_cast<const uint4*>(src + 32 * hf + c))
-                                                   : make_uint4(0u, 0u, 0u, 0u);
-                        qv[c] = __uint_as_float(v.x);
-                        qv[c + 1] = __uint_as_float(v.y);
-                        qv[c + 2] = __uint_as_float(v.z);
-                        qv[c + 3] = __uint_as_float(v.w);
-                    }
-                    ptx::tmem_st32(lane_base + (bi ? kT2QB : kT2QA) + 32 * hf, qv);
-                }
-            }
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(b_qfull);
-            float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-            for (int t = 0; t < nt; ++t) {
-                const int kb = br[0].kt0 + t * kKvTile;
-#pragma unroll 1
-                for (int bi = 0; bi < nblk; ++bi) {
-                    const int n = bi ? nb + t : na + t;  // this block's tile count (barrier phases)
-                    const uint32_t s_addr = lane_base + (bi ? kT2SB : kT2SA);
-                    const uint32_t o_addr = lane_base + (bi ? kT2OB : kT2OA);
-                    ptx::mbar_wait(b_sfull + 8 * bi, n & 1);
-                    ptx::tc_fence_after();
-                    float s[kKvTile];
-                    ptx::tmem_ld32(s_addr, *reinterpret_cast<float(*)[32]>(&s[0]));
-                    ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
-                    ptx::tmem_wait_ld();
-                    const int lo = max(job.kv_begin - kb, 0);
-                    const int hi = row_ok[bi] ? min(min(job.kv_end, vis[bi] + 1) - kb, kKvTile) : 0;
-                    if (!__all_sync(0xffffffffu, lo == 0 && hi == kKvTile)) {
-#pragma unroll
-                        for (int c = 0; c < kKvTile; ++c)
-                            if (c < lo || c >= hi) s[c] = -INFINITY;
-                    }
-                    float tmax = s[0];
-#pragma unroll
-                    for (int c = 1; c < kKvTile; c += 2) tmax = fmaxf(tmax, fmaxf(s[c], s[min(c + 1, kKvTile - 1)]));
-                    const float mr = m_run[bi];
-                    const float m_new = fmaxf(mr, tmax * p.sl2);
-                    const bool need = m_new > mr + 8.f;
-                    const float m_use = need ? m_new : mr;
-                    const float factor = need ? ptx::ex2(mr - m_new) : 1.f;
-                    l_run[bi] *= factor;
-                    m_run[bi] = m_use;
-                    float2 lsum2 = make_float2(0.f, 0.f);
-                    const float neg_m = -m_use;
-                    const bool live = m_use != -INFINITY;
-#pragma unroll
-                    for (int hf = 0; hf < 2; ++hf) {
-                        uint32_t hiv[16], lov[16];
-#pragma unroll
-                        for (int c = 0; c < 32; c += 2) {
-                            const float p0 = live ? ptx::ex2(fmaf(s[32 * hf + c], p.sl2, neg_m)) : 0.f;
-                            const float p1 = live ? ptx::ex2(fmaf(s[32 * hf + c + 1], p.sl2, neg_m)) : 0.f;
-                            lsum2 = fadd2(lsum2, make_float2(p0, p1));
-                            hiv[c / 2] = pack2<kFmt>(p0, p1);
-                            if (p.p_split) {
-                                const float2 hv = unpack2<kFmt>(hiv[c / 2]);
-                                lov[c / 2] = pack2<kFmt>(p0 - hv.x, p1 - hv.y);
-                            }
-                        }
-                        ptx::tmem_st16(s_addr + 16 * hf, hiv);
-                        if (p.p_split) ptx::tmem_st16(s_addr + 32 + 16 * hf, lov);
-                    }
-                    l_run[bi] += lsum2.x + lsum2.y;
-                    if (t > 0) {  // observe PV(t-1) of this block; rescale its O when the max moved
-                        ptx::mbar_wait(b_pv + 8 * bi, (n - 1) & 1);
-                        ptx::tc_fence_after();
-                        if (__any_sync(0xffffffffu, need)) {
-#pragma unroll 1
-                            for (int ch = 0; ch < kHeadDim / 32; ++ch) {
-                                float o[32];
-                                ptx::tmem_ld32(o_addr + ch * 32, o);
-                                ptx::tmem_wait_ld();
-#pragma unroll
-                                for (int c = 0; c < 32; ++c) o[c] *= factor;
-                                ptx::tmem_st32(o_addr + ch * 32, o);
-                            }
-                        }
-                    }
-                    ptx::tmem_wait_st();
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(b_pfull + 8 * bi);
-                }
-            }
-            // ------------------------------------------------- epilogue --
-#pragma unroll 1
-            for (int bi = 0; bi < nblk; ++bi) {
-                const int n = (bi ? nb : na) + nt - 1;
-                ptx::mbar_wait(b_pv + 8 * bi, n & 1);
-                ptx::tc_fence_after();
-                const uint32_t o_addr = lane_base + (bi ? kT2OB : kT2OA);
-                const float inv = l_run[bi] > 0.f ? 1.f / l_run[bi] : 0.f;
-#pragma unroll 1
-                for (int ch = 0; ch < kHeadDim / 32; ++ch) {
-                    float o[32];
-                    ptx::tmem_ld32(o_addr + ch * 32, o);
-                    ptx::tmem_wait_ld();
-                    if (row_ok[bi]) {
-#pragma unroll
-                        for (int c = 0; c < 32; c += 4)
-                            store4(orow[bi], ch * 32 + c,
-                                   make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
-                    }
-                }
-                if (row_ok[bi])
-                    *lrow[bi] = l_run[bi] > 0.f ? (m_run[bi] + ptx::lg2(l_run[bi])) * kLn2 : -INFINITY;
-            }
-            ptx::tc_fence_before();
-            na += nt;
-            nb += hasB ? nt : 0;
-        }
-    }
-}
-
 // ============================================================= decode ===
 static_assert(kDecWarpsK * kDecWarpBytes <= kOffBar, "decode rings must fit below the barrier block");
 
@@ -1314,7 +989,7 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
         out_o = out_row(p.o_prefill, row * kHeadDim, p.out_fmt);
         out_l = p.lse_prefill + row;
     } else {
-        n = r >= p.dec_tail_start ? p.decode_splits : p.dec_split_base;  // per request (whole waves)
+        n = p.dec_nsplit[r];  // this request's own split count (min(splits, ctx), whole waves)
         if (n <= 1) return;
         const size_t row = static_cast<size_t>(r) * p.decode_splits * p.hq + qh;
         po = p.dpart_o + row * kHeadDim;
@@ -1350,26 +1025,7 @@ __device__ __forceinline__ int2 claim_item(const RunParams& p, uint32_t sm, int3
     const int ratio = p.prefill_ratio + p.decode_ratio;
     const uint32_t raw = atomicAdd(&p.ctr->sm_ctr[sm], 1u);
     int op;
-    if (p.policy == POD_POLICY_BALANCED) {
-        // remaining work of each pool (racy snapshot of the claim counters)
-        const float rp = static_cast<float>(p.num_pctas - min(p.num_pctas, static_cast<int>(
-                             *reinterpret_cast<volatile uint32_t*>(&p.ctr->cta_assign[0])))) * p.w_prefill;
-        const float rd = static_cast<float>(p.num_dctas - min(p.num_dctas, static_cast<int>(
-                             *reinterpret_cast<volatile uint32_t*>(&p.ctr->cta_assign[1])))) * p.w_decode;
-        if (rp > 1.25f * rd)
-            op = 0;
-        else if (rd > 1.25f * rp)
-            op = 1;
-        else  // comparable: complement what is resident on this SM
-            op = *reinterpret_cast<volatile uint32_t*>(&p.ctr->running_prefill[sm]) == 0u ? 0 : 1;
-        if (op == 0) atomicAdd(&p.ctr->running_prefill[sm], 1u);
-    } else if (p.policy == POD_POLICY_PARTITION) {
-        // spatial split spread evenly over the SM ids: SM s binds prefill iff
-        // floor((s + 1) x / n) > floor(s x / n)
-        // (fraction prefill_sms / num_sms applied over the %smid range, which may have gaps)
-        const float f = static_cast<float>(p.prefill_sms) / static_cast<float>(max(p.num_sms, 1));
-        op = floorf((sm + 1) * f) > floorf(sm * f) ? 0 : 1;
-    } else if (p.policy == POD_POLICY_COMPLEMENT) {
+    if (p.policy == POD_POLICY_COMPLEMENT) {
         // bind from what is resident on this SM: prefill while fewer than
         // prefill_ratio prefill items run here, decode otherwise
         const uint32_t resident = atomicAdd(&p.ctr->running_prefill[sm], 1u);
@@ -1381,13 +1037,12 @@ __device__ __forceinline__ int2 claim_item(const RunParams& p, uint32_t sm, int3
     }
     int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
     if (id >= (op == 0 ? p.num_pctas : p.num_dctas)) {
-        if ((p.policy == POD_POLICY_COMPLEMENT || p.policy == POD_POLICY_BALANCED) && op == 0)
-            atomicSub(&p.ctr->running_prefill[sm], 1u);
+        if (p.policy == POD_POLICY_COMPLEMENT && op == 0) atomicSub(&p.ctr->running_prefill[sm], 1u);
         op ^= 1;
         id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
         if (id >= (op == 0 ? p.num_pctas : p.num_dctas))
             op = -1;
-        else if ((p.policy == POD_POLICY_COMPLEMENT || p.policy == POD_POLICY_BALANCED) && op == 0)
+        else if (p.policy == POD_POLICY_COMPLEMENT && op == 0)
             atomicAdd(&p.ctr->running_prefill[sm], 1u);
     }
     *log_slot_out = -1;
@@ -1414,7 +1069,7 @@ __device__ __forceinline__ int2 claim_item(const RunParams& p, uint32_t sm, int3
 // of the serial comparator.  Persistence matters on sm_100: kernels that use
 // tcgen05 get one new CTA dispatched only into an idle SM, so a classic
 // CTA-per-task grid would lose the second slot after the first wave.
-template <int G, int kFmt, bool kSlots>
+template <int G, int kFmt>
 __global__ void __launch_bounds__(kThreads, 2)
     pod_fused_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmq,
                      const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
@@ -1425,27 +1080,19 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int tid = threadIdx.x, warp = uniform_warp(), lane = tid & 31;
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t sm = ptx::smid();
-    constexpr bool slots = kSlots;  // POD_POLICY_SLOTS (engine 2) vs ticket policies (engine 1)
     if (tid == 0) {
         if (sbase & 1023u) __trap();  // SW128 atoms need a 1024-aligned base
-        // p_full (12, 13) get one arrival per softmax warp; so does engine 2's q_full (0),
-        // which engine 1 fills by TMA (expect_tx, one arrival)
-        for (int i = 0; i < 16; ++i)
-            ptx::mbar_init(sbase + kOffBar + 8 * i, (i == 12 || i == 13 || (i == 0 && slots)) ? kPrefillWarps : 1);
+        // p_full (12, 13) get one arrival per softmax warp; q_full (0) is filled by TMA
+        // (expect_tx, one arrival)
+        for (int i = 0; i < 16; ++i) ptx::mbar_init(sbase + kOffBar + 8 * i, (i == 12 || i == 13) ? kPrefillWarps : 1);
         for (int i = 0; i < kDecWarpsK * kDecStages; ++i) ptx::mbar_init(sbase + kOffDecBar + 8 * i, 1);
         ptx::fence_mbar_init();
-        // POD_POLICY_SLOTS: the first CTA resident on this SM takes the prefill slot
-        role[3] = slots ? static_cast<int>(atomicAdd(&p.ctr->sm_slot[sm], 1u)) : 0;
     }
-    __syncthreads();
-    const int my_slot = role[3];
-    const bool prefill_slot = !slots || my_slot == 0;
-    // TMEM: the slots policy gives the prefill slot the whole SM (512 columns);
-    // ticket policies give every CTA 256.  Every CTA that allocates relinquishes
-    // its permit at once: on sm_100 a second CTA of a tcgen05 kernel is only
-    // co-scheduled on an SM after the resident one has relinquished.
-    const uint32_t ncols = slots ? (p.num_pctas > 0 ? kTmemCols2 : 32u) : kTmemCols;
-    if (warp == 0 && prefill_slot) {
+    // TMEM: every CTA holds 256 columns.  Every CTA that allocates relinquishes its
+    // permit at once: on sm_100 a second CTA of a tcgen05 kernel is only co-scheduled
+    // on an SM after the resident one has relinquished.
+    const uint32_t ncols = kTmemCols;
+    if (warp == 0) {
         ptx::tmem_alloc(ptx::smem_u32(tmem_slot), ncols);
         ptx::tmem_relinquish();
     }
@@ -1459,38 +1106,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = prefill_slot ? *tmem_slot : 0u;
+    const uint32_t tmem = *tmem_slot;
     PrefillState ps;
-    Prefill2State ps2;
     int dpos = 0;
     while (true) {
         if (tid == 0) {
             int32_t slot = -1;
-            int2 w;
-            if constexpr (kSlots) {
-                // prefill slot: prefill items first, then decode; decode slot: decode only
-                int op = prefill_slot ? 0 : 1;
-                int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[op], 1u));
-                if (op == 0 && id >= p.num_pctas) {
-                    op = 1;
-                    id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[1], 1u));
-                }
-                if (id >= (op == 0 ? p.num_pctas : p.num_dctas)) op = -1;
-                w = make_int2(op, id);
-                if (p.role_log && op >= 0) {
-                    slot = static_cast<int32_t>(atomicAdd(&p.ctr->arrival, 1u));
-                    int32_t* rec = p.role_log + 8 * slot;
-                    rec[0] = static_cast<int32_t>(sm);
-                    rec[1] = my_slot;
-                    rec[2] = op;
-                    rec[3] = id;
-                    rec[4] = slot;
-                    rec[5] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
-                    rec[7] = static_cast<int32_t>(blockIdx.x);
-                }
-            } else {
-                w = claim_item(p, sm, &slot);
-            }
+            const int2 w = claim_item(p, sm, &slot);
             role[0] = w.x;
             role[1] = w.y;
             role[2] = slot;
@@ -1500,10 +1122,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncthreads();  // role[] is rewritten by the next claim
         if (op < 0) break;
         if (op == 0) {
-            if constexpr (kSlots)
-                prefill_item2<kFmt>(p, &tmk, &tmv, id, smem, tmem, ps2);
-            else
-                prefill_item<kFmt>(p, &tmq, &tmk, &tmv, id, smem, tmem, ps);
+            prefill_item<kFmt>(p, &tmq, &tmk, &tmv, id, smem, tmem, ps);
         } else {
             if (warp < kDecWarpsK)
                 decode_item<G, kFmt, kDecWarpsK, kDecStages>(p, &tdk, &tdv, id, warp, sbase, sbase + kOffDecBar,
@@ -1513,12 +1132,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncthreads();
         ptx::tc_fence_after();
         if (tid == 0) {
-            if ((p.policy == POD_POLICY_COMPLEMENT || p.policy == POD_POLICY_BALANCED) && op == 0)
-                atomicSub(&p.ctr->running_prefill[sm], 1u);
+            if (p.policy == POD_POLICY_COMPLEMENT && op == 0) atomicSub(&p.ctr->running_prefill[sm], 1u);
             if (slot >= 0) p.role_log[8 * slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
         }
     }
-    if (warp == 0 && prefill_slot) {
+    if (warp == 0) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, ncols);
     }
@@ -1531,7 +1149,6 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (uint32_t i = 0; i < n; ++i) {
                 p.ctr->sm_ctr[i] = 0;
                 p.ctr->running_prefill[i] = 0;
-                p.ctr->sm_slot[i] = 0;
             }
             p.ctr->cta_assign[0] = 0;
             p.ctr->cta_assign[1] = 0;
@@ -1732,23 +1349,18 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.dec_split_base = static_cast<int32_t>(plan->dec_split_base);
     p.dec_tail_start = static_cast<int32_t>(plan->dec_tail_start);
     p.policy = plan->opts.policy;
-    p.w_prefill = static_cast<float>(plan->w_prefill);
-    p.w_decode = static_cast<float>(plan->w_decode);
     p.p_split = plan->opts.precision == POD_PRECISION_SPLIT ? 1 : 0;
     p.pf_tn64 = plan->pf_tn64 ? 1 : 0;
     p.out_fmt = plan->opts.out_dtype;
-    {
-        static const char* grid_env = std::getenv("POD_GRID_PER_SM");  // experiment knob
-        p.grid_per_sm = grid_env ? std::max(1, std::min(2, std::atoi(grid_env))) : 2;
-    }
-    {
-        static const char* trace_env = std::getenv("POD_TRACE");  // debug knob
+    p.dec_nsplit = reinterpret_cast<const int32_t*>(ws + plan->ws.off_dec_nsplit);
+#if POD_TRACE_STAMPS
+    {  // debug builds only: POD_TRACE=1 (stamps) / 2 (serialised MMA issue) after the role log
+        static const char* trace_env = std::getenv("POD_TRACE");
         const int t = trace_env ? std::atoi(trace_env) : 0;
         p.trace = t ? static_cast<int32_t>(8 * (plan->pctas.size() + plan->dctas.size())) : 0;
         p.trace_mode = t;
     }
-    p.prefill_sms = plan->prefill_sms;
-    p.num_sms = plan->dev.num_sms;
+#endif
     p.num_pages = num_pages;
     p.sl2 = static_cast<float>(1.4426950408889634 / plan->shape.scale);
     return p;
@@ -1771,36 +1383,45 @@ pod_status check_supported(const pod_plan* plan) {
     return POD_OK;
 }
 
+// cudaFuncSetAttribute is per device context: set the large dynamic-smem limits once
+// per (kernel instantiation, device), thread-safely, and report a failure.
+template <int G, int kFmt>
+pod_status set_kernel_attributes() {
+    constexpr int kMaxDev = 64;
+    static std::once_flag once[kMaxDev];
+    static cudaError_t err[kMaxDev];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxDev) {
+        set_last_error("device ordinal out of range");
+        return POD_ERR_CUDA;
+    }
+    std::call_once(once[dev], [&] {
+        cudaError_t r = cudaFuncSetAttribute(pod_fused_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kSmemBytes);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(pod_sm_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3::kSmem);
+        err[dev] = r;
+    });
+    if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    return POD_OK;
+}
+
 template <int G, int kFmt>
 pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const Maps& maps, cudaStream_t s) {
     // mode 0 fused, 1 serial, 2 prefill only, 3 decode only
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaFuncSetAttribute(pod_fused_kernel<G, kFmt, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        cudaFuncSetAttribute(pod_fused_kernel<G, kFmt, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        attr_done = true;
-    }
+    pod_status st = set_kernel_attributes<G, kFmt>();
+    if (st != POD_OK) return st;
     const int nsm = plan->dev.num_sms;
-    static bool attr_sm = false;
-    if (!attr_sm) {
-        cudaFuncSetAttribute(pod_sm_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3::kSmem);
-        attr_sm = true;
-    }
     auto launch = [&](const RunParams& q) {
         const int items = q.num_pctas + q.num_dctas;
         if (items <= 0) return;
         if (q.policy == POD_POLICY_WARPSPEC) {
             pod_sm_kernel<G, kFmt><<<nsm, sm3::kThreads, sm3::kSmem, s>>>(q, maps.k, maps.v, maps.dk, maps.dv);
-        } else if (q.policy == POD_POLICY_SLOTS) {
-            const int grid = std::min(items, q.num_dctas == 0 ? nsm : 2 * nsm);  // prefill slots only / 2 per SM
-            pod_fused_kernel<G, kFmt, true><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk,
-                                                                               maps.dv);
         } else {
-            int grid = std::min(items, q.grid_per_sm * nsm);  // persistent: 2 resident CTAs per SM
-            static const char* grid_ctas = std::getenv("POD_GRID_CTAS");  // experiment knob
-            if (grid_ctas) grid = std::min(grid, std::max(1, std::atoi(grid_ctas)));
-            pod_fused_kernel<G, kFmt, false><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk,
-                                                                                maps.dv);
+            const int grid = std::min(items, 2 * nsm);  // persistent: 2 resident CTAs per SM
+            pod_fused_kernel<G, kFmt><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk, maps.dv);
         }
     };
     if (mode == 0) {
@@ -1863,18 +1484,23 @@ pod_status run_mode(const pod_plan* plan, int mode, const void* q_prefill, const
     if (need_d && (!q_decode || !o_decode || !lse_decode)) return POD_ERR_INVALID_ARGUMENT;
     Maps maps;
     static_assert(sizeof(Maps) == sizeof(plan->map_blob), "map cache size");
-    pod_plan* mp = const_cast<pod_plan*>(plan);  // the cache is not part of the plan's semantics
-    if (mp->map_key[0] == q_prefill && mp->map_key[1] == k_pool && mp->map_key[2] == v_pool &&
-        mp->map_pages == num_pages) {
-        std::memcpy(&maps, mp->map_blob, sizeof(Maps));
-    } else {
-        st = make_maps(plan, q_prefill, k_pool, v_pool, num_pages, &maps);
-        if (st != POD_OK) return st;
-        std::memcpy(mp->map_blob, &maps, sizeof(Maps));
-        mp->map_key[0] = q_prefill;
-        mp->map_key[1] = k_pool;
-        mp->map_key[2] = v_pool;
-        mp->map_pages = num_pages;
+    {
+        // Tensor-map cache (host launch cost): the plan is const for callers, the cache
+        // is not part of its semantics; a mutex keeps concurrent runs of one plan safe.
+        pod_plan* mp = const_cast<pod_plan*>(plan);
+        std::lock_guard<std::mutex> lock(mp->map_mu);
+        if (mp->map_key[0] == q_prefill && mp->map_key[1] == k_pool && mp->map_key[2] == v_pool &&
+            mp->map_pages == num_pages) {
+            std::memcpy(&maps, mp->map_blob, sizeof(Maps));
+        } else {
+            st = make_maps(plan, q_prefill, k_pool, v_pool, num_pages, &maps);
+            if (st != POD_OK) return st;
+            std::memcpy(mp->map_blob, &maps, sizeof(Maps));
+            mp->map_key[0] = q_prefill;
+            mp->map_key[1] = k_pool;
+            mp->map_key[2] = v_pool;
+            mp->map_pages = num_pages;
+        }
     }
     RunParams p = make_params(plan, q_prefill, q_decode, k_pool, v_pool, num_pages, indptr, indices, o_prefill,
                               lse_prefill, o_decode, lse_decode, workspace);
@@ -1925,6 +1551,9 @@ pod_status pod_attn_workspace_init(const pod_plan* plan, void* workspace, void* 
     if (e == cudaSuccess && !plan->dec_pos.empty())
         e = cudaMemcpyAsync(ws + plan->ws.off_dec_pos, plan->dec_pos.data(), plan->dec_pos.size() * sizeof(int32_t),
                             cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && !plan->dec_nsplit.empty())
+        e = cudaMemcpyAsync(ws + plan->ws.off_dec_nsplit, plan->dec_nsplit.data(),
+                            plan->dec_nsplit.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && !plan->tile_splits.empty())
         e = cudaMemcpyAsync(ws + plan->ws.off_tile_splits, plan->tile_splits.data(),
                             plan->tile_splits.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
@@ -2010,8 +1639,9 @@ pod_status pod_attn_occupancy(const pod_plan* plan, int32_t* fused, int32_t* pre
     const int G = plan->shape.num_q_heads / plan->shape.num_kv_heads;
     if (G != 4) return POD_ERR_UNSUPPORTED;
     int a = 0;
-    cudaFuncSetAttribute(pod_fused_kernel<4, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, pod_fused_kernel<4, 1, false>, kThreads, kSmemBytes);
+    pod_status st = set_kernel_attributes<4, 1>();
+    if (st != POD_OK) return st;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, pod_fused_kernel<4, 1>, kThreads, kSmemBytes);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
     // one persistent kernel serves all three launch kinds
     *fused = a;

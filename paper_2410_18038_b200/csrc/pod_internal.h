@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -53,7 +54,6 @@ struct SchedCounters {
     uint32_t done;
     uint32_t arrival;
     uint32_t running_prefill[kMaxSms];  // POD_POLICY_COMPLEMENT: prefill CTAs resident per SM
-    uint32_t sm_slot[kMaxSms];          // POD_POLICY_SLOTS: CTAs that have arrived on each SM
 };
 
 struct WorkspaceLayout {
@@ -66,6 +66,7 @@ struct WorkspaceLayout {
     size_t off_dpart_o = 0;       // [num_decodes][splits][Hq][d]
     size_t off_dpart_lse = 0;     // [num_decodes][splits][Hq]
     size_t off_dec_pos = 0;       // int32 per decode: position of its new token (context_len - 1)
+    size_t off_dec_nsplit = 0;    // int32 per decode: its KV split count (the merge reads it)
     size_t total = 0;
 };
 
@@ -86,6 +87,7 @@ struct pod_plan {
     std::vector<pod::DecodeCta> dctas;
     std::vector<int32_t> tile_splits;
     std::vector<int32_t> dec_pos;  // context_len - 1 per decode (KV append)
+    std::vector<int32_t> dec_nsplit;  // KV splits per decode request (min(splits, ctx))
     bool pf_tn64 = false;          // warp-specialised: 64-key pair engine (see pod_plan.cpp)
     int64_t decode_splits = 1;     // largest split count (partials' stride)
     int64_t dec_split_base = 1;    // splits of requests [0, dec_tail_start)
@@ -96,13 +98,12 @@ struct pod_plan {
     int32_t merge_rows_prefill = 0;
     int32_t merge_rows_decode = 0;
     int64_t smem_bytes = 0;
-    double w_prefill = 1.0;  // estimated slot-us per prefill item (POD_POLICY_BALANCED)
-    double w_decode = 1.0;   // estimated slot-us per decode item
-    int32_t prefill_sms = 0; // POD_POLICY_PARTITION: SMs whose slots bind prefill first
     pod::WorkspaceLayout ws;
     int32_t* role_log = nullptr;
     // Tensor maps of the last run (5 x CUtensorMap, 128 B each), re-encoded only when
     // the Q / K / V pointers or the pool size change: host launch cost per run.
+    // Guarded by map_mu (concurrent pod_attn_run calls on one plan).
+    std::mutex map_mu;
     const void* map_key[3] = {nullptr, nullptr, nullptr};
     int64_t map_pages = -1;
     alignas(64) unsigned char map_blob[5 * 128];

@@ -284,10 +284,8 @@ void lower(pod_plan& p) {
     // decode-dominant fused batches (+2..9 % from a share of 0.62, C2 B=64 among them),
     // so they serve batches with a decode share below 0.57.
     {
-        static const char* tn_env = std::getenv("POD_TN64");  // experiment knob: 0 / 1 forces
         const int32_t keys = p.opts.prefill_tile_keys;
-        const bool auto64 = tn_env ? std::atoi(tn_env) != 0 : decode_share(p) < 0.57;
-        p.pf_tn64 = warpspec && p.batch.has_prefill && (keys == 64 || (keys == 0 && auto64));
+        p.pf_tn64 = warpspec && p.batch.has_prefill && (keys == 64 || (keys == 0 && decode_share(p) < 0.57));
     }
     // Whole waves (warp-specialised kernel): the decode items are claimed in id order
     // (request-major) by one decode group per SM, so a count that is not a multiple of
@@ -317,9 +315,11 @@ void lower(pod_plan& p) {
         return static_cast<int64_t>(r) >= p.dec_tail_start ? p.decode_splits : p.dec_split_base;
     };
     const int page_row0 = p.batch.has_prefill ? 1 : 0;
+    p.dec_nsplit.clear();
     for (size_t r = 0; r < p.decode_ctx.size(); ++r) {
         const long ctx = p.decode_ctx[r];
         const long sp_n = std::min<long>(splits_of(r), ctx);
+        p.dec_nsplit.push_back(static_cast<int32_t>(sp_n));
         const long base = ctx / sp_n, rem = ctx % sp_n;
         for (int h = 0; h < s.num_kv_heads; ++h) {
             long pos = 0;
@@ -353,58 +353,6 @@ void lower(pod_plan& p) {
             p.merge_rows_decode += s.num_q_heads;
 }
 
-// Per-item slot-time estimates for POD_POLICY_BALANCED, from the algorithmic
-// work and the per-CTA rates measured on B200 (one resident CTA of the role:
-// ~3.0 TFLOP/s of causal prefill, ~31 GB/s of paged decode).
-void item_costs(pod_plan& p) {
-    const double d = p.shape.head_dim;
-    const int group = p.shape.num_q_heads / p.shape.num_kv_heads;
-    double flops = 0, bytes = 0;
-    for (const pod::PrefillCta& c : p.pctas) {
-        const double keys = std::max(0, std::min(c.kv_end, static_cast<int32_t>(p.batch.prefill.position_offset) +
-                                                               c.row_begin + c.rows) - c.kv_begin);
-        flops += 4.0 * d * c.rows * group * keys;
-    }
-    for (const pod::DecodeCta& c : p.dctas) bytes += 4.0 * d * (c.kv_end - c.kv_begin);
-    const double kPrefillFlopsPerSlotUs = 3.0e6, kDecodeBytesPerSlotUs = 31.0e3;
-    p.w_prefill = p.pctas.empty() ? 1.0 : flops / p.pctas.size() / kPrefillFlopsPerSlotUs;
-    p.w_decode = p.dctas.empty() ? 1.0 : bytes / p.dctas.size() / kDecodeBytesPerSlotUs;
-}
-
-// POD_POLICY_PARTITION: how many SMs bind prefill first.  Prefill on x SMs runs
-// at its 2-CTA/SM rate; decode on the other SMs at min(per-SM stream rate, the
-// HBM share); x balances the two finish times.  B200 rates:
-// ~4.6 TFLOP/s of causal prefill per SM (2 CTAs), ~90 GB/s of paged decode per
-// SM (2 CTAs) up to the measured HBM copy bandwidth.
-int32_t partition_prefill_sms(const pod_plan& p) {
-    const int n = p.dev.num_sms > 0 ? p.dev.num_sms : 148;
-    if (const char* e = std::getenv("POD_PART_SMS")) return std::clamp(std::atoi(e), 0, n);  // experiment knob
-    if (p.pctas.empty()) return 0;
-    if (p.dctas.empty()) return n;
-    const double d = p.shape.head_dim;
-    const int group = p.shape.num_q_heads / p.shape.num_kv_heads;
-    double flops = 0, bytes = 0;
-    for (const pod::PrefillCta& c : p.pctas) {
-        const double keys = std::max(0, std::min(c.kv_end, static_cast<int32_t>(p.batch.prefill.position_offset) +
-                                                               c.row_begin + c.rows) - c.kv_begin);
-        flops += 4.0 * d * c.rows * group * keys;
-    }
-    for (const pod::DecodeCta& c : p.dctas) bytes += 4.0 * d * (c.kv_end - c.kv_begin);
-    const double kPrefillFlopsPerSmUs = 4.6e6, kDecodeBytesPerSmUs = 90.0e3, kHbmBytesPerUs = 6.5e6;
-    int best = 1;
-    double best_t = 1e300;
-    for (int x = 1; x < n; ++x) {
-        const double tp = flops / (x * kPrefillFlopsPerSmUs);
-        const double td = bytes / std::min(kHbmBytesPerUs, (n - x) * kDecodeBytesPerSmUs);
-        const double t = std::max(tp, td);
-        if (t < best_t) {
-            best_t = t;
-            best = x;
-        }
-    }
-    return best;
-}
-
 // make_scheduler_state (gpu_sim.hpp:91-107) over PHYSICAL CTA counts.
 void scheduler_ratio(pod_plan& p) {
     const long P = static_cast<long>(p.pctas.size());
@@ -417,14 +365,6 @@ void scheduler_ratio(pod_plan& p) {
         p.prefill_ratio = g > 0 ? P / g : (P > 0 ? 1 : 0);
         p.decode_ratio = g > 0 ? D / g : (D > 0 ? 1 : 0);
         if (p.prefill_ratio == 0 && p.decode_ratio == 0) p.prefill_ratio = 1;
-    } else if (p.opts.policy == POD_POLICY_BALANCED) {
-        p.prefill_ratio = P > 0 ? 1 : 0;
-        p.decode_ratio = D > 0 ? 1 : 0;
-        if (P == 0 && D == 0) p.prefill_ratio = 1;
-    } else if (p.opts.policy == POD_POLICY_SLOTS) {
-        // fixed 1:1 per SM: one prefill slot, one decode slot (2 CTAs/SM)
-        p.prefill_ratio = 1;
-        p.decode_ratio = 1;
     } else if (p.opts.policy == POD_POLICY_COMPLEMENT) {
         // one prefill CTA per SM (2 slots): the other slot streams decode
         p.prefill_ratio = P > 0 ? 1 : 0;
@@ -434,11 +374,6 @@ void scheduler_ratio(pod_plan& p) {
         p.prefill_ratio = P > 0 ? 1 : 0;
         p.decode_ratio = D > 0 ? 1 : 0;
         if (P == 0 && D == 0) p.prefill_ratio = 1;
-    } else if (p.opts.policy == POD_POLICY_PARTITION) {
-        p.prefill_ratio = P > 0 ? 1 : 0;
-        p.decode_ratio = D > 0 ? 1 : 0;
-        if (P == 0 && D == 0) p.prefill_ratio = 1;
-        p.prefill_sms = partition_prefill_sms(p);
     } else {
         // proportional share rounded to the per-SM slot count, never starving an op
         const int slots = std::max(2, p.cfg.ctas_per_sm);
@@ -480,6 +415,8 @@ void layout_workspace(pod_plan& p) {
     off = align(off + dp * sizeof(float));
     p.ws.off_dec_pos = off;
     off = align(off + p.decode_ctx.size() * sizeof(int32_t));
+    p.ws.off_dec_nsplit = off;
+    off = align(off + p.decode_ctx.size() * sizeof(int32_t));
     p.ws.total = off;
     p.dec_pos.clear();
     for (int64_t c : p.decode_ctx) p.dec_pos.push_back(static_cast<int32_t>(c - 1));
@@ -490,9 +427,8 @@ pod_tile_config b200_tile_config(const pod_plan& p) {
     // kernel's KV tile is 64 keys.  Two CTAs per SM (smem ~112 KB each).
     pod_tile_config c = make_tile_config(2);
     const int group = p.shape.num_q_heads / p.shape.num_kv_heads;
-    // slots policy: two 128-row M-blocks per prefill item (ping-pong engine)
-    const bool two_blocks = (p.opts.policy == POD_POLICY_SLOTS || p.opts.policy == POD_POLICY_WARPSPEC) &&
-                            !std::getenv("POD_ONE_BLOCK");  // experiment knob
+    // warp-specialised kernel: two 128-row M-blocks per prefill item (pair engine)
+    const bool two_blocks = p.opts.policy == POD_POLICY_WARPSPEC;
     const int rows = (two_blocks ? 2 : 1) * pod::kMBlock;
     c.prefill_tile_q = std::max(1, rows / group);
     c.tile_kv = pod::kKvTile;
@@ -563,6 +499,10 @@ void build(pod_plan& p) {
             p.cfg = make_tile_config(prefill_dominant ? 2 : 4);
         }
     }
+    // the warp-specialised pair engine runs at most two 128-row M-blocks per item
+    if (p.opts.policy == POD_POLICY_WARPSPEC && p.batch.has_prefill &&
+        p.cfg.prefill_tile_q * (p.shape.num_q_heads / p.shape.num_kv_heads) > 2 * pod::kMBlock)
+        fail(POD_ERR_UNSUPPORTED, "POD_POLICY_WARPSPEC: prefill_tile_q x group must be <= 256 (use POD_TILE_B200)");
     // -1 keeps the config's flag (reference configs: off; B200 config: on)
     if (p.opts.virtual_decode == 0) p.cfg.virtual_decode = 0;
     if (p.opts.virtual_decode == 1) p.cfg.virtual_decode = 1;
@@ -570,7 +510,6 @@ void build(pod_plan& p) {
     if (p.batch.has_prefill) decompose_prefill(p);
     if (!p.decode_ctx.empty()) decompose_decode(p);
     lower(p);
-    item_costs(p);
     scheduler_ratio(p);
     p.smem_bytes = p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes() : pod::fused_smem_bytes();
     layout_workspace(p);
@@ -625,6 +564,12 @@ pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const p
             p->opts = *opts;
         else
             pod_options_default(&p->opts);
+        {
+            const int32_t pol = p->opts.policy;
+            if (!(pol == POD_POLICY_FIFTY_FIFTY || pol == POD_POLICY_PROPORTIONAL || pol == POD_POLICY_CLAMPED ||
+                  pol == POD_POLICY_COMPLEMENT || pol == POD_POLICY_WARPSPEC || pol == POD_POLICY_AUTO))
+                fail(POD_ERR_INVALID_ARGUMENT, "pod_options: policy must be a POD_POLICY_* value (4-6 are retired)");
+        }
         if (p->opts.out_dtype < POD_OUT_F32 || p->opts.out_dtype > POD_OUT_F16)
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: out_dtype must be a POD_OUT_* value");
         if (p->opts.prefill_tile_keys != 0 && p->opts.prefill_tile_keys != 32 && p->opts.prefill_tile_keys != 64)

@@ -914,7 +914,6 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
             for (uint32_t i = 0; i < n; ++i) {
                 p.ctr->sm_ctr[i] = 0;
                 p.ctr->running_prefill[i] = 0;
-                p.ctr->sm_slot[i] = 0;
             }
             p.ctr->cta_assign[0] = 0;
             p.ctr->cta_assign[1] = 0;

@@ -13,7 +13,7 @@ import torch
 
 from . import _abi
 from ._abi import lib
-from .pod import GpuSpec, HybridBatchSpec, Plan, PlanOptions, _check
+from .pod import GpuSpec, HybridBatchSpec, InvalidArgument, Plan, PlanOptions, _check
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -44,8 +44,9 @@ class PodAttention:
         nbytes = max(256, self.plan.workspace_bytes())
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         stream = torch.cuda.current_stream(self.device)
-        _check(lib().pod_attn_workspace_init(self.plan.handle, _ptr(self.workspace), C.c_void_p(stream.cuda_stream)),
-               "pod_attn_workspace_init")
+        with torch.cuda.device(self.device):
+            _check(lib().pod_attn_workspace_init(self.plan.handle, _ptr(self.workspace),
+                                                 C.c_void_p(stream.cuda_stream)), "pod_attn_workspace_init")
         self.role_log: Optional[torch.Tensor] = None
 
     def enable_role_log(self, extra_ints: int = 0) -> torch.Tensor:
@@ -75,9 +76,58 @@ class PodAttention:
             ld = torch.empty(b, s.num_q_heads, dtype=torch.float32, device=dev)
         return HybridOutputs(op, lp, od, ld)
 
+    def _check_args(self, q_prefill, q_decode, k_pool, v_pool, page_indptr, page_indices, out: HybridOutputs,
+                    mode: str) -> None:
+        """Shapes, dtypes, contiguity and device of every tensor handed to pod_attn_run*: the
+        C ABI takes raw pointers, so a mismatch here would be silently misread by the kernels."""
+        b, s = self.batch, self.batch.shape
+        kv_dt = torch.float16 if b.dtype == _abi.POD_DTYPE_FP16 else torch.bfloat16
+        m = self.MODES[mode]
+        need_p = b.prefill is not None and m != 3
+        need_d = bool(b.decodes) and m != 2
+
+        def t(x, name, dtype, shape=None):
+            if x is None:
+                raise InvalidArgument(f"{name} is required for this batch")
+            if x.device != self.device:
+                raise InvalidArgument(f"{name} is on {x.device}, the plan runs on {self.device}")
+            if x.dtype != dtype:
+                raise InvalidArgument(f"{name} must be {dtype}, got {x.dtype}")
+            if not x.is_contiguous():
+                raise InvalidArgument(f"{name} must be contiguous")
+            if shape is not None and tuple(x.shape) != tuple(shape):
+                raise InvalidArgument(f"{name} has shape {tuple(x.shape)}, expected {tuple(shape)}")
+
+        if k_pool.dim() != 4 or k_pool.shape != v_pool.shape:
+            raise InvalidArgument("k_pool / v_pool must be equal 4-D pools")
+        ps = b.page_size
+        pool = ((k_pool.shape[0], s.num_kv_heads, ps, s.head_dim) if b.kv_layout == _abi.POD_KV_HND
+                else (k_pool.shape[0], ps, s.num_kv_heads, s.head_dim))
+        t(k_pool, "k_pool", kv_dt, pool)
+        t(v_pool, "v_pool", kv_dt, pool)
+        nreq = (1 if b.prefill is not None else 0) + len(b.decodes)
+        t(page_indptr, "page_indptr", torch.int32, (nreq + 1,))
+        t(page_indices, "page_indices", torch.int32)
+        odt = self.out_dtype
+        if need_p:
+            c = b.prefill.chunk_size
+            t(q_prefill, "q_prefill", kv_dt, (c, s.num_q_heads, s.head_dim))
+            t(out.o_prefill, "o_prefill", odt, (c, s.num_q_heads, s.head_dim))
+            t(out.lse_prefill, "lse_prefill", torch.float32, (c, s.num_q_heads))
+        if need_d:
+            nb = len(b.decodes)
+            t(q_decode, "q_decode", kv_dt, (nb, s.num_q_heads, s.head_dim))
+            t(out.o_decode, "o_decode", odt, (nb, s.num_q_heads, s.head_dim))
+            t(out.lse_decode, "lse_decode", torch.float32, (nb, s.num_q_heads))
+
     def run(self, q_prefill, q_decode, k_pool, v_pool, page_indptr, page_indices,
             out: Optional[HybridOutputs] = None, mode: str = "fused", stream=None) -> HybridOutputs:
         out = out or self.alloc_outputs()
+        self._check_args(q_prefill, q_decode, k_pool, v_pool, page_indptr, page_indices, out, mode)
+        with torch.cuda.device(self.device):
+            return self._launch(q_prefill, q_decode, k_pool, v_pool, page_indptr, page_indices, out, mode, stream)
+
+    def _launch(self, q_prefill, q_decode, k_pool, v_pool, page_indptr, page_indices, out, mode, stream):
         st = stream or torch.cuda.current_stream(self.device)
         num_pages = k_pool.shape[0]
         args = (_ptr(q_prefill), _ptr(q_decode), _ptr(k_pool), _ptr(v_pool), C.c_int64(num_pages),
@@ -98,6 +148,12 @@ class PodAttention:
         """pod_attn_append_kv: scatter the batch's new K/V rows ([chunk][Hkv][d] and
         [B][Hkv][d], pool dtype) into their page slots (before run())."""
         st = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            self._append(k_new_prefill, v_new_prefill, k_new_decode, v_new_decode, k_pool, v_pool, page_indptr,
+                         page_indices, st)
+
+    def _append(self, k_new_prefill, v_new_prefill, k_new_decode, v_new_decode, k_pool, v_pool, page_indptr,
+                page_indices, st) -> None:
         _check(lib().pod_attn_append_kv(self.plan.handle, _ptr(k_new_prefill), _ptr(v_new_prefill), _ptr(k_new_decode),
                                         _ptr(v_new_decode), _ptr(k_pool), _ptr(v_pool), C.c_int64(k_pool.shape[0]),
                                         _ptr(page_indptr), _ptr(page_indices), _ptr(self.workspace),

@@ -13,7 +13,7 @@ import torch
 import paper_2410_18038_b200 as pkg
 from oracle import pyoracle as O
 from paper_2410_18038_b200._abi import (POD_DTYPE_FP16, POD_KV_NHD, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT,
-                                        POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_SLOTS,
+                                        POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL,
                                         POD_POLICY_WARPSPEC,
                                         POD_PRECISION_FAST, POD_TILE_B200, POD_TILE_REFERENCE)
 from paper_2410_18038_b200.workload import build_workload, make_batch
@@ -70,12 +70,11 @@ def test_matches_oracle(name, mode):
     batch = make_batch(pkg.ModelShape(hq, hkv, 128, SCALE), chunk=chunk, offset=off, decode_ctx=dec)
     wl, _, out = _run(batch, mode)
     _check(wl, out)
-    # the two-block ping-pong prefill engine of the slots policy
-    wl, _, out = _run(batch, mode, options=pkg.PlanOptions(policy=POD_POLICY_SLOTS), wl=wl)
-    _check(wl, out)
-    # the warp-specialised one-CTA-per-SM kernel
-    wl, _, out = _run(batch, mode, options=pkg.PlanOptions(policy=POD_POLICY_WARPSPEC), wl=wl)
-    _check(wl, out)
+    # the warp-specialised one-CTA-per-SM kernel, both pair-engine tile widths
+    for keys in (32, 64):
+        wl, _, out = _run(batch, mode, options=pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=keys),
+                          wl=wl)
+        _check(wl, out)
 
 
 def test_fast_precision_bf16_p_within_loose_bound():
@@ -89,11 +88,16 @@ def test_fast_precision_bf16_p_within_loose_bound():
 
 
 @pytest.mark.parametrize("policy", [POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED,
-                                    POD_POLICY_COMPLEMENT, POD_POLICY_SLOTS])
+                                    POD_POLICY_COMPLEMENT, POD_POLICY_WARPSPEC])
 def test_policies_and_reference_tiles(policy):
     _need_gpu()
     batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=200, offset=37, decode_ctx=[500, 33, 90])
     for tile_mode in (POD_TILE_B200, POD_TILE_REFERENCE):
+        if policy == POD_POLICY_WARPSPEC and tile_mode == POD_TILE_REFERENCE:
+            # the reference's 128-row q tiles are 4 M-blocks: more than the pair engine runs
+            with pytest.raises(pkg.Unsupported):
+                _run(batch, options=pkg.PlanOptions(policy=policy, tile_mode=tile_mode))
+            continue
         wl, _, out = _run(batch, options=pkg.PlanOptions(policy=policy, tile_mode=tile_mode))
         _check(wl, out)
 
@@ -243,6 +247,19 @@ def test_split_invariance(policy):
         d = (o.o_decode - base.o_decode).abs().max().item() / base.o_decode.abs().max().item()
         p = (o.o_prefill - base.o_prefill).abs().max().item() / base.o_prefill.abs().max().item()
         assert d <= O_TOL and p <= O_TOL
+
+
+@pytest.mark.parametrize("policy", KERNELS)
+def test_short_decode_contexts_with_more_splits_than_keys(policy):
+    """an explicit decode_splits above a request's context length.
+    Each request is split min(splits, ctx) ways, and the merge reads that per-request
+    count, so no request merges partial slots that no CTA wrote."""
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=40, offset=60, decode_ctx=[1, 3, 2000, 2, 17])
+    wl = build_workload(batch, device="cuda")
+    for ds in (4, 8):
+        _, _, out = _run(batch, options=_kopts(policy, decode_splits=ds), wl=wl)
+        _check(wl, out)
 
 
 @pytest.mark.parametrize("chunk,offset,ctx,keys", [(256, 1000, [300, 90], 64), (16, 100, [4096] * 8, 32)])

@@ -262,17 +262,17 @@ def test_plan_ratio_policies():
 
 
 def test_b200_plan_lowering():
-    """B200 tile mode: one 128-row M-block per prefill item (two for the slots
-    policy's ping-pong engine); decode items cover each (request, kv head) with
+    """B200 tile mode: one 128-row M-block per prefill item (two for the warp-
+    specialised pair engine); decode items cover each (request, kv head) with
     4 virtual warps whose ranges are the reference's virtual tasks when
     decode_splits = 1."""
-    from paper_2410_18038_b200._abi import POD_POLICY_FIFTY_FIFTY, POD_POLICY_SLOTS
+    from paper_2410_18038_b200._abi import POD_POLICY_FIFTY_FIFTY, POD_POLICY_WARPSPEC
     shape = ModelShape(32, 8, 128, math.sqrt(128))
     b = HybridBatchSpec(prefill=PrefillSpec(1024, 16384, 15360), decodes=[DecodeSpec(16384)] * 64, shape=shape)
     i = Plan(b, GpuSpec.b200(), PlanOptions(tile_mode=POD_TILE_B200, policy=POD_POLICY_FIFTY_FIFTY)).info()
     assert i.config.prefill_tile_q * shape.group_size() == 128
     assert i.num_prefill_ctas == i.num_prefill_tasks == 32 * 8 * i.prefill_splits
-    p = Plan(b, GpuSpec.b200(), PlanOptions(tile_mode=POD_TILE_B200, decode_splits=1, policy=POD_POLICY_SLOTS))
+    p = Plan(b, GpuSpec.b200(), PlanOptions(tile_mode=POD_TILE_B200, decode_splits=1, policy=POD_POLICY_WARPSPEC))
     i = p.info()
     assert i.config.prefill_tile_q * shape.group_size() == 256
     assert i.num_prefill_ctas == i.num_prefill_tasks == 16 * 8 * i.prefill_splits
@@ -282,3 +282,24 @@ def test_b200_plan_lowering():
         assert t.is_virtual
     # the virtual ranges of parent (0, 0) are split_ranges(16384, 4)
     assert [t.kv_split for t in wd.decode_tasks[:4]] == pkg.split_ranges(16384, 4)
+
+
+@pytest.mark.parametrize("policy", [4, 5, 6, 9, -1])
+def test_retired_and_unknown_policies_are_rejected(policy):
+    shape = ModelShape(32, 8, 128, math.sqrt(128))
+    b = HybridBatchSpec(prefill=PrefillSpec(64, 128, 64), decodes=[DecodeSpec(100)], shape=shape)
+    with pytest.raises(InvalidArgument, match="policy"):
+        Plan(b, GpuSpec.b200(), PlanOptions(policy=policy))
+
+
+def test_decode_split_count_per_request_is_clamped_to_context():
+    """an explicit decode_splits larger than a request's context
+    gives that request min(splits, ctx) CTAs; the plan's per-request counts (read by
+    the merge) match the CTA table."""
+    shape = ModelShape(32, 8, 128, math.sqrt(128))
+    b = HybridBatchSpec(decodes=[DecodeSpec(1), DecodeSpec(3), DecodeSpec(2000)], shape=shape)
+    for policy in (3, 7):
+        p = Plan(b, GpuSpec.b200(), PlanOptions(policy=policy, decode_splits=4))
+        i = p.info()
+        assert i.num_decode_ctas == 8 * (1 + 3 + 4)
+        assert i.num_merge_rows_decode == 2 * 32  # requests 1 and 2 merge, request 0 writes directly
