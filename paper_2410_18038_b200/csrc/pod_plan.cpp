@@ -466,8 +466,11 @@ void build(pod_plan& p) {
         double avg_ctx = 0;
         for (int64_t c : p.decode_ctx) avg_ctx += static_cast<double>(c);
         avg_ctx = p.decode_ctx.empty() ? 0 : avg_ctx / static_cast<double>(p.decode_ctx.size());
-        p.opts.policy = (p.batch.has_prefill && decode_share(p) >= 0.1 && avg_ctx >= 2048) ? POD_POLICY_WARPSPEC
-                                                                                              : POD_POLICY_COMPLEMENT;
+        // (the warp-specialised pair engine needs the B200 tile config's 256-row items)
+        const bool b200_tiles = p.opts.tile_mode == POD_TILE_B200 && !p.opts.tile_override;
+        p.opts.policy = (b200_tiles && p.batch.has_prefill && decode_share(p) >= 0.1 && avg_ctx >= 2048)
+                            ? POD_POLICY_WARPSPEC
+                            : POD_POLICY_COMPLEMENT;
     }
     if (p.opts.tile_override) {
         p.cfg = *p.opts.tile_override;
