@@ -127,11 +127,94 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- CPU baseline --
+_CPU_INPUTS = {}
+
+
+def _cpu_layer_inputs(hq, hkv, chunk, off, b, ctx, threads, seed=7, rows_per_block=64):
+    """Full-layer inputs for the reference's CPU path, built once per process (the step
+    times only the reference's attention, not input generation):
+      prefill: one shard per (KV head, block of `rows_per_block` chunk rows) --
+               tiled_prefill_attention on QueryChunk(rows, group, d, off + r0) against
+               that KV head's cache prefix, an exact restriction of the full call by GQA
+               consistency (test_attention.cpp:252-270) and row independence
+               (attention.hpp:183-212);
+      decode:  one shard per (request, KV head) -- decode_attention over ctx keys.
+    Decode caches are drawn from a pool of min(B*Hkv, 4*threads) distinct [ctx][1][d]
+    arrays (each 2*ctx*d*8 bytes, far beyond the CPU caches), so the 16 GB of distinct
+    fp64 caches of C2 B=64 need not be materialised."""
+    import numpy as np
+
+    key = (hq, hkv, chunk, off, b, ctx, threads)
+    if key in _CPU_INPUTS:
+        return _CPU_INPUTS[key]
+    d, G = 128, hq // hkv
+    rng = np.random.default_rng(seed)
+    pf, dc, keep = [], [], []
+    if chunk:
+        kvlen = off + chunk
+        for h in range(hkv):
+            k = rng.uniform(-1, 1, (kvlen, 1, d))
+            v = rng.uniform(-1, 1, (kvlen, 1, d))
+            keep += [k, v]
+            for r0 in range(0, chunk, rows_per_block):
+                rows = min(rows_per_block, chunk - r0)
+                q = rng.uniform(-1, 1, (rows, G, d))
+                o = np.zeros((rows, G * d))
+                n = off + r0 + rows
+                pf.append(dict(kind=0, group=G, rows=rows, offset=off + r0, q=q, k=k[:n], v=v[:n], out=o))
+    if b:
+        npool = min(b * hkv, 4 * threads)
+        pool = [(rng.uniform(-1, 1, (ctx, 1, d)), rng.uniform(-1, 1, (ctx, 1, d))) for _ in range(npool)]
+        keep += pool
+        for i in range(b * hkv):
+            k, v = pool[i % npool]
+            dc.append(dict(kind=1, group=G, rows=1, offset=0, q=rng.uniform(-1, 1, (G, d)), k=k, v=v,
+                           out=np.zeros((G, d))))
+    _CPU_INPUTS[key] = (pf, dc, keep)
+    return _CPU_INPUTS[key]
+
+
+def cpu_reference_layer(hq, hkv, chunk, off, b, ctx, threads=None, max_core_s=900.0):
+    """Times ONE FULL layer of the reference's own tiled_prefill_attention /
+    decode_attention (oracle/_ref, compiled from /root/reference; its parallel_for over
+    all host threads, tile_q = tile_kv = 64) -- no sampling, no extrapolation.
+    Layers estimated above `max_core_s` core-seconds (C5 extremes) fall back to
+    `cpu_reference_sample`.  Returns (us_per_layer, threads, description, wall_s)."""
+    import numpy as np
+
+    from oracle import pyoracle as O
+
+    if not O.ref_available():
+        raise RuntimeError("oracle/_ref missing")
+    threads = threads or os.cpu_count() or 1
+    d, G = 128, hq // hkv
+    # single-core rate of the reference's inner loops (one small decode shard)
+    rng = np.random.default_rng(1)
+    kcal = rng.uniform(-1, 1, (4096, 1, d))
+    t = O.run_shards([dict(kind=1, group=G, rows=1, offset=0, q=rng.uniform(-1, 1, (G, d)), k=kcal, v=kcal,
+                           out=np.zeros((G, d)))], d, math.sqrt(d), 64, 64, 1)
+    rate1 = G * 4096 / max(t, 1e-6)
+    pairs = hkv * G * (chunk * off + chunk * (chunk + 1) / 2.0) + b * hkv * G * float(ctx)
+    if pairs / rate1 > max_core_s:
+        us, thr, desc, wall = cpu_reference_sample(hq, hkv, chunk, off, b, ctx, target_s=max_core_s / 4,
+                                                   threads=threads)
+        return us, thr, desc + f" (full layer ~{pairs / rate1:.0f} core-s > {max_core_s:.0f}: sampled)", wall
+    pf, dc, _ = _cpu_layer_inputs(hq, hkv, chunk, off, b, ctx, threads)
+    t_pf = O.run_shards(pf, d, math.sqrt(d), 64, 64, threads) if pf else 0.0
+    t_dc = O.run_shards(dc, d, math.sqrt(d), 64, 64, threads) if dc else 0.0
+    desc = (f"full layer, no extrapolation: {len(pf)} prefill shards (KV head x 64-row block, "
+            f"{G} q heads each) + {len(dc)} decode (request, KV head) shards at {ctx} keys; "
+            f"prefill {t_pf:.2f} s + decode {t_dc:.2f} s wall on {threads} threads (the reference's parallel_for; "
+            f"each shard builds its KVCache, as the reference API requires)")
+    return (t_pf + t_dc) * 1e6, threads, desc, t_pf + t_dc
+
+
 def cpu_reference_sample(hq, hkv, chunk, off, b, ctx, target_s=12.0, threads=None, seed=7):
     """Times the reference's own tiled_prefill_attention / decode_attention
     (oracle/_ref, built from /root/reference) on a bounded, representative sample
-    of the layer and extrapolates linearly in (q-head row, key) pairs.
-    Returns (us_per_layer, threads, sample_description)."""
+    of the layer and extrapolates linearly in (q-head row, key) pairs.  Only used
+    for layers too large to time whole (cpu_reference_layer).
+    Returns (us_per_layer, threads, sample_description, wall_s)."""
     import numpy as np
 
     from oracle import pyoracle as O
@@ -143,18 +226,15 @@ def cpu_reference_sample(hq, hkv, chunk, off, b, ctx, target_s=12.0, threads=Non
     G = hq // hkv
     scale = math.sqrt(d)
     rng = np.random.default_rng(seed)
-    # full-layer pairs
     pf_pairs = hkv * G * (chunk * off + chunk * (chunk + 1) / 2.0)
     dec_pairs = b * hkv * G * float(ctx)
     total_pairs = pf_pairs + dec_pairs
-    # calibrate throughput with one small shard
     kcal = rng.uniform(-1, 1, (4096, 1, d)).round(3)
     qcal = rng.uniform(-1, 1, (G, d))
     out = np.zeros((G, d))
     t = O.run_shards([dict(kind=1, group=G, rows=1, offset=0, q=qcal, k=kcal, v=kcal, out=out)], d, scale, 64, 64, 1)
-    rate1 = G * 4096 / max(t, 1e-6)  # pairs/s on one core
-    budget_pairs = target_s * rate1  # ~target_s core-seconds of the reference's own work
-    # sample: prefill row blocks spread over the chunk + decode shards, in proportion
+    rate1 = G * 4096 / max(t, 1e-6)
+    budget_pairs = target_s * rate1
     n_shards = max(2 * threads, 8)
     pf_share = pf_pairs / total_pairs
     shards = []
@@ -186,21 +266,17 @@ def cpu_reference_sample(hq, hkv, chunk, off, b, ctx, target_s=12.0, threads=Non
             o = np.zeros((G, d))
             shards.append(dict(kind=1, group=G, rows=1, offset=0, q=q, k=k, v=v, out=o))
             keep += [k, v, q, o]
-        dec_scale = ctx / dctx
     else:
-        dctx, dec_scale = 0, 1.0
-    # time prefill and decode shards separately so each extrapolates by its own work
+        dctx = 0
     pf = [s for s in shards if s["kind"] == 0]
     dc = [s for s in shards if s["kind"] == 1]
     t_pf = O.run_shards(pf, d, scale, 64, 64, threads) if pf else 0.0
     t_dc = O.run_shards(dc, d, scale, 64, 64, threads) if dc else 0.0
-    pf_sample_pairs = sample_pairs
-    dc_sample_pairs = len(dc) * G * dctx
     us = 0.0
     if pf:
-        us += t_pf * (pf_pairs / pf_sample_pairs) * 1e6
+        us += t_pf * (pf_pairs / sample_pairs) * 1e6
     if dc:
-        us += t_dc * (dec_pairs / dc_sample_pairs) * 1e6
+        us += t_dc * (dec_pairs / (len(dc) * G * dctx)) * 1e6
     desc = (f"{len(pf)} prefill row-blocks x {pf[0]['rows'] if pf else 0} rows (1 KV head, {G} q heads) + "
             f"{len(dc)} decode (request, KV head) shards at {dctx} keys; {t_pf + t_dc:.1f} s wall on {threads} "
             f"threads; extrapolated linearly in (q-head row, key) pairs to the full layer")
@@ -208,41 +284,24 @@ def cpu_reference_sample(hq, hkv, chunk, off, b, ctx, target_s=12.0, threads=Non
 
 
 # --------------------------------------------------------------- GPU arm ---
-def run_pod(args, rank, world, local_rank):
+def _max_over_ranks(t, dev):
     import torch
     import torch.distributed as dist
 
-    import paper_2410_18038_b200 as pkg
-    from paper_2410_18038_b200.hybrid import PodAttention
-    from paper_2410_18038_b200.tp import gather_outputs, shard_heads
-    from paper_2410_18038_b200.workload import build_workload, make_batch
+    x = torch.tensor([t], device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(x, op=dist.ReduceOp.MAX)
+    return float(x.item())
 
-    hq, hkv, chunk, off, b, ctx = CONFIGS[args.config]
-    if hkv % world:
-        raise SystemExit(f"Hkv={hkv} not divisible by {world} GPUs")
-    shard = shard_heads(pkg.ModelShape(hq, hkv, 128, math.sqrt(128)), rank, world)
-    hq_r, hkv_r = shard.shape.num_q_heads, shard.shape.num_kv_heads
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    shape = shard.shape
-    batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
-    wl = build_workload(batch, device=dev, seed_q=42 + 1000 * rank, seed_kv=43 + 1000 * rank)
-    opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode, precision=args.precision,
-                           decode_splits=args.decode_splits, split_wave_cap=args.split_wave_cap,
-                           out_dtype={"f32": 0, "bf16": 1}[args.out_dtype])
-    op = PodAttention(batch, options=opts, device=local_rank)
-    out = op.alloc_outputs()
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
-    def step(mode):
-        op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=out, mode=mode)
-        if world > 1:  # assemble the layer output: one all-gather of [tokens][Hq/T][d] over NVLink
-            local = torch.cat([out.o_prefill.reshape(-1), out.o_decode.reshape(-1)])
-            gather_outputs(local, world)
+def _timer(dev, flush, world):
+    import torch
+    import torch.distributed as dist
 
-    def timed(mode, steps, warmup):
+    def timed(step, steps, warmup):
+        """Mean device time of `steps` calls of step() (CUDA events on the launching
+        stream, L2 flushed before each), max over ranks."""
         for _ in range(warmup):
-            step(mode)
+            step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -250,17 +309,85 @@ def run_pod(args, rank, world, local_rank):
         for i in range(steps):
             flush.zero_()  # L2 flush (512 MB > 126 MB L2), outside the timed events
             ev[i][0].record()
-            step(mode)
+            step()
             ev[i][1].record()
         torch.cuda.synchronize()
         ms = [a.elapsed_time(e) for a, e in ev]
         t = sum(ms) / len(ms)
         if world > 1:
-            x = torch.tensor([t], device=dev)
-            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            t = _max_over_ranks(t, dev)
             dist.barrier()
-            t = float(x.item())
         return t, ms
+
+    return timed
+
+
+def serial_candidates(batch):
+    """Every way the repo can run the prefill alone and the decode alone: both POD
+    kernels, both pair-engine tile widths, prefill split caps 1..8 (gpu_sim.hpp:496-506
+    defines serial as prefill-then-decode with the same kernels; the honest comparator
+    takes the fastest of each)."""
+    import paper_2410_18038_b200 as pkg
+    from paper_2410_18038_b200._abi import POD_POLICY_COMPLEMENT, POD_POLICY_WARPSPEC
+
+    pf, dc = [], []
+    if batch.prefill is not None:
+        for tk in (32, 64):
+            for cap in (1, 2):
+                pf.append((f"warpspec/{tk}-key/cap{cap}",
+                           pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=tk, split_wave_cap=cap)))
+        for cap in (1, 2, 4, 8):
+            pf.append((f"complement/cap{cap}", pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT, split_wave_cap=cap)))
+    if batch.decodes:
+        dc = [("warpspec", pkg.PlanOptions(policy=POD_POLICY_WARPSPEC)),
+              ("complement", pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT))]
+    return pf, dc
+
+
+def run_pod(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_18038_b200 as pkg
+    from paper_2410_18038_b200.hybrid import PodAttention
+    from paper_2410_18038_b200.tp import (all_gather_bytes, assemble_layer, gather_buffers, layer_error,
+                                          shard_heads, shard_workload)
+    from paper_2410_18038_b200.workload import build_workload, make_batch
+
+    hq, hkv, chunk, off, b, ctx = CONFIGS[args.config]
+    if hkv % world:
+        raise SystemExit(f"Hkv={hkv} not divisible by {world} GPUs")
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    full_shape = pkg.ModelShape(hq, hkv, 128, math.sqrt(128))
+    shard = shard_heads(full_shape, rank, world)
+    hq_r, hkv_r = shard.shape.num_q_heads, shard.shape.num_kv_heads
+    # every rank draws the SAME seeded full layer and keeps its KV-head group (SURVEY.md 8(e))
+    full_batch = make_batch(full_shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
+    full_wl = build_workload(full_batch, device=dev)
+    wl = shard_workload(full_wl, shard) if world > 1 else full_wl
+    if world > 1 and rank != 0:
+        del full_wl
+        full_wl = None
+        torch.cuda.empty_cache()
+    batch = wl.batch
+    odt = {"f32": torch.float32, "bf16": torch.bfloat16}[args.out_dtype]
+    opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode, precision=args.precision,
+                           decode_splits=args.decode_splits, split_wave_cap=args.split_wave_cap,
+                           out_dtype={"f32": 0, "bf16": 1}[args.out_dtype])
+    op = PodAttention(batch, options=opts, device=local_rank)
+    # the kernel writes straight into the all-gather send buffer (two, for the pipelined e2e)
+    gbs = [gather_buffers(batch, world, odt, dev) for _ in range(2)]
+    out = gbs[0].outputs
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    timed = _timer(dev, flush, world)
+
+    def layer(mode, o=None, gb=None, stream=None):
+        op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices,
+               out=o or out, mode=mode, stream=stream)
+        if world > 1:  # assemble the layer output: one all-gather of [tokens][Hq/T][d] + LSE over NVLink
+            g = gb or gbs[0]
+            all_gather_bytes(g.send, g.recv, world)
 
     # KV append (the write step before attention, SURVEY.md 8(f) N2): the batch's new
     # K/V rows (chunk tokens + one per decode, read back from their slots) scattered
@@ -279,44 +406,50 @@ def run_pod(args, rank, world, local_rank):
                      k_rows[chunk:] if b else None, v_rows[chunk:] if b else None,
                      wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
 
-    for _ in range(args.warmup):
-        append()
-    torch.cuda.synchronize()
-    aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for i in range(args.steps):
-        flush.zero_()
-        aev[i][0].record()
-        append()
-        aev[i][1].record()
-    torch.cuda.synchronize()
-    t_append = sum(x.elapsed_time(y) for x, y in aev) / args.steps
+    t_append, _ = timed(append, args.steps, args.warmup)
     append_bytes = 2 * 2 * k_rows.numel() * k_rows.element_size()  # K + V, read + write
 
     sampler = ClockSampler(local_rank)
     with sampler:
-        t_fused, ms_fused = timed("fused", args.steps, args.warmup)
-        t_serial, _ = timed("serial", args.steps, args.warmup)
-        t_pf, _ = timed("prefill", args.steps, args.warmup) if chunk else (0.0, [])
-        t_dec, _ = timed("decode", args.steps, args.warmup) if b else (0.0, [])
+        t_fused, ms_fused = timed(lambda: layer("fused"), args.steps, args.warmup)
+        t_serial, _ = timed(lambda: layer("serial"), args.steps, args.warmup)
+        t_pf, _ = timed(lambda: layer("prefill"), args.steps, args.warmup) if chunk else (0.0, [])
+        t_dec, _ = timed(lambda: layer("decode"), args.steps, args.warmup) if b else (0.0, [])
+        t_attn = timed(lambda: op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr,
+                                      wl.page_indices, out=out), args.steps, args.warmup)[0] if world > 1 else t_fused
+        # honest serial comparator: the fastest prefill-alone and decode-alone over every
+        # kernel / tile width / split cap the repo has (no all-gather: attention only)
+        best = {}
+        if not args.no_serial_search:
+            pf_c, dc_c = serial_candidates(batch)
+            for role, cands, mode in (("prefill", pf_c, "prefill"), ("decode", dc_c, "decode")):
+                for name, o in cands:
+                    c_op = PodAttention(batch, options=o, device=local_rank)
+                    c_out = c_op.alloc_outputs()
+                    t, _ = timed(lambda: c_op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr,
+                                                  wl.page_indices, out=c_out, mode=mode), args.steps, args.warmup)
+                    if role not in best or t < best[role][0]:
+                        best[role] = (t, name)
+                    del c_op, c_out
     clocks = sampler.summary()
 
     # e2e through the C ABI with HOST buffers (pinned): every step copies its queries
-    # H2D, runs the fused layer and copies its outputs (O + LSE) D2H.  Steps are
-    # pipelined the way a serving loop runs them: double-buffered device Q / O, the
-    # H2D of step i+1 and the D2H of step i-1 on their own copy streams (separate
-    # copy engines) overlap the kernel of step i.  The paged KV cache is device state.
+    # H2D, runs the fused layer (+ the all-gather at N > 1) and copies its outputs
+    # (O + LSE) D2H.  Steps are pipelined the way a serving loop runs them:
+    # double-buffered device Q / O, the H2D of step i+1 and the D2H of step i-1 on their
+    # own copy streams (separate copy engines) overlap the kernel of step i.  The paged
+    # KV cache is device state.
     qp_h = wl.q_prefill.cpu().pin_memory() if chunk else None
     qd_h = wl.q_decode.cpu().pin_memory() if b else None
-    outs = [out, op.alloc_outputs()]
     q_dev = [(wl.q_prefill, wl.q_decode),
              (wl.q_prefill.clone() if chunk else None, wl.q_decode.clone() if b else None)]
 
-    def _dev_out(o):
-        return [t for t in (o.o_prefill, o.lse_prefill, o.o_decode, o.lse_decode) if t is not None]
+    def _dev_out(g):  # what the step hands back to the host: this rank's O + LSE, or the gathered layer
+        return [g.send] if world == 1 else [g.recv]
 
-    host_out = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in _dev_out(o)] for o in outs]
+    host_out = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in _dev_out(g)] for g in gbs]
     h2d = (qp_h.numel() * 2 if qp_h is not None else 0) + (qd_h.numel() * 2 if qd_h is not None else 0)
-    d2h = sum(t.numel() * t.element_size() for t in _dev_out(out))
+    d2h = sum(t.numel() * t.element_size() for t in _dev_out(gbs[0]))
     s_c = torch.cuda.current_stream(dev)
     s_h, s_d = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ev_h = [torch.cuda.Event() for _ in range(2)]
@@ -337,15 +470,14 @@ def run_pod(args, rank, world, local_rank):
             ev_h[j].record(s_h)
         s_c.wait_event(ev_h[j])
         s_c.wait_event(ev_d[j])  # O buffer j drained by the D2H of step i-2
-        op.run(qp, qd, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=outs[j], mode="fused",
+        op.run(qp, qd, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, out=gbs[j].outputs, mode="fused",
                stream=s_c)
         if world > 1:
-            local = torch.cat([outs[j].o_prefill.reshape(-1), outs[j].o_decode.reshape(-1)])
-            gather_outputs(local, world)
+            all_gather_bytes(gbs[j].send, gbs[j].recv, world)
         ev_c[j].record(s_c)
         with torch.cuda.stream(s_d):  # D2H of this step's outputs
             s_d.wait_event(ev_c[j])
-            for hsrc, dsrc in zip(host_out[j], _dev_out(outs[j])):
+            for hsrc, dsrc in zip(host_out[j], _dev_out(gbs[j])):
                 hsrc.copy_(dsrc, non_blocking=True)
             ev_d[j].record(s_d)
 
@@ -366,14 +498,31 @@ def run_pod(args, rank, world, local_rank):
     torch.cuda.synchronize()
     t_e2e = t0.elapsed_time(t1) / args.steps
     if world > 1:
-        x = torch.tensor([t_e2e], device=dev)
-        dist.all_reduce(x, op=dist.ReduceOp.MAX)
-        t_e2e = float(x.item())
+        t_e2e = _max_over_ranks(t_e2e, dev)
+
+    # TP self-check: the assembled layer (every rank's kernel + the all-gather) against a
+    # TP1 run of the same seeded layer on rank 0 (north-star tolerance, 2e-3)
+    tp_check = None
+    if world > 1:
+        layer("fused")
+        torch.cuda.synchronize()
+        if rank == 0:
+            o_tp, lse_tp = assemble_layer(gbs[0])
+            ref_op = PodAttention(full_batch, options=pkg.PlanOptions(out_dtype=opts.out_dtype), device=local_rank)
+            ro = ref_op.run(full_wl.q_prefill, full_wl.q_decode, full_wl.k_pool, full_wl.v_pool,
+                            full_wl.page_indptr, full_wl.page_indices)
+            torch.cuda.synchronize()
+            o_ref = torch.cat([t for t in (ro.o_prefill, ro.o_decode) if t is not None])
+            lse_ref = torch.cat([t for t in (ro.lse_prefill, ro.lse_decode) if t is not None])
+            eo, el = layer_error(o_tp, lse_tp, o_ref, lse_ref, hq // hkv)
+            tp_check = {"vs": "tp1 fused run of the same layer on rank 0", "o_rel_err": eo, "lse_abs_err": el,
+                        "tol": 2e-3, "ok": bool(eo <= 2e-3 and el <= 2e-3)}
+        dist.barrier()
 
     info = op.info
     launches_per_step = 1 + (1 if info.num_merge_rows_prefill > 0 else 0) + (1 if info.num_merge_rows_decode > 0 else 0)
     res = dict(t_fused=t_fused, ms_fused=ms_fused, t_serial=t_serial, t_pf=t_pf, t_dec=t_dec, t_e2e=t_e2e,
-               t_append=t_append, append_bytes=append_bytes,
+               t_attn=t_attn, t_append=t_append, append_bytes=append_bytes, best=best, tp_check=tp_check,
                clocks=clocks, info=info, launches=launches_per_step, h2d=h2d, d2h=d2h, hq_r=hq_r, hkv_r=hkv_r)
     return res
 
@@ -392,8 +541,10 @@ def main():
                     help="element type of the attention outputs (LSE stays fp32); f32 = the reference's")
     ap.add_argument("--decode-splits", type=int, default=0)
     ap.add_argument("--split-wave-cap", type=int, default=0)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="wall seconds of the CPU reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-serial-search", action="store_true",
+                    help="skip the search for the fastest prefill-alone / decode-alone (serial_best_us)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -414,13 +565,10 @@ def main():
             return
         steps = max(1, args.steps)
         vals = []
-        t_wall = 0.0
         for i in range(args.warmup + steps):
-            us, thr, desc, wall = cpu_reference_sample(hq, hkv, chunk, off, b, ctx,
-                                                       target_s=min(args.cpu_seconds, 6.0), seed=7 + i)
+            us, thr, desc, wall = cpu_reference_layer(hq, hkv, chunk, off, b, ctx)
             if i >= args.warmup:
                 vals.append(us)
-                t_wall += wall
         v = sum(vals) / len(vals)
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "us/layer", "n_gpus": args.gpus,
@@ -438,8 +586,14 @@ def main():
 
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # one rank per GPU; --dist-backend gloo with more ranks than GPUs is a plumbing
+        # check of the TP path on a 1-GPU box (ranks share the device), never a number
+        local_rank = local_rank % torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(args.dist_backend)
     r = run_pod(args, rank, world, local_rank)
     if world > 1:
         dist.barrier()
@@ -469,14 +623,13 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:  # the CPU baseline runs on rank 0 at N = 1 only
         try:
-            # ~cpu_seconds of wall time on all host threads (cpu_seconds x threads core-seconds)
-            cus, thr, desc, _ = cpu_reference_sample(hq, hkv, chunk, off, b, ctx,
-                                                     target_s=args.cpu_seconds * (os.cpu_count() or 1))
+            cus, thr, desc, _ = cpu_reference_layer(hq, hkv, chunk, off, b, ctx)
             cpu = {"value": round(cus, 1), "unit": "us/layer", "cores": thr, "kind": "reference", "sample": desc}
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": "us/layer", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
     info = r["info"]
+    serial_best = sum(v[0] for v in r["best"].values()) if r["best"] else None
     line = {
         "metric": METRIC, "value": round(us, 2), "unit": "us/layer", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(r["t_fused"], 4), "higher_is_better": False,
@@ -486,6 +639,9 @@ def main():
         "speedup_vs_serial": round(r["t_serial"] / r["t_fused"], 3),
         "prefill_alone_us": round(r["t_pf"] * 1000, 2), "decode_alone_us": round(r["t_dec"] * 1000, 2),
         "fused_vs_max_alone": round(r["t_fused"] / max(r["t_pf"], r["t_dec"], 1e-9), 3),
+        "serial_best_us": round(serial_best * 1000, 2) if serial_best else None,
+        "speedup_vs_best_serial": round(serial_best / r["t_fused"], 3) if serial_best else None,
+        "serial_best": {k: {"us": round(v[0] * 1000, 2), "kernel": v[1]} for k, v in r["best"].items()},
         "combined_roofline_us": round(roof_us, 2), "combined_roofline_frac": round(roof_us / us, 4),
         "prefill_tensor_frac_alone": round(t_pf_roof / max(r["t_pf"] * 1000, 1e-9), 4) if chunk else None,
         "decode_hbm_frac_alone": round(t_dec_roof / max(r["t_dec"] * 1000, 1e-9), 4) if b else None,
@@ -505,6 +661,8 @@ def main():
         "e2e": {"value": round(r["t_e2e"] * 1000, 2), "unit": "us/layer", "h2d_bytes_per_step": r["h2d"],
                 "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": r["launches"] * args.steps,
+        "tp_check": r["tp_check"],
+        "attention_only_us": round(r["t_attn"] * 1000, 2),
         "clocks": r["clocks"],
     }
     print(json.dumps(line), flush=True)

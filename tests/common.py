@@ -120,3 +120,49 @@ def token_slots(wl):
         t = d.context_len - 1
         out.append((ix[ip[base + i] + t // 16], t % 16))
     return out
+
+
+def dense_layer(wl):
+    """The whole layer as float64 dense attention (torch, on the workload's device): O
+    [chunk + B][Hq][d] and natural-log LSE [chunk + B][Hq], prefill rows first.  K / V
+    are gathered from the paged pools through the block table (HND), so this checks the
+    sharded pools and tables too.  Semantics: attention.hpp:148-222 (row r of the chunk
+    sees keys [0, offset + r]) and :240-333 (a decode sees all ctx keys)."""
+    import torch
+
+    b, s = wl.batch, wl.batch.shape
+    G, d = s.group_size(), s.head_dim
+    ip = wl.page_indptr.tolist()
+
+    def kv(req):
+        ctx = wl.kv_lens[req]
+        pages = wl.page_indices[ip[req]:ip[req + 1]].long()
+        k = wl.k_pool[pages].permute(0, 2, 1, 3).reshape(-1, s.num_kv_heads, d)[:ctx].double()
+        v = wl.v_pool[pages].permute(0, 2, 1, 3).reshape(-1, s.num_kv_heads, d)[:ctx].double()
+        return k, v
+
+    def attend(q, k, v, limit):  # q [m][Hq][d], k/v [n][Hkv][d], row i sees keys <= limit[i]
+        kk = k.repeat_interleave(G, dim=1)
+        vv = v.repeat_interleave(G, dim=1)
+        sc = torch.einsum("mhd,nhd->hmn", q, kk) / s.scale
+        j = torch.arange(k.shape[0], device=q.device)
+        sc = sc.masked_fill(j[None, None, :] > limit[None, :, None], float("-inf"))
+        lse = torch.logsumexp(sc, dim=-1)
+        o = torch.einsum("hmn,nhd->mhd", torch.softmax(sc, dim=-1), vv)
+        return o, lse.transpose(0, 1)
+
+    os_, ls_ = [], []
+    base = 0
+    if b.prefill is not None:
+        k, v = kv(0)
+        c, off = b.prefill.chunk_size, b.prefill.position_offset
+        o, lse = attend(wl.q_prefill.double(), k, v, off + torch.arange(c, device=k.device))
+        os_.append(o)
+        ls_.append(lse)
+        base = 1
+    for i in range(len(b.decodes)):
+        k, v = kv(base + i)
+        o, lse = attend(wl.q_decode[i:i + 1].double(), k, v, torch.tensor([k.shape[0] - 1], device=k.device))
+        os_.append(o)
+        ls_.append(lse)
+    return torch.cat(os_), torch.cat(ls_)

@@ -1,0 +1,56 @@
+"""Small hybrid batches through every POD kernel path, for compute-sanitizer.
+
+    compute-sanitizer --tool memcheck  python tools/sanitize.py
+    compute-sanitizer --tool synccheck python tools/sanitize.py
+    compute-sanitizer --tool racecheck python tools/sanitize.py
+
+Covers the warp-specialised kernel (both pair-engine tile widths), the two-CTA
+kernel, the decode split merge, the prefill split merge, serial mode, and the
+KV append.  Outputs are checked loosely (finite) -- parity is the test suite's job;
+this script only drives the kernels under the sanitizer.
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+import paper_2410_18038_b200 as pkg  # noqa: E402
+from paper_2410_18038_b200._abi import POD_POLICY_COMPLEMENT, POD_POLICY_WARPSPEC  # noqa: E402
+from paper_2410_18038_b200.hybrid import PodAttention  # noqa: E402
+from paper_2410_18038_b200.workload import build_workload, make_batch  # noqa: E402
+
+
+def run(batch, opts, modes=("fused",)):
+    wl = build_workload(batch, device="cuda")
+    op = PodAttention(batch, options=opts)
+    for mode in modes:
+        out = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, mode=mode)
+        torch.cuda.synchronize()
+        for t in (out.o_prefill, out.o_decode):
+            if t is not None:
+                assert torch.isfinite(t.float()).all()
+    info = op.info
+    print(f"ok policy={info.policy} tile_keys={getattr(info, 'prefill_tile_keys', '?')} "
+          f"pctas={info.num_prefill_ctas} dctas={info.num_decode_ctas} modes={modes}", flush=True)
+
+
+def main():
+    shape = pkg.ModelShape(32, 8, 128, 128 ** 0.5)
+    small = make_batch(shape, chunk=128, offset=448, decode_ctx=[512, 300, 17, 1])
+    cases = [
+        (small, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC), ("fused", "serial")),
+        (small, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64), ("fused",)),
+        (small, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32, decode_splits=3), ("fused",)),
+        (small, pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT, split_wave_cap=4, decode_splits=2), ("fused", "serial")),
+    ]
+    for batch, opts, modes in cases:
+        run(batch, opts, modes)
+    print("sanitize driver done")
+
+
+if __name__ == "__main__":
+    main()
