@@ -536,7 +536,7 @@ def main():
     ap.add_argument("--impl", default="pod", choices=["pod", "reference"])
     ap.add_argument("--policy", type=int, default=8, help="POD_POLICY_*: 8 = AUTO (default), 7 = WARPSPEC, 3 = COMPLEMENT")
     ap.add_argument("--tile-mode", type=int, default=1)
-    ap.add_argument("--precision", type=int, default=0, help="0: prefill P as bf16 hi+lo (default), 1: single bf16")
+    ap.add_argument("--precision", type=int, default=2, help="POD_PRECISION_*: 0 prefill P as bf16 hi+lo, 1 single bf16, 2 fp16 P x fp16 V")
     ap.add_argument("--out-dtype", default="f32", choices=["f32", "bf16"],
                     help="element type of the attention outputs (LSE stays fp32); f32 = the reference's")
     ap.add_argument("--decode-splits", type=int, default=0)
@@ -649,7 +649,7 @@ def main():
         "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
                  "prefill_splits": info.prefill_splits, "decode_splits": info.decode_splits,
                  "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
-                 "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_p": {0: "bf16 hi+lo", 1: "bf16"}[args.precision], "out_dtype": args.out_dtype},
+                 "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_p": {0: "bf16 hi+lo", 1: "bf16", 2: "fp16 (V -> fp16 in smem)"}[args.precision], "out_dtype": args.out_dtype},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": {7: "pod_sm_kernel (+merge)"}.get(r["info"].policy, "pod_fused_kernel (+merge)"),

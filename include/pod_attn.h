@@ -159,8 +159,13 @@ enum {
 };
 
 enum {
-    POD_PRECISION_SPLIT = 0, /* P = bf16 hi + bf16 lo (two PV MMAs): ~16-bit P, default */
-    POD_PRECISION_FAST = 1   /* P rounded to one bf16 (FlashAttention-style)            */
+    POD_PRECISION_SPLIT = 0, /* P = bf16 hi + bf16 lo (two PV MMAs): ~16-bit P, any V     */
+    POD_PRECISION_FAST = 1,  /* P rounded to one bf16 (FlashAttention-style): error ~2e-3,
+                                at the north-star bar itself at 16K keys                  */
+    POD_PRECISION_F16PV = 2  /* default: P rounded to fp16 (11-bit), V tiles converted
+                                bf16 -> fp16 in shared memory, one fp16 PV MMA: error
+                                ~3e-4 of the output scale; exact V for |V| <= 65504 (larger
+                                V saturates: use SPLIT); fp16 pools: P fp16, no conversion */
 };
 
 /* What the plan decided, for benches and tests. */

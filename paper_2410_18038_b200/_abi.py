@@ -24,7 +24,7 @@ POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED, POD_POLICY_
 # 4-6 retired (measured slower; pod_attn_plan rejects them)
 POD_POLICY_WARPSPEC, POD_POLICY_AUTO = 7, 8
 POD_TILE_REFERENCE, POD_TILE_B200 = 0, 1
-POD_PRECISION_SPLIT, POD_PRECISION_FAST = 0, 1
+POD_PRECISION_SPLIT, POD_PRECISION_FAST, POD_PRECISION_F16PV = 0, 1, 2
 POD_OUT_F32, POD_OUT_BF16, POD_OUT_F16 = 0, 1, 2
 
 

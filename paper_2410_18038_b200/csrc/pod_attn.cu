@@ -130,6 +130,7 @@ struct RunParams {
     int32_t dec_tail_start;
     int32_t policy;
     int32_t p_split;  // prefill P as bf16 hi + lo (two PV MMAs)
+    int32_t p_f16;    // POD_PRECISION_F16PV: P as fp16, V stages converted to fp16 in smem (bf16 data)
     int32_t pf_tn64;  // warp-specialised kernel: 64-key single-S pair engine (prefill-dominant plans)
     const int32_t* dec_nsplit;  // KV splits of each decode request (min(splits, ctx), pod_plan.cpp)
     int32_t trace;         // debug builds (POD_TRACE_STAMPS): per-tile cycle stamps after the role log
@@ -191,7 +192,7 @@ __device__ __forceinline__ void prefill_issue_qk(uint32_t tmem_s, uint32_t sQ, u
 template <int kFmt>
 __device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint32_t sV,
                                                  bool accumulate, bool split) {
-    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);
+    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);  // kFmt: P and V format
 #pragma unroll
     for (int kk = 0; kk < kKvTile / 16; ++kk) {
         const uint64_t b = ptx::sw128_desc(sV + kk * 2048, kKvTile * 128, 1024);
@@ -208,6 +209,7 @@ __device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t tmem_
 //            hi = top 16 bits of p, lo = p - hi (exact in fp32) truncated; hi in
 //            [0,32), lo in [32,64); hi + lo keeps ~15 mantissa bits
 //   kMode 2: hi + lo rounded to nearest (fp16 inputs)
+//   kMode 3: one P rounded to fp16 (POD_PRECISION_F16PV), columns [0, kN/2)
 template <int kFmt, int kMode, int kN = kKvTile>
 __device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, float neg_m, uint32_t s_addr) {
     const float2 sl2v = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
@@ -230,6 +232,8 @@ __device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, 
                 const float2 lv = fadd2(make_float2(p0, p1), make_float2(-__uint_as_float(u0 & 0xffff0000u),
                                                                          -__uint_as_float(u1 & 0xffff0000u)));
                 lo[c / 2] = __byte_perm(__float_as_uint(lv.x), __float_as_uint(lv.y), 0x7632);
+            } else if constexpr (kMode == 3) {
+                hi[c / 2] = pack2<0>(p0, p1);
             } else {
                 hi[c / 2] = pack2<kFmt>(p0, p1);
                 if constexpr (kMode == 2) {
@@ -239,9 +243,40 @@ __device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, 
             }
         }
         ptx::tmem_st16(s_addr + 16 * hf, hi);
-        if constexpr (kMode != 0) ptx::tmem_st16(s_addr + kN / 2 + 16 * hf, lo);
+        if constexpr (kMode == 1 || kMode == 2) ptx::tmem_st16(s_addr + kN / 2 + 16 * hf, lo);
     }
     return lsum2.x + lsum2.y;
+}
+
+// POD_PRECISION_F16PV: one V stage converted bf16 -> fp16 in place in shared memory.
+// The conversion is elementwise, so the SW128 image stays the B operand layout of
+// the PV MMA, which then runs fp16 x fp16 with P rounded to fp16 (11-bit significand:
+// ~8x less P rounding error than bf16, one PV MMA instead of the hi + lo pair).
+// Exact for |v| in [2^-14, 65504] (bf16's 8-bit significand fits fp16's 11); smaller
+// magnitudes become fp16 subnormals (abs error <= 2^-25), larger ones saturate.
+// kThr threads (tid in [0, kThr)) share the stage; the generic -> async proxy fence
+// makes the stores visible to the tensor core once the caller's mbarrier arrival
+// (the P-full hand-off) is observed by the MMA issuer.
+__device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t w) {
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;"
+        : "=r"(r)
+        : "f"(__uint_as_float(w & 0xffff0000u)), "f"(__uint_as_float(w << 16)));
+    return r;
+}
+template <uint32_t kBytes, int kThr>
+__device__ __forceinline__ void v_stage_to_f16(uint32_t stage, int tid) {
+    static_assert(kBytes % (16u * kThr) == 0, "whole 16-byte chunks per thread");
+#pragma unroll
+    for (uint32_t i = 0; i < kBytes / (16u * kThr); ++i) {
+        const uint32_t a = stage + (i * kThr + static_cast<uint32_t>(tid)) * 16u;
+        uint32_t w0, w1, w2, w3;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(a));
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(bf16x2_to_f16x2(w0)),
+                     "r"(bf16x2_to_f16x2(w1)), "r"(bf16x2_to_f16x2(w2)), "r"(bf16x2_to_f16x2(w3))
+                     : "memory");
+    }
+    ptx::fence_proxy_async_smem();
 }
 
 struct BlockRange {
@@ -466,8 +501,12 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                     ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
                     trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 4);
                     ptx::tc_fence_after();
-                    prefill_issue_pv<kFmt>(tmem + kTmemO, tmem + kTmemS0 + st * kKvTile, sV + st * kKvStageBytes,
-                                           t > 0, p.p_split != 0);
+                    if (kFmt == 1 && p.p_f16)  // fp16 P x fp16 V (converted by the softmax warps)
+                        prefill_issue_pv<0>(tmem + kTmemO, tmem + kTmemS0 + st * kKvTile, sV + st * kKvStageBytes,
+                                            t > 0, false);
+                    else
+                        prefill_issue_pv<kFmt>(tmem + kTmemO, tmem + kTmemS0 + st * kKvTile,
+                                               sV + st * kKvStageBytes, t > 0, p.p_split != 0);
                     ptx::umma_commit_elect(b_pv + 8 * st);
                     ptx::umma_commit_elect(b_vempty + 8 * st);
                     trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 7);
@@ -564,13 +603,19 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                 // offset 0 keeps ex2(-inf) = 0 without a predicate per score.
                 const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
                 float lsum;
-                if (kFmt == 1 && p.p_split)
+                if (kFmt == 1 && p.p_f16)
+                    lsum = softmax_p_row<kFmt, 3>(s, p.sl2, neg_m, s_addr);
+                else if (kFmt == 1 && p.p_split)
                     lsum = softmax_p_row<kFmt, 1>(s, p.sl2, neg_m, s_addr);
                 else if (p.p_split)
                     lsum = softmax_p_row<kFmt, 2>(s, p.sl2, neg_m, s_addr);
                 else
                     lsum = softmax_p_row<kFmt, 0>(s, p.sl2, neg_m, s_addr);
                 l_run += lsum;
+                if (kFmt == 1 && p.p_f16) {  // V(t) -> fp16 before P(t) is handed to the MMA issuer
+                    ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
+                    v_stage_to_f16<kKvStageBytes, 128>(sV + st * kKvStageBytes, tid);
+                }
                 if (tid == 0) trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), t, 2);
                 // O is rescaled only when the reference max moved (rare, lazy): only
                 // then wait for PV_{t-1}, the newest MMA that writes O (PV_t cannot be
@@ -1350,6 +1395,7 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.dec_tail_start = static_cast<int32_t>(plan->dec_tail_start);
     p.policy = plan->opts.policy;
     p.p_split = plan->opts.precision == POD_PRECISION_SPLIT ? 1 : 0;
+    p.p_f16 = plan->opts.precision == POD_PRECISION_F16PV ? 1 : 0;
     p.pf_tn64 = plan->pf_tn64 ? 1 : 0;
     p.out_fmt = plan->opts.out_dtype;
     p.dec_nsplit = reinterpret_cast<const int32_t*>(ws + plan->ws.off_dec_nsplit);

@@ -542,7 +542,7 @@ void pod_options_default(pod_options* out) {
     out->split_wave_cap = 0;
     out->decode_splits = 0;
     out->tile_override = nullptr;
-    out->precision = POD_PRECISION_SPLIT;
+    out->precision = POD_PRECISION_F16PV;
     out->out_dtype = POD_OUT_F32;
     out->prefill_tile_keys = 0;
 }
@@ -573,6 +573,8 @@ pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const p
                   pol == POD_POLICY_COMPLEMENT || pol == POD_POLICY_WARPSPEC || pol == POD_POLICY_AUTO))
                 fail(POD_ERR_INVALID_ARGUMENT, "pod_options: policy must be a POD_POLICY_* value (4-6 are retired)");
         }
+        if (p->opts.precision < POD_PRECISION_SPLIT || p->opts.precision > POD_PRECISION_F16PV)
+            fail(POD_ERR_INVALID_ARGUMENT, "pod_options: precision must be a POD_PRECISION_* value");
         if (p->opts.out_dtype < POD_OUT_F32 || p->opts.out_dtype > POD_OUT_F16)
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: out_dtype must be a POD_OUT_* value");
         if (p->opts.prefill_tile_keys != 0 && p->opts.prefill_tile_keys != 32 && p->opts.prefill_tile_keys != 64)

@@ -141,7 +141,7 @@ __device__ __forceinline__ void issue_qk32(uint32_t tmem_s, uint32_t tmem_q, uin
 }
 // O (+)= P V for one 32-key tile: A = P (TMEM; hi in columns [0,16), lo in [16,32)),
 // B = V (smem, MN-major SW128 [d-half][32 keys][64 d]), N = 128.
-template <int kFmt>
+template <int kFmt>  // kFmt: format of P and V (fp16 under POD_PRECISION_F16PV)
 __device__ __forceinline__ void issue_pv32(uint32_t tmem_o, uint32_t tmem_p, uint32_t sV, bool accumulate,
                                            bool split) {
     if (POD_SM_NOMMA) return;  // timing experiment only
@@ -244,8 +244,12 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         }
     } else if (!kDualMma && warp == kMmaWarp) {
         // the P-split flag is hoisted out of the loop (a runtime branch per PV cost ~7 %)
-        auto mma_issuer = [&](auto split_c) {
-            constexpr bool kSplit = decltype(split_c)::value;
+        // kPv: 0 = bf16 hi + lo (two PV MMAs), 1 = one P in the data format, 2 = fp16 P x
+        // fp16 V (POD_PRECISION_F16PV: block A's softmax warps convert V(t) before P_A(t))
+        auto mma_issuer = [&](auto pv_c) {
+            constexpr int kPv = decltype(pv_c)::value;
+            constexpr bool kSplit = kPv == 0;
+            constexpr int kPvFmt = kPv == 2 ? 0 : kFmt;
             // -------------------------------------------------- MMA issuer --
             // Per block, QK_X(t+2) reuses the S buffer of tile t after PV_X(t) (in-order
             // pipe), so the softmax of tile t+1 overlaps PV_X(t) and QK_X(t+2); the two
@@ -276,8 +280,8 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                     if (!POD_SM_EXP_NOVWAIT) sm_wait<POD_SM_MMA_SLEEP>(bar(kBarVF + st), (gg / kNS) & 1);
                     trace_stamp(p, first, t < 128 ? 384 + t : 9999, 4);
                     ptx::tc_fence_after();
-                    issue_pv32<kFmt>(tmem + kOA, tmem + kSA + 32 * bA, sV + (POD_SM_EXP_ST0 ? 0 : st) * kStage, t > 0,
-                                     kSplit);
+                    issue_pv32<kPvFmt>(tmem + kOA, tmem + kSA + 32 * bA, sV + (POD_SM_EXP_ST0 ? 0 : st) * kStage,
+                                       t > 0, kSplit);
                     trace_stamp(p, first, t < 128 ? 384 + t : 9999, 5);
                     if (pv_commit(t)) ptx::umma_commit_elect(bar(kBarPV + bA));
                     trace_stamp(p, first, t, 5);
@@ -294,8 +298,8 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                         sm_wait<POD_SM_MMA_SLEEP>(bar(kBarP + 2 + bB), (nB >> 1) & 1);
                         trace_stamp(p, first, t < 128 ? 384 + t : 9999, 7);
                         ptx::tc_fence_after();
-                        issue_pv32<kFmt>(tmem + kOB, tmem + kSB + 32 * bB, sV + (POD_SM_EXP_ST0 ? 0 : st) * kStage, t > 0,
-                                         kSplit);
+                        issue_pv32<kPvFmt>(tmem + kOB, tmem + kSB + 32 * bB, sV + (POD_SM_EXP_ST0 ? 0 : st) * kStage,
+                                           t > 0, kSplit);
                         if (pv_commit(t)) ptx::umma_commit_elect(bar(kBarPV + 2 + bB));
                         if (more) {
                             issue_qk32<kFmt>(tmem + kSB + 32 * bB, tmem + kQB, sK + (POD_SM_EXP_ST0 ? 0 : st2) * kStage);
@@ -313,10 +317,12 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                 }
             }
         };
-        if (POD_SM_EXP_SPLITCONST || p.p_split != 0)
-            mma_issuer(std::true_type{});
+        if (kFmt == 1 && p.p_f16)
+            mma_issuer(std::integral_constant<int, 2>{});
+        else if (POD_SM_EXP_SPLITCONST || p.p_split != 0)
+            mma_issuer(std::integral_constant<int, 0>{});
         else
-            mma_issuer(std::false_type{});
+            mma_issuer(std::integral_constant<int, 1>{});
     } else if (kDualMma && (warp == kMmaWarp || warp == kMmaWarpB)) {
         // ------------------------------------------ MMA issuers (per block) --
         // Block X: QK_X(t+2) reuses the S buffer of tile t after PV_X(t) (in-order
@@ -477,13 +483,20 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             }
             const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
             float lsum;
-            if (kFmt == 1 && p.p_split)
+            if (kFmt == 1 && p.p_f16)
+                lsum = softmax_p_row<kFmt, 3, kTN>(s, p.sl2, neg_m, s_addr);
+            else if (kFmt == 1 && p.p_split)
                 lsum = softmax_p_row<kFmt, 1, kTN>(s, p.sl2, neg_m, s_addr);
             else if (p.p_split)
                 lsum = softmax_p_row<kFmt, 2, kTN>(s, p.sl2, neg_m, s_addr);
             else
                 lsum = softmax_p_row<kFmt, 0, kTN>(s, p.sl2, neg_m, s_addr);
             l_run += lsum;
+            if (kFmt == 1 && p.p_f16 && X == 0) {  // block A converts V(t) before P_A(t) (PV_B(t) follows PV_A(t))
+                const int gg = s0.g + t, st = gg % kNS;
+                ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
+                v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
+            }
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
@@ -591,6 +604,10 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
     const uint32_t bar0 = sbase + kOffBars;
     auto bar = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
     const uint32_t sK = sbase + kOffKs, sV = sbase + kOffKs + kNSK * kStage;
+    // debug trace (POD_TRACE_STAMPS builds): CTA 0's first item; row t = block A + MMA A,
+    // row 384 + t = block B + MMA B + producer (tools/profile_run.py --trace64)
+    const int first = s0.n[0] == 0 ? 0 : 1;
+    auto rowB = [&](int t) { return t < 384 ? 384 + t : 9999; };
 
     if (warp == kProdWarp) {
         // ------------------------------------------------ TMA producer --
@@ -601,14 +618,18 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             if (gg >= kNSK) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarKE + sk), ((gg / kNSK) - 1) & 1);
             ptx::mbar_arrive_expect_tx_elect(bar(kBarKF + sk), kStage);
             sm64::load_tile64(p, tmk, sK + sk * kStage, bar(kBarKF + sk), kt0 + t * kTN, job.kv_head, ids);
+            if (lane == 0) trace_stamp(p, first, rowB(t), 6);
             if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarVE + st), ((gg / kNS) - 1) & 1);
             ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
             sm64::load_tile64(p, tmv, sV + st * kStage, bar(kBarVF + st), kt0 + t * kTN, job.kv_head, ids);
+            if (lane == 0) trace_stamp(p, first, rowB(t), 7);
         }
     } else if (warp == kMmaWarp) {
         // -------------------------------------------------- MMA issuer --
-        auto mma_issuer = [&](auto split_c) {
-            constexpr bool kSplit = decltype(split_c)::value;
+        auto mma_issuer = [&](auto pv_c) {  // kPv as in prefill_item_sm
+            constexpr int kPv = decltype(pv_c)::value;
+            constexpr bool kSplit = kPv == 0;
+            constexpr int kPvFmt = kPv == 2 ? 0 : kFmt;
             if (nt == 0) return;
             ptx::mbar_wait(bar(0), s0.nq[0] & 1);
             if (hasB) ptx::mbar_wait(bar(1), s0.nq[1] & 1);
@@ -633,16 +654,17 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
                     if (X == 1 && !hasB) break;
                     const int n = s0.n[X] + t;
                     ptx::mbar_wait(bar(kBarP + X), n & 1);
+                    if (lane == 0) trace_stamp(p, first, X ? rowB(t) : t, 4);
                     if (X == 0) ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
                     ptx::tc_fence_after();
                     if (POD_SM64_BATCHED_PV) {
-                        constexpr uint32_t idesc_pv = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);
+                        constexpr uint32_t idesc_pv = ptx::idesc_f16(kPvFmt, kMBlock, kHeadDim, 1);
                         ptx::umma_pv64_elect<kSplit>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA),
                                                      ptx::sw128_desc(sV + st * kStage, kTN * 128, 1024), idesc_pv,
                                                      t > 0 ? 1u : 0u);
                     } else {
-                        prefill_issue_pv<kFmt>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA), sV + st * kStage,
-                                               t > 0, kSplit);
+                        prefill_issue_pv<kPvFmt>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA), sV + st * kStage,
+                                                 t > 0, kSplit);
                     }
                     if (last) ptx::umma_commit_elect(bar(kBarPV + X));
                     if (more) {
@@ -653,15 +675,18 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
                         sm64::issue_qk64<kFmt>(tmem + (X ? kSB : kSA), tmem + (X ? kQB : kQA), sK + sk1 * kStage);
                         ptx::umma_commit_elect(bar(kBarS + X));
                     }
+                    if (lane == 0) trace_stamp(p, first, X ? rowB(t) : t, 5);
                 }
                 ptx::umma_commit_elect(bar(kBarVE + st));          // V(t): both PVs issued above
                 if (more) ptx::umma_commit_elect(bar(kBarKE + sk1));  // K(t+1): both QKs
             }
         };
-        if (p.p_split != 0)
-            mma_issuer(std::true_type{});
+        if (kFmt == 1 && p.p_f16)
+            mma_issuer(std::integral_constant<int, 2>{});
+        else if (p.p_split != 0)
+            mma_issuer(std::integral_constant<int, 0>{});
         else
-            mma_issuer(std::false_type{});
+            mma_issuer(std::integral_constant<int, 1>{});
     } else if (warp < kProdWarp) {
         // ------------------------------------ softmax (4 warps per block) --
         const int X = warp >> 2;  // block
@@ -718,7 +743,9 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
         float m_run = -INFINITY, l_run = 0.f;
         for (int t = 0; t < nt; ++t) {
             const int n = s0.n[X] + t;
+            if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 0);
             ptx::mbar_wait(bar(kBarS + X), n & 1);  // also: PV_X(t-1) complete
+            if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 1);
             ptx::tc_fence_after();
             float s[kTN];
             ptx::tmem_ld32(s_addr, *reinterpret_cast<float(*)[32]>(&s[0]));
@@ -754,16 +781,25 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             }
             const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
             float lsum;
-            if (kFmt == 1 && p.p_split)
+            if (kFmt == 1 && p.p_f16)
+                lsum = softmax_p_row<kFmt, 3, kTN>(s, p.sl2, neg_m, s_addr);
+            else if (kFmt == 1 && p.p_split)
                 lsum = softmax_p_row<kFmt, 1, kTN>(s, p.sl2, neg_m, s_addr);
             else if (p.p_split)
                 lsum = softmax_p_row<kFmt, 2, kTN>(s, p.sl2, neg_m, s_addr);
             else
                 lsum = softmax_p_row<kFmt, 0, kTN>(s, p.sl2, neg_m, s_addr);
             l_run += lsum;
+            if (kFmt == 1 && p.p_f16 && X == 0) {  // block A converts V(t) before P_A(t) (PV_B(t) follows PV_A(t))
+                const int gg = s0.g + t, st = gg % kNS;
+                ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
+                v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
+            }
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
+            if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 2);
+            if (lane == 0 && q == 3) trace_stamp(p, first, X ? rowB(t) : t, 3);
             if (lane == 0) ptx::mbar_arrive(bar(kBarP + X));
         }
         ptx::mbar_wait(bar(kBarPV + X), s0.npv[X][0] & 1);  // the last PV (commit covers all)

@@ -223,7 +223,7 @@ class PlanOptions:
     split_wave_cap: int = 0
     decode_splits: int = 0
     tile_override: Optional[TileConfig] = None
-    precision: int = _abi.POD_PRECISION_SPLIT
+    precision: int = _abi.POD_PRECISION_F16PV
     out_dtype: int = _abi.POD_OUT_F32
     prefill_tile_keys: int = 0  # warp-specialised pair engine: 0 = auto, 32 or 64
 

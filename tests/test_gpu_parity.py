@@ -15,7 +15,7 @@ from oracle import pyoracle as O
 from paper_2410_18038_b200._abi import (POD_DTYPE_FP16, POD_KV_NHD, POD_POLICY_CLAMPED, POD_POLICY_COMPLEMENT,
                                         POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL,
                                         POD_POLICY_WARPSPEC,
-                                        POD_PRECISION_FAST, POD_TILE_B200, POD_TILE_REFERENCE)
+                                        POD_PRECISION_F16PV, POD_PRECISION_FAST, POD_PRECISION_SPLIT, POD_TILE_B200, POD_TILE_REFERENCE)
 from paper_2410_18038_b200.workload import build_workload, make_batch
 from tests.common import LSE_TOL, O_TOL, compare_decode, compare_prefill
 
@@ -85,6 +85,27 @@ def test_fast_precision_bf16_p_within_loose_bound():
     wl, _, out = _run(batch, options=pkg.PlanOptions(precision=POD_PRECISION_FAST))
     eo, el = compare_prefill(wl, out.o_prefill.cpu().numpy(), out.lse_prefill.cpu().numpy())
     assert eo <= 2.0 ** -8 and el <= LSE_TOL
+
+
+@pytest.mark.parametrize("precision", [POD_PRECISION_F16PV, POD_PRECISION_SPLIT])
+@pytest.mark.parametrize("kernel", ["complement", 32, 64])
+@pytest.mark.parametrize("q_scale", [1.0, 8.0])
+@pytest.mark.parametrize("name", ["hybrid_gqa4", "page_edges", "gqa8", "mha", "prefill_only"])
+def test_precision_modes_match_oracle(precision, kernel, q_scale, name):
+    """POD_PRECISION_F16PV (default): P rounded to fp16 and each V tile converted bf16 ->
+    fp16 in shared memory (exact for |V| <= 65504), one PV MMA.  POD_PRECISION_SPLIT: P
+    as bf16 hi + lo, two PV MMAs.  Both are held to the default 2e-3 bar AND to a 3x
+    tighter one: fp16's 11-bit P keeps the error near 2^-11 / sqrt(keys) of the output
+    scale (~3e-4 measured; SPLIT ~3e-6; one bf16 P sits at ~2e-3, the bar itself)."""
+    _need_gpu()
+    hq, hkv, chunk, off, dec = CASES[name]
+    batch = make_batch(pkg.ModelShape(hq, hkv, 128, SCALE), chunk=chunk, offset=off, decode_ctx=dec)
+    opts = (pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT, precision=precision) if kernel == "complement"
+            else pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=kernel, precision=precision))
+    wl, _, out = _run(batch, options=opts, q_scale=q_scale)
+    _check(wl, out)
+    eo, el = compare_prefill(wl, out.o_prefill.cpu().numpy(), out.lse_prefill.cpu().numpy())
+    assert eo <= 6e-4 and el <= 1e-4, (eo, el)
 
 
 @pytest.mark.parametrize("policy", [POD_POLICY_FIFTY_FIFTY, POD_POLICY_PROPORTIONAL, POD_POLICY_CLAMPED,

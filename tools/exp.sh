@@ -4,7 +4,7 @@
 cfg=${1:-c2_b64}; shift
 for v in "$@"; do
   IFS=: read -r prec pf pol swc ds <<< "$v"
-  line=$(timeout 300 python bench.py --config $cfg --precision $prec --policy ${pol:-3} --split-wave-cap ${swc:-0} --decode-splits ${ds:-0} --no-cpu-baseline --steps 10 2>/dev/null | tail -1)
+  line=$(timeout 300 python bench.py --config $cfg --precision $prec --policy ${pol:-8} --split-wave-cap ${swc:-0} --decode-splits ${ds:-0} --no-cpu-baseline --no-serial-search --steps 10 2>/dev/null | tail -1)
   python - "$v" "$line" <<'PY'
 import json,sys
 v=sys.argv[1]
