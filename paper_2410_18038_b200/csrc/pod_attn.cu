@@ -156,6 +156,30 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     return *reinterpret_cast<float2*>(&d);
 }
 
+// 2^x on the FMA pipe for a pair (FA4-style MUFU offload): x = j + f with j = round(x)
+// (the 1.5 * 2^23 magic add), f in [-0.5, 0.5], 2^f by a degree-4 minimax polynomial
+// (max rel. error 2.6e-6, far below fp16 P's 2^-12), 2^j added into the exponent field.
+// x is clamped at -126 (masked scores, x = -inf, give 2^-126: 0 once P is rounded to
+// 16 bits; their share of the fp32 row sum is < 1e-37 relative).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 t = fadd2(x, magic);
+    const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));  // round(x)
+    const float2 f = ffma2(r, make_float2(-1.f, -1.f), x);                // x - round(x)
+    float2 q = ffma2(make_float2(0.009570068679749966f, 0.009570068679749966f), f,
+                     make_float2(0.055917806923389435f, 0.055917806923389435f));
+    q = ffma2(q, f, make_float2(0.240247443318367f, 0.240247443318367f));
+    q = ffma2(q, f, make_float2(0.6931218504905701f, 0.6931218504905701f));
+    q = ffma2(q, f, make_float2(0.9999992847442627f, 0.9999992847442627f));
+    return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                       __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
+}
+#ifndef POD_EXP_POLY
+#define POD_EXP_POLY 0  // pairs per 8 whose exp2 runs on the FMA pipe (0 = all on MUFU; 2-4 measured
+                        // 1-3 % slower on B200: the softmax is not MUFU-bound)
+#endif
+
 template <int kFmt>
 __device__ __forceinline__ uint32_t pack2(float x, float y) {
     if constexpr (kFmt == 1) {
@@ -188,14 +212,16 @@ __device__ __forceinline__ void prefill_issue_qk(uint32_t tmem_s, uint32_t sQ, u
 }
 
 // O (+)= P V with P (bf16, 128 x 64) read from TMEM (2 values per 32-bit column,
-// 8 columns per K=16 step) and V (64 keys x 128 d, MN-major SW128) from smem.
+// 8 columns per K=16 step) and V (64 keys x 128 d, MN-major SW128) from smem in the
+// page-major image of prefill_load_v_pages: K-step kk = head-page kk (4 KB), the two
+// 64-d halves 2 KB apart (LBO).
 template <int kFmt>
 __device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint32_t sV,
                                                  bool accumulate, bool split) {
     constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);  // kFmt: P and V format
 #pragma unroll
     for (int kk = 0; kk < kKvTile / 16; ++kk) {
-        const uint64_t b = ptx::sw128_desc(sV + kk * 2048, kKvTile * 128, 1024);
+        const uint64_t b = ptx::sw128_desc(sV + kk * 4096, 2048, 1024);
         ptx::umma_f16_ts_elect(tmem_o, tmem_p + kk * 8, b, idesc, (accumulate || kk > 0) ? 1u : 0u);
         if (split) ptx::umma_f16_ts_elect(tmem_o, tmem_p + 32 + kk * 8, b, idesc, 1u);  // + P_lo V
     }
@@ -213,7 +239,7 @@ __device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t tmem_
 template <int kFmt, int kMode, int kN = kKvTile>
 __device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, float neg_m, uint32_t s_addr) {
     const float2 sl2v = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
-    float2 lsum2 = make_float2(0.f, 0.f);
+    float2 lsum2 = make_float2(0.f, 0.f), lsum2b = make_float2(0.f, 0.f);  // two chains
 #pragma unroll
     for (int hf = 0; hf < kN / 32; ++hf) {
         uint32_t hi[16], lo[16];
@@ -223,9 +249,20 @@ __device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, 
 #if POD_EXP_FAKE  // timing experiment only: exp2 replaced by one FMA-pipe op
             const float p0 = x.x * 0.5f, p1 = x.y * 0.5f;
 #else
-            const float p0 = ptx::ex2(x.x), p1 = ptx::ex2(x.y);
+            float p0, p1;
+            if (POD_EXP_POLY > 0 && (c / 2) % 8 >= 8 - POD_EXP_POLY) {
+                const float2 e = ex2_poly2(x);
+                p0 = e.x;
+                p1 = e.y;
+            } else {
+                p0 = ptx::ex2(x.x);
+                p1 = ptx::ex2(x.y);
+            }
 #endif
-            lsum2 = fadd2(lsum2, make_float2(p0, p1));
+            if (c & 2)
+                lsum2b = fadd2(lsum2b, make_float2(p0, p1));
+            else
+                lsum2 = fadd2(lsum2, make_float2(p0, p1));
             if constexpr (kMode == 1) {
                 const uint32_t u0 = __float_as_uint(p0), u1 = __float_as_uint(p1);
                 hi[c / 2] = __byte_perm(u0, u1, 0x7632);
@@ -245,7 +282,21 @@ __device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, 
         ptx::tmem_st16(s_addr + 16 * hf, hi);
         if constexpr (kMode == 1 || kMode == 2) ptx::tmem_st16(s_addr + kN / 2 + 16 * hf, lo);
     }
-    return lsum2.x + lsum2.y;
+    return (lsum2.x + lsum2.y) + (lsum2b.x + lsum2b.y);
+}
+
+// Row max of kN scores as a tree (depth log3 kN of FMNMX3 instead of a kN/2-long chain).
+template <int kN>
+__device__ __forceinline__ float row_max(const float (&s)[kN]) {
+    float m[kN / 2];
+#pragma unroll
+    for (int c = 0; c < kN / 2; ++c) m[c] = fmaxf(s[2 * c], s[2 * c + 1]);
+#pragma unroll
+    for (int w = kN / 4; w >= 1; w /= 2) {
+#pragma unroll
+        for (int c = 0; c < w; ++c) m[c] = fmaxf(m[c], m[c + w]);
+    }
+    return m[0];
 }
 
 // POD_PRECISION_F16PV: one V stage converted bf16 -> fp16 in place in shared memory.
@@ -332,6 +383,22 @@ __device__ __forceinline__ void prefill_load_kv_tile(const RunParams& p, const C
                 ptx::tma_load_4d_elect(d, tm, bar, dh * 64, kv_head, 0, phys);
         }
     }
+}
+
+// V of one prefill tile as one 4 KB TMA box per head-page (the decode role's 5-D
+// view: (64 d, 16 slots, 2 d-halves, head, page)): smem [page][d-half][16 keys][64 d],
+// SW128.  Half the TMA issues of the K layout ([d-half][keys][64 d], two boxes per
+// page), which the QK MMA needs for a uniform 8-key group stride along N; the PV MMA
+// reads V with K = keys, one head-page per K=16 step (LBO = 2 KB between the d-halves,
+// K-steps 4 KB apart), so the page-major image serves it directly.
+template <int kPages>
+__device__ __forceinline__ void prefill_load_v_pages(const CUtensorMap* tdv, uint32_t dst, uint32_t bar, int kt,
+                                                     int kv_head, const PageIds& ids) {
+    int phys[kPages];
+#pragma unroll
+    for (int pg = 0; pg < kPages; ++pg) phys[pg] = ids.get(min(kt / 16 + pg, ids.n - 1));
+#pragma unroll
+    for (int pg = 0; pg < kPages; ++pg) ptx::tma_load_5d_elect(dst + pg * 4096, tdv, bar, 0, 0, 0, kv_head, phys[pg]);
 }
 
 // Prefill role: one CTA = one CtaTask of decompose_prefill (q tile x kv head x kv
@@ -469,8 +536,8 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                         if (gg >= 2) ptx::mbar_wait_relaxed<>(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t - 1, 6);
                         ptx::mbar_arrive_expect_tx_elect(b_vfull + 8 * st, kKvStageBytes);
-                        prefill_load_kv_tile(p, tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
-                                             br.kt0 + (t - 1) * kKvTile, job.kv_head, pvi);
+                        prefill_load_v_pages<kKvTile / 16>(tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
+                                                           br.kt0 + (t - 1) * kKvTile, job.kv_head, pvi);
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t - 1, 7);
                     }
                 }
@@ -585,9 +652,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                     for (int c = 0; c < kKvTile; ++c)
                         if (c < lo || c >= hi) s[c] = -INFINITY;
                 }
-                float tmax = s[0];
-#pragma unroll
-                for (int c = 1; c < kKvTile; c += 2) tmax = fmaxf(tmax, fmaxf(s[c], s[min(c + 1, kKvTile - 1)]));
+                const float tmax = row_max<kKvTile>(s);
                 const float m_new = fmaxf(m_run, tmax * p.sl2);
                 // lazy rescale (only when the max grows by > 2^8): exact algebra,
                 // the stale reference max bounds p by 256.
@@ -1167,7 +1232,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncthreads();  // role[] is rewritten by the next claim
         if (op < 0) break;
         if (op == 0) {
-            prefill_item<kFmt>(p, &tmq, &tmk, &tmv, id, smem, tmem, ps);
+            prefill_item<kFmt>(p, &tmq, &tmk, &tdv, id, smem, tmem, ps);
         } else {
             if (warp < kDecWarpsK)
                 decode_item<G, kFmt, kDecWarpsK, kDecStages>(p, &tdk, &tdv, id, warp, sbase, sbase + kOffDecBar,

@@ -147,7 +147,7 @@ __device__ __forceinline__ void issue_pv32(uint32_t tmem_o, uint32_t tmem_p, uin
     if (POD_SM_NOMMA) return;  // timing experiment only
     constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kHeadDim, 1);
     static_assert(kTN == 32, "umma_pv32_elect: two K-steps, lo part 16 columns after hi");
-    const uint64_t b = ptx::sw128_desc(sV, kTN * 128, 1024);
+    const uint64_t b = ptx::sw128_desc(sV, 2048, 1024);  // page-major V (prefill_load_v_pages)
     if (split)
         ptx::umma_pv32_elect<true>(tmem_o, tmem_p, b, idesc, accumulate ? 1u : 0u);
     else
@@ -175,7 +175,7 @@ __device__ __forceinline__ void load_tile32(const RunParams& p, const CUtensorMa
 // One prefill item of the warp-specialised engine: up to two 128-row M-blocks of
 // one (q tile, KV head, KV split) CtaTask over the same 32-key K/V tiles.
 template <int kFmt>
-__device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv, int item,
+__device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv /* 5-D page map */, int item,
                                 uint32_t sbase, uint32_t tmem, sm3::PfState& ps, int warp, int lane) {
     using namespace sm3;
     const PrefillCta job = p.pctas[item];
@@ -238,7 +238,8 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                     if (lane == 0) ptx::mbar_arrive(bar(kBarVF + st));
                 } else {
                     ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
-                    load_tile32(p, tmv, sV + st * kStage, bar(kBarVF + st), kt0 + (t - 1) * kTN, job.kv_head, ids);
+                    prefill_load_v_pages<2>(tmv, sV + st * kStage, bar(kBarVF + st), kt0 + (t - 1) * kTN, job.kv_head,
+                                            ids);
                 }
             }
         }
@@ -428,6 +429,15 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(bar(X));
         }
+        // POD_PRECISION_F16PV: block A converts V(t) to fp16 in smem before its P(t)
+        // arrival (PV_B(t) is issued after PV_A(t)); V(t+1) is converted right after
+        // P(t) is handed over, while the next S is computed, off the critical path.
+        auto v_to_f16 = [&](int t) {
+            const int gg = s0.g + t, st = gg % kNS;
+            ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
+            v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
+        };
+        if (kFmt == 1 && p.p_f16 && X == 0) v_to_f16(0);
         float m_run = -INFINITY, l_run = 0.f;
         for (int t = 0; t < nt; ++t) {
             const int n = s0.n[X] + t, b = n & 1;
@@ -452,9 +462,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                 for (int c = 0; c < kTN; ++c)
                     if (c < lo || c >= hi) s[c] = -INFINITY;
             }
-            float tmax = s[0];
-#pragma unroll
-            for (int c = 1; c < kTN; c += 2) tmax = fmaxf(tmax, fmaxf(s[c], s[min(c + 1, kTN - 1)]));
+            const float tmax = row_max<kTN>(s);
             const float m_new = fmaxf(m_run, tmax * p.sl2);
             const bool need = m_new > m_run + 8.f;  // lazy rescale (see prefill_item)
             const float m_use = need ? m_new : m_run;
@@ -492,17 +500,13 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             else
                 lsum = softmax_p_row<kFmt, 0, kTN>(s, p.sl2, neg_m, s_addr);
             l_run += lsum;
-            if (kFmt == 1 && p.p_f16 && X == 0) {  // block A converts V(t) before P_A(t) (PV_B(t) follows PV_A(t))
-                const int gg = s0.g + t, st = gg % kNS;
-                ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
-                v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
-            }
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0 && q == 0) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 2);
             if (lane == 0 && q == 3) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 3);
             if (lane == 0) ptx::mbar_arrive(bar(kBarP + 2 * X + b));
+            if (kFmt == 1 && p.p_f16 && X == 0 && t + 1 < nt) v_to_f16(t + 1);  // off the P(t) -> PV(t) path
         }
         // ------------------------------------------------- epilogue --
         {  // the last PV's commit covers every earlier MMA of this thread
@@ -538,7 +542,25 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
 // in the in-order pipe, and S_X(t) complete implies PV_X(t-1) complete, so the
 // lazy O rescale needs no extra wait.  K and V rings: 2 stages of 16 KB each with
 // separate empty barriers (K freed after both QKs, V after both PVs).
+#ifndef POD_SM64_SPIN_MMA
+#define POD_SM64_SPIN_MMA 0  // MMA issuer polls P_X with test_wait (no suspend) instead of try_wait
+#endif
+#ifndef POD_SM64_SPIN_SOFTMAX
+#define POD_SM64_SPIN_SOFTMAX 0  // softmax warps poll S_X with test_wait
+#endif
 namespace sm64 {
+__device__ __forceinline__ void wait_mma(uint32_t bar, uint32_t parity) {
+    if (POD_SM64_SPIN_MMA)
+        ptx::mbar_wait_spin(bar, parity);
+    else
+        ptx::mbar_wait(bar, parity);
+}
+__device__ __forceinline__ void wait_softmax(uint32_t bar, uint32_t parity) {
+    if (POD_SM64_SPIN_SOFTMAX)
+        ptx::mbar_wait_spin(bar, parity);
+    else
+        ptx::mbar_wait(bar, parity);
+}
 constexpr int kTN = 64;
 constexpr int kNS = 2;                      // V stages
 constexpr int kNSK = POD_SM64_KSTAGES;      // K stages
@@ -570,7 +592,7 @@ __device__ __forceinline__ void issue_qk64(uint32_t tmem_s, uint32_t tmem_q, uin
 }  // namespace sm64
 
 template <int kFmt>
-__device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv, int item,
+__device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv /* 5-D page map */, int item,
                                   uint32_t sbase, uint32_t tmem, sm3::PfState& ps, int warp, int lane) {
     using namespace sm3;
     using sm64::kTN;
@@ -621,7 +643,7 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             if (lane == 0) trace_stamp(p, first, rowB(t), 6);
             if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarVE + st), ((gg / kNS) - 1) & 1);
             ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
-            sm64::load_tile64(p, tmv, sV + st * kStage, bar(kBarVF + st), kt0 + t * kTN, job.kv_head, ids);
+            prefill_load_v_pages<4>(tmv, sV + st * kStage, bar(kBarVF + st), kt0 + t * kTN, job.kv_head, ids);
             if (lane == 0) trace_stamp(p, first, rowB(t), 7);
         }
     } else if (warp == kMmaWarp) {
@@ -653,14 +675,14 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
                 for (int X = 0; X < 2; ++X) {
                     if (X == 1 && !hasB) break;
                     const int n = s0.n[X] + t;
-                    ptx::mbar_wait(bar(kBarP + X), n & 1);
+                    sm64::wait_mma(bar(kBarP + X), n & 1);
                     if (lane == 0) trace_stamp(p, first, X ? rowB(t) : t, 4);
                     if (X == 0) ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
                     ptx::tc_fence_after();
                     if (POD_SM64_BATCHED_PV) {
                         constexpr uint32_t idesc_pv = ptx::idesc_f16(kPvFmt, kMBlock, kHeadDim, 1);
                         ptx::umma_pv64_elect<kSplit>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA),
-                                                     ptx::sw128_desc(sV + st * kStage, kTN * 128, 1024), idesc_pv,
+                                                     ptx::sw128_desc(sV + st * kStage, 2048, 1024), idesc_pv,
                                                      t > 0 ? 1u : 0u);
                     } else {
                         prefill_issue_pv<kPvFmt>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA), sV + st * kStage,
@@ -740,17 +762,25 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(bar(X));
         }
+        // POD_PRECISION_F16PV: as in prefill_item_sm (V(t+1) converted after P(t) is handed over)
+        auto v_to_f16 = [&](int t) {
+            const int gg = s0.g + t, st = gg % kNS;
+            ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
+            v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
+        };
+        if (kFmt == 1 && p.p_f16 && X == 0) v_to_f16(0);
         float m_run = -INFINITY, l_run = 0.f;
         for (int t = 0; t < nt; ++t) {
             const int n = s0.n[X] + t;
             if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 0);
-            ptx::mbar_wait(bar(kBarS + X), n & 1);  // also: PV_X(t-1) complete
+            sm64::wait_softmax(bar(kBarS + X), n & 1);  // also: PV_X(t-1) complete
             if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 1);
             ptx::tc_fence_after();
             float s[kTN];
             ptx::tmem_ld32(s_addr, *reinterpret_cast<float(*)[32]>(&s[0]));
             ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
             ptx::tmem_wait_ld();
+            if (lane == 0 && q == 0 && X == 0) trace_stamp(p, first, t, 6);
             const int kb = kt0 + t * kTN;
             const int lo = max(job.kv_begin - kb, 0);
             const int hi = row_ok ? min(min(job.kv_end, vis + 1) - kb, kTN) : 0;
@@ -759,9 +789,7 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
                 for (int c = 0; c < kTN; ++c)
                     if (c < lo || c >= hi) s[c] = -INFINITY;
             }
-            float tmax = s[0];
-#pragma unroll
-            for (int c = 1; c < kTN; c += 2) tmax = fmaxf(tmax, fmaxf(s[c], s[min(c + 1, kTN - 1)]));
+            const float tmax = row_max<kTN>(s);
             const float m_new = fmaxf(m_run, tmax * p.sl2);
             const bool need = m_new > m_run + 8.f;  // lazy rescale (see prefill_item)
             const float m_use = need ? m_new : m_run;
@@ -790,17 +818,14 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             else
                 lsum = softmax_p_row<kFmt, 0, kTN>(s, p.sl2, neg_m, s_addr);
             l_run += lsum;
-            if (kFmt == 1 && p.p_f16 && X == 0) {  // block A converts V(t) before P_A(t) (PV_B(t) follows PV_A(t))
-                const int gg = s0.g + t, st = gg % kNS;
-                ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
-                v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
-            }
+            if (lane == 0 && q == 0 && X == 0) trace_stamp(p, first, t, 7);
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 2);
             if (lane == 0 && q == 3) trace_stamp(p, first, X ? rowB(t) : t, 3);
             if (lane == 0) ptx::mbar_arrive(bar(kBarP + X));
+            if (kFmt == 1 && p.p_f16 && X == 0 && t + 1 < nt) v_to_f16(t + 1);  // off the P(t) -> PV(t) path
         }
         ptx::mbar_wait(bar(kBarPV + X), s0.npv[X][0] & 1);  // the last PV (commit covers all)
         ptx::tc_fence_after();
@@ -910,9 +935,9 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
             prev_slot = misc[3];
             if (id < 0) break;
             if (p.pf_tn64)
-                prefill_item_sm64<kFmt>(p, &tmk, &tmv, id, sbase, tmem, ps, warp, lane);
+                prefill_item_sm64<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);
             else
-                prefill_item_sm<kFmt>(p, &tmk, &tmv, id, sbase, tmem, ps, warp, lane);
+                prefill_item_sm<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);
         }
         ptx::tc_fence_before();
         ptx::named_bar_sync(1, kPrefillThreads);

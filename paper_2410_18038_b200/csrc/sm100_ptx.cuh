@@ -59,6 +59,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+// Wait by polling test_wait (never suspends the warp): for the latency-critical hand-offs
+// where try_wait's suspend/wake-up adds to the chain.  Bounded like mbar_wait.
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
+    if (mbar_test_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_test_wait(bar, parity)) {
+        if (clock64() - t0 > (1ll << 34)) __trap();
+    }
+}
+
 // Wait with a sleep back-off, for a warp that is not latency-critical (a TMA
 // producer running stages ahead): spinning on try_wait would take issue slots
 // from the softmax warps sharing its SM sub-partition.
@@ -297,41 +307,43 @@ __device__ __forceinline__ void umma_ts_k128_elect(uint32_t d_tmem, uint32_t a_t
         : "memory");
 }
 // O (+)= P V over 32 keys (2 K-steps of 16) with P as bf16 hi (A columns +0, +8)
-// and, if kSplit, lo (columns +16, +24); B MN-major SW128, K-steps 2 KB apart.
-template <bool kSplit>
+// and, if kSplit, lo (columns +16, +24); B MN-major SW128, K-steps kStep 16-byte
+// units apart (one 4 KB head-page [d-half][16 keys][64 d] per K-step: 256).
+template <bool kSplit, int kStep = 256>
 __device__ __forceinline__ void umma_pv32_elect(uint32_t d_tmem, uint32_t p_tmem, uint64_t b_desc, uint32_t idesc,
                                                 uint32_t accumulate) {
     if constexpr (kSplit)
         asm volatile(
             "{\n\t.reg .pred e, acc;\n\t.reg .b64 b1;\n\t.reg .b32 a1, a2, a3;\n\t"
             "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 acc, %4, 0;\n\t"
-            "add.s64 b1, %2, 128;\n\tadd.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+            "add.s64 b1, %2, %5;\n\tadd.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, acc;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], %2, %3, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b1, %3, 1;\n\t}" ::"r"(d_tmem),
-            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "n"(kStep)
             : "memory");
     else
         asm volatile(
             "{\n\t.reg .pred e, acc;\n\t.reg .b64 b1;\n\t.reg .b32 a1;\n\t"
             "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 acc, %4, 0;\n\t"
-            "add.s64 b1, %2, 128;\n\tadd.u32 a1, %1, 8;\n\t"
+            "add.s64 b1, %2, %5;\n\tadd.u32 a1, %1, 8;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, acc;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t}" ::"r"(d_tmem),
-            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "n"(kStep)
             : "memory");
 }
 // O (+)= P V over 64 keys (4 K-steps of 16) in one asm block: P hi in A columns
-// +0/+8/+16/+24, lo (if kSplit) in +32..+56; B MN-major SW128, K-steps 2 KB apart.
-template <bool kSplit>
+// +0/+8/+16/+24, lo (if kSplit) in +32..+56; B MN-major SW128, K-steps kStep
+// 16-byte units apart (one 4 KB head-page per K-step: 256).
+template <bool kSplit, int kStep = 256>
 __device__ __forceinline__ void umma_pv64_elect(uint32_t d_tmem, uint32_t p_tmem, uint64_t b_desc, uint32_t idesc,
                                                 uint32_t accumulate) {
     if constexpr (kSplit)
         asm volatile(
             "{\n\t.reg .pred e, acc;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 a1, a2, a3, l0, l1, l2, l3;\n\t"
             "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 acc, %4, 0;\n\t"
-            "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\t"
+            "add.s64 b1, %2, %5;\n\tadd.s64 b2, b1, %5;\n\tadd.s64 b3, b2, %5;\n\t"
             "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
             "add.u32 l0, %1, 32;\n\tadd.u32 l1, %1, 40;\n\tadd.u32 l2, %1, 48;\n\tadd.u32 l3, %1, 56;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, acc;\n\t"
@@ -342,19 +354,19 @@ __device__ __forceinline__ void umma_pv64_elect(uint32_t d_tmem, uint32_t p_tmem
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l2], b2, %3, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l3], b3, %3, 1;\n\t}" ::"r"(d_tmem),
-            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "n"(kStep)
             : "memory");
     else
         asm volatile(
             "{\n\t.reg .pred e, acc;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 a1, a2, a3;\n\t"
             "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 acc, %4, 0;\n\t"
-            "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\t"
+            "add.s64 b1, %2, %5;\n\tadd.s64 b2, b1, %5;\n\tadd.s64 b3, b2, %5;\n\t"
             "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, acc;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, 1;\n\t}" ::"r"(d_tmem),
-            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            "r"(p_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "n"(kStep)
             : "memory");
 }
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {

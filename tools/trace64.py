@@ -32,12 +32,20 @@ def main():
     ap.add_argument("--mode", default="prefill")
     ap.add_argument("--precision", type=int, default=2)
     ap.add_argument("--keys", type=int, default=64)
+    ap.add_argument("--chunk", type=int, default=0, help="override the config's chunk (32 rows x G=4 = one M-block)")
     a = ap.parse_args()
     assert os.environ.get("POD_TRACE"), "set POD_TRACE=1 with a POD_TRACE_STAMPS build (POD_LIB)"
     hq, hkv, chunk, off, b, ctx = CONFIGS[a.config]
+    if a.chunk:
+        off, chunk = off + chunk - a.chunk, a.chunk
     batch = make_batch(pkg.ModelShape(hq, hkv, 128, math.sqrt(128)), chunk=chunk, offset=off, decode_ctx=[ctx] * b)
     wl = build_workload(batch, device="cuda")
-    op = PodAttention(batch, options=pkg.PlanOptions(policy=7, prefill_tile_keys=a.keys, precision=a.precision))
+    gpu = pkg.GpuSpec.from_device(0)
+    if a.chunk:  # one item per KV head, unsplit: plan for as many SMs as items
+        import dataclasses
+        gpu = dataclasses.replace(gpu, num_sms=hkv)
+    op = PodAttention(batch, gpu=gpu,
+                      options=pkg.PlanOptions(policy=7, prefill_tile_keys=a.keys, precision=a.precision))
     log = op.enable_role_log(768 * 8)
     out = op.alloc_outputs()
     for _ in range(2):
@@ -48,7 +56,7 @@ def main():
     tr = log.view(-1, 8)[nrec:].cpu().long() & 0xffffffff
     A, B = tr[:384], tr[384:768]
     nt = int((A[:, 1] != 0).sum())
-    print(f"{a.config} {a.mode} precision {a.precision} keys {a.keys}: {nt} tiles traced")
+    print(f"{a.config} chunk {chunk} {a.mode} precision {a.precision} keys {a.keys}: {nt} tiles traced")
     if nt < 40:
         return
     rng = range(16, nt - 16)
@@ -68,6 +76,9 @@ def main():
         "MMA issue PV_A + QK_A": [d(A[t, 4], A[t, 5]) for t in rng],
         "QK_A(t+1) issued -> S_A(t+1) ready": [d(A[t, 5], A[t + 1, 1]) for t in rng],
         "A waits S (k0 -> k1)": [d(A[t, 0], A[t, 1]) for t in rng],
+        "  A: S ready -> S in registers (tcgen05.ld)": [d(A[t, 1], A[t, 6]) for t in rng],
+        "  A: max, rescale check, exp, P pack + tcgen05.st": [d(A[t, 6], A[t, 7]) for t in rng],
+        "  A: wait::st, fence, syncwarp -> arrive": [d(A[t, 7], A[t, 2]) for t in rng],
         "B softmax": [d(B[t, 1], B[t, 2]) for t in rng],
         "B arrive(w3) -> MMA sees P_B": [d(B[t, 3], B[t, 4]) for t in rng],
         "MMA issue PV_B + QK_B": [d(B[t, 4], B[t, 5]) for t in rng],
@@ -78,6 +89,9 @@ def main():
         "producer K(t) issued ahead of S_A(t) ready": [d(B[t, 6], A[t, 1]) for t in rng],
     }
     for k, v in rows.items():
+        if "B" in k.split(" ")[0] or "P_B" in k or "QK_B" in k or "PV_B" in k:
+            if not int((B[:, 1] != 0).sum()):
+                continue
         print(f"  {k:45s} {med(v):6d} cyc")
 
 
