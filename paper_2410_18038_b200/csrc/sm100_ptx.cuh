@@ -306,6 +306,31 @@ __device__ __forceinline__ void umma_ts_k128_elect(uint32_t d_tmem, uint32_t a_t
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "n"(h)
         : "memory");
 }
+// One full K = 128 contraction as 8 back-to-back kind::f16 SS-MMAs in a single asm
+// block: A and B both K-major SW128 in shared memory, K-steps of 16 elements 32 B
+// apart inside a 128 B swizzle row, the second 64-element K-half kAHalf / kBHalf
+// bytes after the first.
+template <uint32_t kAHalf, uint32_t kBHalf>
+__device__ __forceinline__ void umma_ss_k128_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
+    constexpr uint64_t ha = kAHalf >> 4, hb = kBHalf >> 4;
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+        "add.s64 a4, %1, %4;\n\tadd.s64 a5, a4, 2;\n\tadd.s64 a6, a4, 4;\n\tadd.s64 a7, a4, 6;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "add.s64 b4, %2, %5;\n\tadd.s64 b5, b4, 2;\n\tadd.s64 b6, b4, 4;\n\tadd.s64 b7, b4, 6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, 1;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "n"(ha), "n"(hb)
+        : "memory");
+}
 // O (+)= P V over 32 keys (2 K-steps of 16) with P as bf16 hi (A columns +0, +8)
 // and, if kSplit, lo (columns +16, +24); B MN-major SW128, K-steps kStep 16-byte
 // units apart (one 4 KB head-page [d-half][16 keys][64 d] per K-step: 256).

@@ -1,7 +1,7 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 export POD_LIB=tools/micro/libpod_trace.so POD_TRACE=1
-( timeout 300 python tools/trace64.py --config c2_b8 --mode prefill
-  timeout 300 python tools/trace64.py --config c2_b8 --mode prefill --chunk 32
-  for v in $TRACE_VARIANTS; do echo "-- $v"; POD_LIB=tools/micro/libpod_$v.so timeout 300 python tools/trace64.py --config c2_b8 --mode prefill; done
+( timeout 300 python tools/trace64.py --config c2_b8 --mode prefill --engine 1
+  timeout 300 python tools/trace64.py --config c2_b8 --mode prefill --engine 2
+  timeout 300 python tools/trace64.py --config c2_b8 --mode fused --engine 2
 ) > gpurun_out/trace64.log 2>&1
 cat gpurun_out/trace64.log
