@@ -263,6 +263,14 @@ pod_status pod_attn_gather_probe(const pod_plan* plan, const void* kv_pool, int6
                                  const int32_t* page_indptr, const int32_t* page_indices,
                                  int32_t req, int64_t ctx, uint16_t* out, void* stream);
 
+/* Benchmark utility: overwrites `bytes` of device memory (a buffer larger than the
+ * 126 MB L2) with zeros, evicting the L2 between timed layers.  The kernel prefers
+ * the max-shared-memory L1 carve-out, the one the POD kernels use, so the flush does
+ * not leave the SMs in a configuration the next POD launch must switch back from
+ * (a generic memset costs the following launch ~7-10 us of reconfiguration).
+ * Stream-ordered. */
+pod_status pod_attn_l2_flush(void* buf, int64_t bytes, void* stream);
+
 /* KV append (the step before attention in a layer): scatters the
  * batch's new K/V tokens into the paged pools through the block table.  The prefill
  * chunk's tokens take positions [position_offset, position_offset + chunk_size) of

@@ -1079,6 +1079,9 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
 // mode 1: decode requests; partials [req][splits][Hq][d].
 __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* tile_splits,
                                                     int tile_q, int mode, int nrows) {
+    // launched as a programmatic dependent of the POD kernel (its launch latency overlaps
+    // the kernel's tail); every partial it reads is visible once this returns
+    ptx::griddep_wait();
     const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp_global >= nrows) return;
@@ -1251,6 +1254,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, ncols);
     }
+    ptx::griddep_launch_dependents();  // the split merge may start launching (it waits for completion)
     if (tid == 0) {
         __threadfence();
         const uint32_t prev = atomicAdd(&p.ctr->done, 1u);
@@ -1271,6 +1275,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 #include "pod_sm.cuh"
+
+__global__ void __launch_bounds__(256) l2_flush_kernel(uint4* __restrict__ buf, size_t n16) {
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n16;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        buf[i] = z;
+}
 
 __global__ void gather_probe_kernel(const uint16_t* pool, int layout, int hkv, const int32_t* indptr,
                                     const int32_t* indices, int req, int ctx, uint16_t* out) {
@@ -1513,6 +1524,11 @@ pod_status set_kernel_attributes() {
     std::call_once(once[dev], [&] {
         cudaError_t r = cudaFuncSetAttribute(pod_fused_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kSmemBytes);
+        // the merges run right after a max-shared-memory POD kernel: keep the SM's
+        // L1 / shared split (no carve-out reconfiguration between the launches)
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
         if (r == cudaSuccess)
             r = cudaFuncSetAttribute(pod_sm_kernel<G, kFmt, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      SmLayout<0>::kSmem);
@@ -1569,13 +1585,26 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
     const bool do_d = (mode != 2) && plan->merge_rows_decode > 0;
     const uint8_t* ws = reinterpret_cast<const uint8_t*>(p.ctr);
     const int32_t* tile_splits = reinterpret_cast<const int32_t*>(ws - plan->ws.off_counters + plan->ws.off_tile_splits);
+    // the merges are programmatic dependents: their launch overlaps the POD kernel's tail
+    auto merge = [&](int tq, int mode_, int rows) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((rows + 7) / 8);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, merge_kernel, p, tile_splits, tq, mode_, rows);
+    };
     if (do_p) {
-        const int rows = p.chunk * p.hq;
-        merge_kernel<<<(rows + 7) / 8, 256, 0, s>>>(p, tile_splits, static_cast<int>(plan->cfg.prefill_tile_q), 0, rows);
+        e = merge(static_cast<int>(plan->cfg.prefill_tile_q), 0, p.chunk * p.hq);
+        if (e != cudaSuccess) return cuda_fail(e, "pod merge launch");
     }
     if (do_d) {
-        const int rows = static_cast<int>(plan->decode_ctx.size()) * p.hq;
-        merge_kernel<<<(rows + 7) / 8, 256, 0, s>>>(p, tile_splits, 1, 1, rows);
+        e = merge(1, 1, static_cast<int>(plan->decode_ctx.size()) * p.hq);
+        if (e != cudaSuccess) return cuda_fail(e, "pod merge launch");
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "pod merge launch");
@@ -1709,6 +1738,22 @@ pod_status pod_attn_run_part(const pod_plan* plan, int which, const void* q_pref
     if (which != 0 && which != 1) return POD_ERR_INVALID_ARGUMENT;
     return run_mode(plan, which == 0 ? 2 : 3, q_prefill, q_decode, k_pool, v_pool, num_pages, page_indptr,
                     page_indices, o_prefill, lse_prefill, o_decode, lse_decode, workspace, stream);
+}
+
+pod_status pod_attn_l2_flush(void* buf, int64_t bytes, void* stream) {
+    if (!buf || bytes < 16) return POD_ERR_INVALID_ARGUMENT;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(l2_flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        cudaSharedmemCarveoutMaxShared);
+    });
+    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "l2_flush attributes");
+    l2_flush_kernel<<<4 * 148, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<uint4*>(buf),
+                                                                           static_cast<size_t>(bytes) / 16);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "l2_flush");
+    return POD_OK;
 }
 
 pod_status pod_attn_gather_probe(const pod_plan* plan, const void* kv_pool, int64_t num_pages,

@@ -1188,6 +1188,10 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
                      : hw_warp >= 6       ? hw_warp + 2    // producer, MMA: hardware warps 6, 7
                                           : hw_warp + 10;  // decode group: hardware warps 0-5
     const int tid = warp * 32 + lane;
+    // debug builds: CTA entry / exit times after the per-tile trace (tools/profile_run.py --cta-times)
+    int32_t* cta_t = POD_TRACE_STAMPS && p.trace && p.role_log ? p.role_log + p.trace + 768 * 8 + 2 * blockIdx.x
+                                                               : nullptr;
+    if (cta_t && tid == 0) cta_t[0] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
     const uint32_t sbase = ptx::smem_u32(smem);
     volatile int32_t* misc = reinterpret_cast<volatile int32_t*>(smem + kOffMisc);  // [0] tmem, [2..3] pf, [4..5] dec
     if (tid == 0) {
@@ -1276,7 +1280,9 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
                 p.role_log[8 * slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
         }
     }
+    ptx::griddep_launch_dependents();  // the split merge may start launching (it waits for completion)
     __syncthreads();
+    if (cta_t && tid == 0) cta_t[1] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
     if (tid == 0) {
         __threadfence();
         const uint32_t prev = atomicAdd(&p.ctr->done, 1u);

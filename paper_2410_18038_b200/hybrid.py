@@ -28,6 +28,15 @@ class HybridOutputs:
     lse_decode: Optional[torch.Tensor]
 
 
+def l2_flush(buf: torch.Tensor, stream=None) -> None:
+    """pod_attn_l2_flush: zero `buf` (> L2) on the stream, evicting the L2 between timed
+    layers without switching the SMs' L1 / shared-memory carve-out (bench utility)."""
+    st = stream or torch.cuda.current_stream(buf.device)
+    with torch.cuda.device(buf.device):
+        _check(lib().pod_attn_l2_flush(_ptr(buf), C.c_int64(buf.numel() * buf.element_size()),
+                                       C.c_void_p(st.cuda_stream)), "pod_attn_l2_flush")
+
+
 class PodAttention:
     """Plan + workspace for one hybrid batch shape; `run` launches the fused kernel."""
 

@@ -39,7 +39,7 @@ def main():
     op = PodAttention(batch, options=pkg.PlanOptions(policy=a.policy, tile_mode=a.tile_mode,
                                                      decode_splits=a.decode_splits, precision=a.precision,
                                                      split_wave_cap=a.split_wave_cap))
-    log = op.enable_role_log(768 * 8) if a.roles else None
+    log = op.enable_role_log(768 * 8 + 1024) if a.roles else None
     out = op.alloc_outputs()
     evs = []
     for _ in range(a.iters):
@@ -71,6 +71,15 @@ def main():
                 row = tr[t] + tr[256 + t] + tr[512 + t][:3]
                 print(t, [((x - base) & 0xffffffff) if x else None for x in row])
         t0 = min(r[5] for r in rec)
+        cta = allrec[nrec + 768:].reshape(-1).tolist()[: 2 * 148] if len(tr) >= 768 + 37 else []
+        if cta and any(cta):
+            st = [cta[2 * i] for i in range(len(cta) // 2) if cta[2 * i]]
+            en = [cta[2 * i + 1] for i in range(len(cta) // 2) if cta[2 * i + 1]]
+            first_item = min(r[5] for r in rec if r[3] >= 0)
+            last_item = max(r[6] for r in rec if r[3] >= 0)
+            print(f"CTA entry spread {(max(st) - min(st)) / 1e3:.2f} us; first entry -> first item "
+                  f"{(first_item - min(st)) / 1e3:.2f} us; last item end -> last CTA exit {(max(en) - last_item) / 1e3:.2f} us; "
+                  f"first entry -> last exit {(max(en) - min(st)) / 1e3:.2f} us")
         rows = [{"sm": r[0], "ticket": r[1], "op": r[2], "id": r[3], "arrival": r[4],
                  "start_us": (r[5] - t0) / 1000.0, "end_us": ((r[6] - t0) % (1 << 31)) / 1000.0} for r in rec]
         Path(a.roles).write_text(json.dumps(rows))
