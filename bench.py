@@ -523,7 +523,7 @@ def run_pod(args, rank, world, local_rank):
         dist.barrier()
 
     info = op.info
-    launches_per_step = 1 + (1 if info.num_merge_rows_prefill > 0 else 0) + (1 if info.num_merge_rows_decode > 0 else 0)
+    launches_per_step = 1 + (1 if (info.num_merge_rows_prefill or info.num_merge_rows_decode) else 0)  # one merge launch
     res = dict(t_fused=t_fused, ms_fused=ms_fused, t_serial=t_serial, t_pf=t_pf, t_dec=t_dec, t_e2e=t_e2e,
                t_attn=t_attn, t_append=t_append, append_bytes=append_bytes, best=best, tp_check=tp_check,
                clocks=clocks, info=info, launches=launches_per_step, h2d=h2d, d2h=d2h, hq_r=hq_r, hkv_r=hkv_r)

@@ -1073,18 +1073,50 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
 }
 
 // ============================================================== merge ===
+// merge_partials (attention.hpp:294-326) for one output row, one warp: lse_tot = m +
+// log sum exp(lse_i - m), O = sum_i exp(lse_i - lse_tot) O_i in split (= kv-range)
+// order.  Partials are read through L2 (ld.global.cg): they were written by other
+// SMs during this launch (in-kernel merge) or the previous one.
+__device__ __forceinline__ void merge_row(const float* po, const float* pl, size_t stride_o, size_t stride_l, int n,
+                                          const ORow& out_o, float* out_l, int lane) {
+    float M = -INFINITY;
+    for (int i = 0; i < n; ++i) M = fmaxf(M, __ldcg(pl + i * stride_l));
+    float tot = 0.f;
+    for (int i = 0; i < n; ++i) tot += ptx::ex2((__ldcg(pl + i * stride_l) - M) * kLog2e);
+    const float lse_tot = M + ptx::lg2(tot) * kLn2;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < n; ++i) {
+        const float w = ptx::ex2((__ldcg(pl + i * stride_l) - lse_tot) * kLog2e);
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(po + i * stride_o + lane * 4));
+        acc.x += w * v.x;
+        acc.y += w * v.y;
+        acc.z += w * v.z;
+        acc.w += w * v.w;
+    }
+    store4(out_o, lane * 4, acc);
+    if (lane == 0) *out_l = lse_tot;
+}
+
+
 // One warp per output (row, q head): O = sum_i exp(lse_i - lse_tot) O_i in
 // split order (= kv-range order), lse_tot = m + log(sum exp(lse_i - m)).
 // mode 0: prefill rows r in [0, chunk); partials [split][chunk][Hq][d].
 // mode 1: decode requests; partials [req][splits][Hq][d].
+// One launch merges both kinds: warps [0, prefill_rows) the prefill rows (mode 0),
+// the next decode_rows warps the decode rows (mode 1).
 __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* tile_splits,
-                                                    int tile_q, int mode, int nrows) {
+                                                    int tile_q, int prefill_rows, int decode_rows) {
     // launched as a programmatic dependent of the POD kernel (its launch latency overlaps
     // the kernel's tail); every partial it reads is visible once this returns
     ptx::griddep_wait();
-    const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (warp_global >= nrows) return;
+    int mode = 0;
+    if (warp_global >= prefill_rows) {
+        warp_global -= prefill_rows;
+        mode = 1;
+        if (warp_global >= decode_rows) return;
+    }
     const int r = warp_global / p.hq, qh = warp_global % p.hq;
     int n;
     const float* po;
@@ -1113,22 +1145,7 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
         out_o = out_row(p.o_decode, (static_cast<size_t>(r) * p.hq + qh) * kHeadDim, p.out_fmt);
         out_l = p.lse_decode + static_cast<size_t>(r) * p.hq + qh;
     }
-    float M = -INFINITY;
-    for (int i = 0; i < n; ++i) M = fmaxf(M, pl[i * stride_l]);
-    float tot = 0.f;
-    for (int i = 0; i < n; ++i) tot += ptx::ex2((pl[i * stride_l] - M) * kLog2e);
-    const float lse_tot = M + ptx::lg2(tot) * kLn2;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = 0; i < n; ++i) {
-        const float w = ptx::ex2((pl[i * stride_l] - lse_tot) * kLog2e);
-        const float4 v = *reinterpret_cast<const float4*>(po + i * stride_o + lane * 4);
-        acc.x += w * v.x;
-        acc.y += w * v.y;
-        acc.z += w * v.z;
-        acc.w += w * v.w;
-    }
-    store4(out_o, lane * 4, acc);
-    if (lane == 0) *out_l = lse_tot;
+    merge_row(po, pl, stride_o, stride_l, n, out_o, out_l, lane);
 }
 
 // ============================================================ kernels ===
@@ -1579,14 +1596,19 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "pod kernel launch");
     // split merges
+    // (an in-kernel merge -- each finished split releases its parent with red.release, a
+    // drained engine merges complete parents -- measured slower than this one launch:
+    // C1 fused 86 vs 63 us, TP8 rank 233 vs 131 us: the merges then run in the launch's
+    // tail on the few warps of drained engines instead of the whole machine)
     const bool do_p = (mode != 3) && plan->merge_rows_prefill > 0;
     // (an in-kernel merge by the group finishing a parent's last split measured ~8 us
     // slower at C2 B=64 than this 5 us launch: per-item fences + barriers)
     const bool do_d = (mode != 2) && plan->merge_rows_decode > 0;
     const uint8_t* ws = reinterpret_cast<const uint8_t*>(p.ctr);
     const int32_t* tile_splits = reinterpret_cast<const int32_t*>(ws - plan->ws.off_counters + plan->ws.off_tile_splits);
-    // the merges are programmatic dependents: their launch overlaps the POD kernel's tail
-    auto merge = [&](int tq, int mode_, int rows) {
+    // the merges are ONE programmatic dependent launch: it overlaps the POD kernel's tail
+    auto merge = [&](int tq, int prows, int drows) {
+        const int rows = prows + drows;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((rows + 7) / 8);
         cfg.blockDim = dim3(256);
@@ -1596,14 +1618,11 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, merge_kernel, p, tile_splits, tq, mode_, rows);
+        return cudaLaunchKernelEx(&cfg, merge_kernel, p, tile_splits, tq, prows, drows);
     };
-    if (do_p) {
-        e = merge(static_cast<int>(plan->cfg.prefill_tile_q), 0, p.chunk * p.hq);
-        if (e != cudaSuccess) return cuda_fail(e, "pod merge launch");
-    }
-    if (do_d) {
-        e = merge(1, 1, static_cast<int>(plan->decode_ctx.size()) * p.hq);
+    if (do_p || do_d) {
+        e = merge(static_cast<int>(plan->cfg.prefill_tile_q), do_p ? p.chunk * p.hq : 0,
+                  do_d ? static_cast<int>(plan->decode_ctx.size()) * p.hq : 0);
         if (e != cudaSuccess) return cuda_fail(e, "pod merge launch");
     }
     e = cudaGetLastError();
