@@ -377,7 +377,8 @@ def run_pod(args, rank, world, local_rank):
     odt = {"f32": torch.float32, "bf16": torch.bfloat16}[args.out_dtype]
     opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode, precision=args.precision,
                            decode_splits=args.decode_splits, split_wave_cap=args.split_wave_cap,
-                           out_dtype={"f32": 0, "bf16": 1}[args.out_dtype], prefill_engine=args.prefill_engine)
+                           out_dtype={"f32": 0, "bf16": 1}[args.out_dtype], prefill_engine=args.prefill_engine,
+                           prefill_tile_keys=args.prefill_tile_keys)
     op = PodAttention(batch, options=opts, device=local_rank)
     # the kernel writes straight into the all-gather send buffer (two, for the pipelined e2e)
     gbs = [gather_buffers(batch, world, odt, dev) for _ in range(2)]
@@ -543,6 +544,7 @@ def main():
     ap.add_argument("--out-dtype", default="f32", choices=["f32", "bf16"],
                     help="element type of the attention outputs (LSE stays fp32); f32 = the reference's")
     ap.add_argument("--decode-splits", type=int, default=0)
+    ap.add_argument("--prefill-tile-keys", type=int, default=0, help="warp-specialised pair engine: 0 auto, 32 or 64")
     ap.add_argument("--prefill-engine", type=int, default=0,
                     help="warp-specialised prefill engine: 0 auto, 1 Q in TMEM, 2 Q in smem (double-buffered 64-key S)")
     ap.add_argument("--split-wave-cap", type=int, default=0)
