@@ -491,8 +491,9 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
     const int nblocks = (job.rows + rpb - 1) / rpb;
     const int pbeg = p.page_indptr[0];
     const int npages = p.page_indptr[1] - pbeg;
-    // every thread advances the shared counters identically
-    int g0 = ps.g, qb0 = ps.qb;
+    // every thread advances the shared counters identically (broadcast from lane 0: the
+    // compiler then keeps the stage / phase arithmetic on the uniform datapath)
+    int g0 = __shfl_sync(0xffffffffu, ps.g, 0), qb0 = __shfl_sync(0xffffffffu, ps.qb, 0);
     for (int b = 0; b < nblocks; ++b) {
         const int nt = prefill_block(p, job, b).nt;
         if (nt > 0) {
@@ -1249,7 +1250,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             role[2] = slot;
         }
         __syncthreads();
-        const int op = role[0], id = role[1], slot = role[2];
+        const int op = __shfl_sync(0xffffffffu, role[0], 0), id = __shfl_sync(0xffffffffu, role[1], 0),
+                  slot = role[2];
         __syncthreads();  // role[] is rewritten by the next claim
         if (op < 0) break;
         if (op == 0) {

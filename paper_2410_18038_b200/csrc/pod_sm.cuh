@@ -46,6 +46,13 @@ __device__ __forceinline__ void sm_wait(uint32_t bar, uint32_t parity) {
     else
         ptx::mbar_wait(bar, parity);
 }
+// Warp-uniform copy of the engines' loop state: every lane holds the same values, but the
+// compiler only keeps them (and the descriptors / stage offsets derived from them) on the
+// uniform datapath -- no R2UR per MMA issue -- once they come out of a shuffle broadcast.
+#ifndef POD_SM_UNIFORM_STATE
+#define POD_SM_UNIFORM_STATE 1
+#endif
+__device__ __forceinline__ int wuni(int x) { return POD_SM_UNIFORM_STATE ? __shfl_sync(0xffffffffu, x, 0) : x; }
 namespace sm3 {
 #ifndef POD_SM_DUAL_MMA
 #define POD_SM_DUAL_MMA 0
@@ -130,6 +137,19 @@ struct PfState {
     int nq[2] = {0, 0};   // Q loads per block (q_full phases)
     int npv[2][2] = {{0, 0}, {0, 0}};  // pv commits per (block, S buffer) (POD_SM_LAZY_PV)
 };
+__device__ __forceinline__ PfState uniform(const PfState& a) {
+    PfState u;
+    u.g = wuni(a.g);
+    u.n[0] = wuni(a.n[0]);
+    u.n[1] = wuni(a.n[1]);
+    u.nq[0] = wuni(a.nq[0]);
+    u.nq[1] = wuni(a.nq[1]);
+    u.npv[0][0] = wuni(a.npv[0][0]);
+    u.npv[0][1] = wuni(a.npv[0][1]);
+    u.npv[1][0] = wuni(a.npv[1][0]);
+    u.npv[1][1] = wuni(a.npv[1][1]);
+    return u;
+}
 
 // S = Q K^T for one 32-key tile: A = Q (TMEM, 128 rows x 128 d), B = K (smem,
 // K-major SW128 [d-half][32 keys][64 d]), N = 32.
@@ -189,7 +209,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
     const int kv_hi = min(job.kv_end, p.offset + (hasB ? rB.r0 + rB.nrows : rA.r0 + rA.nrows));
     const int kt0 = rA.kt0;
     const int nt = kv_hi > job.kv_begin ? (kv_hi - kt0 + kTN - 1) / kTN : 0;
-    const PfState s0 = ps;
+    const PfState s0 = uniform(ps);
     if (nt > 0) {
         ps.g += nt;
         ps.n[0] += nt;
@@ -609,7 +629,7 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
     const int kv_hi = min(job.kv_end, p.offset + (hasB ? rB.r0 + rB.nrows : rA.r0 + rA.nrows));
     const int kt0 = rA.kt0;
     const int nt = kv_hi > job.kv_begin ? (kv_hi - kt0 + kTN - 1) / kTN : 0;
-    const PfState s0 = ps;
+    const PfState s0 = uniform(ps);
     if (nt > 0) {  // g: tiles through the rings; n: S / P completions; npv[X][0]: PV commits
         ps.g += nt;
         ps.n[0] += nt;
@@ -886,7 +906,7 @@ __device__ void prefill_item_sq(const RunParams& p, const CUtensorMap* tmq, cons
     const int kv_hi = min(job.kv_end, p.offset + (hasB ? rB.r0 + rB.nrows : rA.r0 + rA.nrows));
     const int kt0 = rA.kt0;
     const int nt = kv_hi > job.kv_begin ? (kv_hi - kt0 + kTN - 1) / kTN : 0;
-    const sm3::PfState s0 = ps;  // g: tiles through the rings; n[X]: S per block; nq[0]: Q loads
+    const sm3::PfState s0 = sm3::uniform(ps);  // g: tiles through the rings; n[X]: S per block; nq[0]: Q loads
     if (nt > 0) {
         ps.g += nt;
         ps.n[0] += nt;
@@ -1243,7 +1263,7 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
                 misc[3] = slot;
             }
             ptx::named_bar_sync(1, kPrefillThreads);
-            const int id = misc[2];
+            const int id = wuni(misc[2]);
             prev_slot = misc[3];
             if (id < 0) break;
             if constexpr (kEng == 1)
@@ -1271,7 +1291,7 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
                 misc[5] = slot;
             }
             ptx::named_bar_sync(3, kDW * 32);
-            const int id = misc[4], slot = misc[5];
+            const int id = wuni(misc[4]), slot = misc[5];
             ptx::named_bar_sync(3, kDW * 32);
             if (id < 0) break;
             decode_item<G, kFmt, kDW, kDS>(p, &tdk, &tdv, id, dw, sbase + kOffDec, sbase + kOffDecBars,

@@ -71,6 +71,21 @@ def main():
     def d(x, y):  # y - x with 32-bit wrap
         return (y - x) & 0xffffffff
 
+    if a.keys == 32 and a.engine != 2:  # the 32-key double-S engine's stamps (pod_sm.cuh)
+        rng = range(16, min(nt, 128) - 16)
+        rows32 = {
+            "period per 32-key tile (S_A(t) ready -> S_A(t+1) ready)": [d(A[t, 1], A[t + 1, 1]) for t in rng],
+            "A softmax (S ready -> warp0 arrive)": [d(A[t, 1], A[t, 2]) for t in rng],
+            "A waits S (k0 -> k1)": [d(A[t, 0], A[t, 1]) for t in rng],
+            "A arrive(w3) -> MMA sees P_A": [d(A[t, 3], A[t, 4]) for t in rng],
+            "MMA: P_A seen -> PV_A committed": [d(A[t, 4], A[t, 5]) for t in rng],
+            "MMA: PV_A committed -> QK_A(t+2) committed": [d(A[t, 5], A[t, 6]) for t in rng],
+            "B softmax": [d(B[t, 1], B[t, 2]) for t in rng],
+            "B waits S": [d(B[t, 0], B[t, 1]) for t in rng],
+        }
+        for k, v in rows32.items():
+            print(f"  {k:55s} {med(v):6d} cyc")
+        return
     rows = {
         "period (S_A(t) ready -> S_A(t+1) ready)": [d(A[t, 1], A[t + 1, 1]) for t in rng],
         "A softmax (S ready -> warp0 arrive)": [d(A[t, 1], A[t, 2]) for t in rng],
