@@ -150,9 +150,6 @@ typedef struct pod_options {
     int32_t precision;       /* POD_PRECISION_* for the prefill P operand            */
     int32_t out_dtype;       /* POD_OUT_*: element type of o_prefill / o_decode (LSE stays fp32) */
     int32_t prefill_tile_keys; /* warp-specialised pair engine: 0 = by decode share, 32 or 64 forces */
-    int32_t prefill_engine;    /* warp-specialised prefill engine family: 0 = by decode share,
-                                  1 = Q in TMEM (32-key double-S / 64-key single-S tiles),
-                                  2 = Q in shared memory, double-buffered 64-key S          */
 } pod_options;
 
 enum {
@@ -188,7 +185,6 @@ typedef struct pod_plan_info {
     int32_t num_merge_rows_decode;
     int32_t policy;             /* the POD_POLICY_* the plan runs (POD_POLICY_AUTO resolved) */
     int32_t prefill_tile_keys;  /* keys per prefill K/V tile of the warp-specialised pair engine (32 or 64; 0 otherwise) */
-    int32_t prefill_engine;     /* warp-specialised prefill engine family (1 or 2 as in pod_options; 0 otherwise) */
 } pod_plan_info;
 
 typedef struct pod_plan pod_plan;

@@ -26,11 +26,6 @@
 #define POD_WHOLE_WAVES 1  // warp-specialised decode items rounded up to whole waves
 #endif
 
-#ifndef POD_SQ_SHARE
-#define POD_SQ_SHARE 0.0  // decode share below which AUTO picks the Q-in-smem engine (measured: never
-                          // better fused at C1-C4, its 2-stage decode rings cost 15-25 % decode rate;
-                          // faster prefill-alone for MHA, C4 184 vs 213 us)
-#endif
 namespace {
 
 struct Status : std::exception {
@@ -291,15 +286,6 @@ void lower(pod_plan& p) {
     {
         const int32_t keys = p.opts.prefill_tile_keys;
         p.pf_tn64 = warpspec && p.batch.has_prefill && (keys == 64 || (keys == 0 && decode_share(p) < 0.57));
-        // Engine family: Q in shared memory with double-buffered 64-key S (prefill_item_sq),
-        // forced with prefill_engine = 2 (AUTO keeps the Q-in-TMEM engines: see POD_SQ_SHARE);
-        // it takes 64 KB of smem from the decode rings (2 stages per decode warp instead of 3).
-        const int32_t eng = p.opts.prefill_engine;
-        p.pf_eng = warpspec && p.batch.has_prefill &&
-                           (eng == 2 || (eng == 0 && keys == 0 && decode_share(p) < POD_SQ_SHARE))
-                       ? 1
-                       : 0;
-        if (p.pf_eng == 1) p.pf_tn64 = true;
     }
     // Whole waves (warp-specialised kernel): the decode items are claimed in id order
     // (request-major) by one decode group per SM, so a count that is not a multiple of
@@ -446,7 +432,7 @@ pod_tile_config b200_tile_config(const pod_plan& p) {
     const int rows = (two_blocks ? 2 : 1) * pod::kMBlock;
     c.prefill_tile_q = std::max(1, rows / group);
     c.tile_kv = pod::kKvTile;
-    c.shared_mem_per_cta = static_cast<double>(p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes(0)
+    c.shared_mem_per_cta = static_cast<double>(p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes()
                                                                                    : pod::fused_smem_bytes());
     c.virtual_decode = 1;
     return c;
@@ -528,7 +514,7 @@ void build(pod_plan& p) {
     if (!p.decode_ctx.empty()) decompose_decode(p);
     lower(p);
     scheduler_ratio(p);
-    p.smem_bytes = p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes(p.pf_eng) : pod::fused_smem_bytes();
+    p.smem_bytes = p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes() : pod::fused_smem_bytes();
     layout_workspace(p);
 }
 
@@ -559,7 +545,6 @@ void pod_options_default(pod_options* out) {
     out->precision = POD_PRECISION_F16PV;
     out->out_dtype = POD_OUT_F32;
     out->prefill_tile_keys = 0;
-    out->prefill_engine = 0;
 }
 
 pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const pod_device* dev,
@@ -594,8 +579,6 @@ pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const p
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: out_dtype must be a POD_OUT_* value");
         if (p->opts.prefill_tile_keys != 0 && p->opts.prefill_tile_keys != 32 && p->opts.prefill_tile_keys != 64)
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: prefill_tile_keys must be 0, 32 or 64");
-        if (p->opts.prefill_engine < 0 || p->opts.prefill_engine > 2)
-            fail(POD_ERR_INVALID_ARGUMENT, "pod_options: prefill_engine must be 0, 1 or 2");
         build(*p);
         p->opts.tile_override = nullptr;  // do not keep caller pointers
         *out = p;
@@ -631,7 +614,6 @@ pod_status pod_attn_plan_get_info(const pod_plan* p, pod_plan_info* out) {
     out->num_merge_rows_decode = p->merge_rows_decode;
     out->policy = p->opts.policy;
     out->prefill_tile_keys = p->opts.policy == POD_POLICY_WARPSPEC && p->batch.has_prefill ? (p->pf_tn64 ? 64 : 32) : 0;
-    out->prefill_engine = p->opts.policy == POD_POLICY_WARPSPEC && p->batch.has_prefill ? (p->pf_eng == 1 ? 2 : 1) : 0;
     return POD_OK;
 }
 

@@ -867,285 +867,6 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
     }
 }
 
-// ---------------------------------------------------------------------------
-// The pair engine with Q in SHARED memory and double-buffered 64-key S
-// (RunParams::pf_eng == 1, prefill-dominant plans).  Moving Q out of TMEM frees
-// the 128 columns that double-buffer S at 64 keys:
-//     TMEM  S_A[2] (2 x 64) | S_B[2] (2 x 64) | O_A (128) | O_B (128)
-// so QK_X(t+1) runs while the softmax of tile t does, and a softmax warp goes from
-// tile t to t+1 without the S -> P -> MMA -> S round trip of the single-S engine
-// (which the per-tile trace shows is ~60 % of its period, tools/trace64.py).  QK is
-// an SS-MMA (A = Q, B = K, both K-major SW128 in smem, N = 64); PV a TS-MMA (A = P
-// over S in TMEM, B = V page-major in smem).  Shared memory: Q 2 x 32 KB, K 2 x 16
-// KB, V 2 x 16 KB (128 KB), the decode group 6 warps x 2 stages of 8 KB.
-namespace sq {
-constexpr int kTN = 64;
-constexpr uint32_t kStage = kTN * kHeadDim * 2;      // 16 KB
-constexpr uint32_t kQBlock = kMBlock * kHeadDim * 2;  // 32 KB: [d-half][128 rows][64 d]
-constexpr uint32_t kOffQ = 0, kOffK = 2 * kQBlock, kOffV = kOffK + 2 * kStage;
-constexpr uint32_t kRingBytes = kOffV + 2 * kStage;  // 128 KB
-// mbarriers: 0 q_full, 1 q_empty, 2-3 k_full, 4-5 k_empty, 6-7 v_full, 8-9 v_empty,
-// 10-13 s[X][b], 14-17 p[X][b] (4 arrivals), 18-21 pv[X][b]
-constexpr int kBarQF = 0, kBarQE = 1, kBarKF = 2, kBarKE = 4, kBarVF = 6, kBarVE = 8;
-constexpr int kBarS = 10, kBarP = 14, kBarPV = 18, kNumBars = 22;
-constexpr uint32_t kSA = 0, kSB = 128, kOA = 256, kOB = 384;  // TMEM columns
-}  // namespace sq
-
-template <int kFmt>
-__device__ void prefill_item_sq(const RunParams& p, const CUtensorMap* tmq, const CUtensorMap* tmk,
-                                const CUtensorMap* tmv /* 5-D page map */, int item, uint32_t sbase,
-                                uint32_t bars, uint32_t tmem, sm3::PfState& ps, int warp, int lane) {
-    using namespace sq;
-    const PrefillCta job = p.pctas[item];
-    const int G = p.group;
-    const int rpb = kMBlock / G;
-    const int nblocks = (job.rows + rpb - 1) / rpb;  // 1 or 2
-    const bool hasB = nblocks > 1;
-    const BlockRange rA = prefill_block(p, job, 0);
-    const BlockRange rB = hasB ? prefill_block(p, job, 1) : rA;
-    const int kv_hi = min(job.kv_end, p.offset + (hasB ? rB.r0 + rB.nrows : rA.r0 + rA.nrows));
-    const int kt0 = rA.kt0;
-    const int nt = kv_hi > job.kv_begin ? (kv_hi - kt0 + kTN - 1) / kTN : 0;
-    const sm3::PfState s0 = sm3::uniform(ps);  // g: tiles through the rings; n[X]: S per block; nq[0]: Q loads
-    if (nt > 0) {
-        ps.g += nt;
-        ps.n[0] += nt;
-        ps.nq[0] += 1;
-        if (hasB) ps.n[1] += nt;
-        for (int t = max(0, nt - 2); t < nt; ++t) {  // pv commits: the last two tiles per block
-            ps.npv[0][(s0.n[0] + t) & 1] += 1;
-            if (hasB) ps.npv[1][(s0.n[1] + t) & 1] += 1;
-        }
-    }
-    auto pv_commit = [&](int t) { return t + 2 >= nt; };
-    auto bar = [&](int i) { return bars + 8u * static_cast<uint32_t>(i); };
-    const uint32_t sQ = sbase + sq::kOffQ, sK = sbase + sq::kOffK, sV = sbase + sq::kOffV;
-    const int pbeg = p.page_indptr[0];
-    const int npages = p.page_indptr[1] - pbeg;
-    const int first = s0.n[0] == 0 ? 0 : 1;  // debug trace: CTA 0's first item (tools/trace64.py)
-    auto rowB = [&](int t) { return t < 384 ? 384 + t : 9999; };
-
-    if (warp == sm3::kProdWarp) {
-        // ------------------------------------------------ TMA producer --
-        // Q of both blocks, then K runs two tiles ahead of V (QK_X(t+2) is issued
-        // right after PV_X(t)): step u loads K(u) and V(u - 2).
-        if (nt == 0) return;
-        if (s0.nq[0] > 0) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarQE), (s0.nq[0] - 1) & 1);
-        ptx::mbar_arrive_expect_tx_elect(bar(kBarQF), (hasB ? 2 : 1) * kQBlock);
-        ptx::tma_load_3d_elect(sQ, tmq, bar(kBarQF), 0, job.kv_head * G, rA.r0);
-        ptx::tma_load_3d_elect(sQ + kQBlock / 2, tmq, bar(kBarQF), 64, job.kv_head * G, rA.r0);
-        if (hasB) {
-            ptx::tma_load_3d_elect(sQ + kQBlock, tmq, bar(kBarQF), 0, job.kv_head * G, rB.r0);
-            ptx::tma_load_3d_elect(sQ + kQBlock + kQBlock / 2, tmq, bar(kBarQF), 64, job.kv_head * G, rB.r0);
-        }
-        PageIds ids;
-        ids.init(p.page_indices + pbeg, npages, kt0 / 16);
-        for (int u = 0; u < nt + 2; ++u) {
-            if (u < nt) {
-                const int gg = s0.g + u, st = gg & 1;
-                if (gg >= 2) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarKE + st), ((gg >> 1) - 1) & 1);
-                ptx::mbar_arrive_expect_tx_elect(bar(kBarKF + st), kStage);
-                sm64::load_tile64(p, tmk, sK + st * kStage, bar(kBarKF + st), kt0 + u * kTN, job.kv_head, ids);
-                if (lane == 0) trace_stamp(p, first, rowB(u), 6);
-            }
-            if (u >= 2) {
-                const int gg = s0.g + u - 2, st = gg & 1;
-                if (gg >= 2) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarVE + st), ((gg >> 1) - 1) & 1);
-                ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
-                prefill_load_v_pages<4>(tmv, sV + st * kStage, bar(kBarVF + st), kt0 + (u - 2) * kTN, job.kv_head,
-                                        ids);
-            }
-        }
-    } else if (warp == sm3::kMmaWarp) {
-        // -------------------------------------------------- MMA issuer --
-        // Per block, QK_X(t+2) reuses the S buffer of tile t after PV_X(t) (in-order
-        // pipe), so the softmax of tile t+1 overlaps PV_X(t) and QK_X(t+2).
-        auto mma_issuer = [&](auto pv_c) {
-            constexpr int kPv = decltype(pv_c)::value;  // 0 split hi + lo, 1 one P, 2 fp16 P x fp16 V
-            constexpr bool kSplit = kPv == 0;
-            constexpr int kPvFmt = kPv == 2 ? 0 : kFmt;
-            constexpr uint32_t idesc_qk = ptx::idesc_f16(kFmt, kMBlock, kTN, 0);
-            constexpr uint32_t idesc_pv = ptx::idesc_f16(kPvFmt, kMBlock, kHeadDim, 1);
-            if (nt == 0) return;
-            ptx::mbar_wait(bar(kBarQF), s0.nq[0] & 1);
-            auto qk = [&](int X, int t) {  // QK_X(t) into S_X[(n_X + t) & 1]
-                const int gg = s0.g + t, st = gg & 1;
-                const uint32_t sq_x = sQ + X * kQBlock;
-                ptx::umma_ss_k128_elect<kQBlock / 2, kStage / 2>(
-                    tmem + (X ? kSB : kSA) + 64 * ((s0.n[X] + t) & 1), ptx::sw128_desc(sq_x, 16, 1024),
-                    ptx::sw128_desc(sK + st * kStage, 16, 1024), idesc_qk);
-                ptx::umma_commit_elect(bar(kBarS + 2 * X + ((s0.n[X] + t) & 1)));
-            };
-            for (int j = 0; j < 2 && j < nt; ++j) {
-                const int gg = s0.g + j, st = gg & 1;
-                ptx::mbar_wait(bar(kBarKF + st), (gg >> 1) & 1);
-                ptx::tc_fence_after();
-                qk(0, j);
-                if (hasB) qk(1, j);
-                ptx::umma_commit_elect(bar(kBarKE + st));  // K(j) consumed by both QKs
-                if (j == nt - 1) ptx::umma_commit_elect(bar(kBarQE));
-            }
-            for (int t = 0; t < nt; ++t) {
-                const int gg = s0.g + t, st = gg & 1;
-                const bool more = t + 2 < nt;
-                const int g2 = gg + 2, st2 = g2 & 1;
-#pragma unroll
-                for (int X = 0; X < 2; ++X) {
-                    if (X == 1 && !hasB) break;
-                    const int n = s0.n[X] + t, b = n & 1;
-                    ptx::mbar_wait(bar(kBarP + 2 * X + b), (n >> 1) & 1);
-                    if (lane == 0) trace_stamp(p, first, X ? rowB(t) : t, 4);
-                    if (X == 0 && kPv != 2) ptx::mbar_wait(bar(kBarVF + st), (gg >> 1) & 1);  // (F16PV: in P_A)
-                    ptx::tc_fence_after();
-                    ptx::umma_pv64_elect<kSplit>(tmem + (X ? kOB : kOA), tmem + (X ? kSB : kSA) + 64 * b,
-                                                 ptx::sw128_desc(sV + st * kStage, 2048, 1024), idesc_pv,
-                                                 t > 0 ? 1u : 0u);
-                    if (pv_commit(t)) ptx::umma_commit_elect(bar(kBarPV + 2 * X + b));
-                    if (more) {
-                        if (X == 0) {
-                            ptx::mbar_wait(bar(kBarKF + st2), (g2 >> 1) & 1);
-                            ptx::tc_fence_after();
-                        }
-                        qk(X, t + 2);
-                    }
-                    if (lane == 0) trace_stamp(p, first, X ? rowB(t) : t, 5);
-                }
-                ptx::umma_commit_elect(bar(kBarVE + st));           // V(t): both PVs issued
-                if (more) {
-                    ptx::umma_commit_elect(bar(kBarKE + st2));      // K(t+2): both QKs issued
-                    if (t + 2 == nt - 1) ptx::umma_commit_elect(bar(kBarQE));
-                }
-            }
-        };
-        if (kFmt == 1 && p.p_f16)
-            mma_issuer(std::integral_constant<int, 2>{});
-        else if (p.p_split != 0)
-            mma_issuer(std::integral_constant<int, 0>{});
-        else
-            mma_issuer(std::integral_constant<int, 1>{});
-    } else if (warp < sm3::kProdWarp) {
-        // ------------------------------------ softmax (4 warps per block) --
-        const int X = warp >> 2;
-        if (X == 1 && !hasB) return;
-        const int q = warp & 3;
-        const BlockRange br = X ? rB : rA;
-        const int m = q * 32 + lane;
-        const int my_r = br.r0 + m / G;
-        const bool row_ok = (m / G) < br.nrows;
-        const int vis = p.offset + my_r;
-        const int qhead = job.kv_head * G + m % G;
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        const uint32_t o_addr = lane_base + (X ? kOB : kOA);
-        ORow orow;
-        float* lrow;
-        if (job.n_splits == 1) {
-            orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim, p.out_fmt);
-            lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
-        } else {
-            const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
-            orow = out_row(p.ppart_o, row * kHeadDim, 0);
-            lrow = p.ppart_lse + row;
-        }
-        if (nt == 0) {
-            if (row_ok) {
-                for (int c = 0; c < kHeadDim; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
-                *lrow = -INFINITY;
-            }
-            return;
-        }
-        float m_run = -INFINITY, l_run = 0.f;
-        for (int t = 0; t < nt; ++t) {
-            const int n = s0.n[X] + t, b = n & 1;
-            const uint32_t s_addr = lane_base + (X ? kSB : kSA) + 64 * b;
-            if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 0);
-            ptx::mbar_wait(bar(kBarS + 2 * X + b), (n >> 1) & 1);
-            if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 1);
-            ptx::tc_fence_after();
-            float s[kTN];
-            ptx::tmem_ld32(s_addr, *reinterpret_cast<float(*)[32]>(&s[0]));
-            ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
-            ptx::tmem_wait_ld();
-            if (lane == 0 && q == 0 && X == 0) trace_stamp(p, first, t, 6);
-            const int kb = kt0 + t * kTN;
-            const int lo = max(job.kv_begin - kb, 0);
-            const int hi = row_ok ? min(min(job.kv_end, vis + 1) - kb, kTN) : 0;
-            if (!__all_sync(0xffffffffu, lo == 0 && hi == kTN)) {
-#pragma unroll
-                for (int c = 0; c < kTN; ++c)
-                    if (c < lo || c >= hi) s[c] = -INFINITY;
-            }
-            const float tmax = row_max<kTN>(s);
-            const float m_new = fmaxf(m_run, tmax * p.sl2);
-            const bool need = m_new > m_run + 8.f;  // lazy rescale (see prefill_item)
-            const float m_use = need ? m_new : m_run;
-            const float factor = need ? ptx::ex2(m_run - m_new) : 1.f;
-            l_run *= factor;
-            m_run = m_use;
-            // O_X is rescaled only when the reference max moved: PV_X(t-1), the newest
-            // MMA writing O_X, is complete once S_X(t+1) is (QK_X(t+1) was issued after
-            // it by the same thread; in-order pipe), else (last tile) its own commit.
-            if (t > 0 && __any_sync(0xffffffffu, need)) {
-                if (t + 1 < nt)
-                    ptx::mbar_wait(bar(kBarS + 2 * X + ((n + 1) & 1)), ((n + 1) >> 1) & 1);
-                else
-                    ptx::mbar_wait(bar(kBarPV + 2 * X + ((n - 1) & 1)), s0.npv[X][(n - 1) & 1] & 1);
-                ptx::tc_fence_after();
-#pragma unroll 1
-                for (int ch = 0; ch < kHeadDim / 32; ++ch) {
-                    float o[32];
-                    ptx::tmem_ld32(o_addr + ch * 32, o);
-                    ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int c = 0; c < 32; ++c) o[c] *= factor;
-                    ptx::tmem_st32(o_addr + ch * 32, o);
-                }
-            }
-            const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
-            float lsum;
-            if (kFmt == 1 && p.p_f16)
-                lsum = softmax_p_row<kFmt, 3, kTN>(s, p.sl2, neg_m, s_addr);
-            else if (kFmt == 1 && p.p_split)
-                lsum = softmax_p_row<kFmt, 1, kTN>(s, p.sl2, neg_m, s_addr);
-            else if (p.p_split)
-                lsum = softmax_p_row<kFmt, 2, kTN>(s, p.sl2, neg_m, s_addr);
-            else
-                lsum = softmax_p_row<kFmt, 0, kTN>(s, p.sl2, neg_m, s_addr);
-            l_run += lsum;
-            if (lane == 0 && q == 0 && X == 0) trace_stamp(p, first, t, 7);
-            if (kFmt == 1 && p.p_f16 && X == 0) {  // V(t) -> fp16 before P_A(t) (PV_B(t) follows PV_A(t))
-                const int gg = s0.g + t, st = gg & 1;
-                ptx::mbar_wait(bar(kBarVF + st), (gg >> 1) & 1);
-                v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
-            }
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 2);
-            if (lane == 0 && q == 3) trace_stamp(p, first, X ? rowB(t) : t, 3);
-            if (lane == 0) ptx::mbar_arrive(bar(kBarP + 2 * X + b));
-        }
-        {  // the last PV's commit covers every earlier MMA of this thread
-            const int nl = s0.n[X] + nt - 1;
-            ptx::mbar_wait(bar(kBarPV + 2 * X + (nl & 1)), s0.npv[X][nl & 1] & 1);
-        }
-        ptx::tc_fence_after();
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll 1
-        for (int ch = 0; ch < kHeadDim / 32; ++ch) {
-            float o[32];
-            ptx::tmem_ld32(o_addr + ch * 32, o);
-            ptx::tmem_wait_ld();
-            if (row_ok) {
-#pragma unroll
-                for (int c = 0; c < 32; c += 4)
-                    store4(orow, ch * 32 + c, make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
-            }
-        }
-        if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
-        ptx::tc_fence_before();
-    }
-}
-
 __device__ __forceinline__ void sm_log_claim(const RunParams& p, int op, int id, int32_t* slot_out) {
     *slot_out = -1;
     if (!p.role_log || id < 0) return;
@@ -1162,36 +883,13 @@ __device__ __forceinline__ void sm_log_claim(const RunParams& p, int op, int id,
     *slot_out = static_cast<int32_t>(slot);
 }
 
-// Shared-memory layout of the one-CTA-per-SM kernel per prefill engine family:
-//   kEng 0: Q in TMEM (32-key double-S / 64-key single-S pair engines), 64 KB of
-//           prefill rings, 3-stage decode rings (144 KB);
-//   kEng 1: Q in smem, double-buffered 64-key S (prefill_item_sq), 128 KB of prefill
-//           Q + rings, 2-stage decode rings (96 KB).
-template <int kEng>
-struct SmLayout {
-    static constexpr int kDS = kEng == 0 ? sm3::kDS : 2;  // decode ring stages per warp
-    static constexpr uint32_t kOffDec = kEng == 0 ? sm3::kPfRingBytes : sq::kRingBytes;
-    static constexpr uint32_t kOffBars = kOffDec + sm3::kDW * kDS * kDecStageBytes;
-    static constexpr int kNumBars = kEng == 0 ? sm3::kNumBars : sq::kNumBars;
-    static constexpr uint32_t kOffDecBars = kOffBars + kNumBars * 8;
-    static constexpr uint32_t kOffMisc = kOffDecBars + sm3::kDW * kDS * 8;
-    static constexpr uint32_t kSmem = kOffMisc + 64;
-    static_assert(kSmem <= 232448, "one CTA per SM: <= 227 KB dynamic smem");
-    static_assert(kOffDec % 1024 == 0, "SW128 stages are 1024-aligned");
-    static_assert(kEng != 0 || kOffBars == sm3::kOffBars, "engine-0 layout is sm3's");
-};
-
 // One CTA per SM; both engines bind items from their pools until drained.
-template <int G, int kFmt, int kEng>
+template <int G, int kFmt>
 __global__ void __launch_bounds__(sm3::kThreads, 1)
-    pod_sm_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmq,
-                  const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                  const __grid_constant__ CUtensorMap tdk, const __grid_constant__ CUtensorMap tdv) {
+    pod_sm_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmk,
+                  const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tdk,
+                  const __grid_constant__ CUtensorMap tdv) {
     using namespace sm3;
-    using L = SmLayout<kEng>;
-    constexpr uint32_t kOffDec = L::kOffDec, kOffBars = L::kOffBars, kOffDecBars = L::kOffDecBars,
-                       kOffMisc = L::kOffMisc;
-    constexpr int kDS = L::kDS;
     extern __shared__ __align__(1024) uint8_t smem[];
     // Logical warp roles (0-7 softmax, 8 producer, 9 MMA, 10.. decode).  With
     // POD_SM_SOFTMAX_HIGH the decode group takes the lowest hardware warp ids and the
@@ -1217,14 +915,9 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
     if (tid == 0) {
         if (sbase & 1023u) __trap();
         // q_full (0, 1) and p_full (22-25): one arrival per softmax warp of the block
-        if constexpr (kEng == 0) {
-            for (int i = 0; i < kNumBars; ++i)
-                ptx::mbar_init(sbase + kOffBars + 8 * i, (i <= 1 || (i >= kBarP && i < kBarP + 4)) ? kPrefillWarps
-                                                         : (kDualMma && i >= kBarKE && i < kBarVE + kNS && !(i >= kBarVF && i < kBarVE)) ? 2 : 1);
-        } else {
-            for (int i = 0; i < sq::kNumBars; ++i)
-                ptx::mbar_init(sbase + kOffBars + 8 * i, (i >= sq::kBarP && i < sq::kBarP + 4) ? kPrefillWarps : 1);
-        }
+        for (int i = 0; i < kNumBars; ++i)
+            ptx::mbar_init(sbase + kOffBars + 8 * i, (i <= 1 || (i >= kBarP && i < kBarP + 4)) ? kPrefillWarps
+                                                     : (kDualMma && i >= kBarKE && i < kBarVE + kNS && !(i >= kBarVF && i < kBarVE)) ? 2 : 1);
         for (int i = 0; i < kDW * kDS; ++i) ptx::mbar_init(sbase + kOffDecBars + 8 * i, 1);
         ptx::fence_mbar_init();
     }
@@ -1233,7 +926,6 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
         ptx::tmem_relinquish();
     }
     if (warp == kProdWarp && lane == 0) {
-        if (kEng == 1) ptx::prefetch_tmap(&tmq);
         ptx::prefetch_tmap(&tmk);
         ptx::prefetch_tmap(&tmv);
         ptx::prefetch_tmap(&tdk);
@@ -1266,9 +958,7 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
             const int id = wuni(misc[2]);
             prev_slot = misc[3];
             if (id < 0) break;
-            if constexpr (kEng == 1)
-                prefill_item_sq<kFmt>(p, &tmq, &tmk, &tdv, id, sbase, sbase + kOffBars, tmem, ps, warp, lane);
-            else if (p.pf_tn64)
+            if (p.pf_tn64)
                 prefill_item_sm64<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);
             else
                 prefill_item_sm<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);

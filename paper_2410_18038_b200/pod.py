@@ -226,7 +226,6 @@ class PlanOptions:
     precision: int = _abi.POD_PRECISION_F16PV
     out_dtype: int = _abi.POD_OUT_F32
     prefill_tile_keys: int = 0  # warp-specialised pair engine: 0 = auto, 32 or 64
-    prefill_engine: int = 0     # warp-specialised: 0 = auto, 1 = Q in TMEM, 2 = Q in smem (double-S 64-key)
 
 
 def _task(t) -> CtaTask:
@@ -251,7 +250,6 @@ class Plan:
         o.precision = options.precision
         o.out_dtype = options.out_dtype
         o.prefill_tile_keys = options.prefill_tile_keys
-        o.prefill_engine = options.prefill_engine
         tc = None
         if options.tile_override is not None:
             tc = options.tile_override._c()

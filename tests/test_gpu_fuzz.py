@@ -3,8 +3,8 @@
 48 seeded cases: GQA group 1/2/4/8, ragged decode contexts (1 .. 3000 keys, page edges
 included), chunks of 1 .. 300 rows at random offsets (0 included), prefill-only and
 decode-only batches, uniform and peaky (Q x 8) queries, and every kernel the plan can
-pick (AUTO, the two-CTA kernel, the warp-specialised kernel with its 32-key, 64-key and
-Q-in-smem engines).  Every (row, q head) and (request, q head) is compared with a float64
+pick (AUTO, the two-CTA kernel, the warp-specialised kernel with its 32-key and 64-key
+pair engines).  Every (row, q head) and (request, q head) is compared with a float64
 dense softmax(QK^T / scale) V of the same bf16 inputs gathered through the block table
 (tests/common.py::dense_layer; semantics attention.hpp:148-222, :240-333), at the
 north-star bound: max |O - O_ref| <= 2e-3 * max |O_ref| per (token, KV head) block,
@@ -29,7 +29,6 @@ KERNELS = [
     ("complement", dict(policy=POD_POLICY_COMPLEMENT)),
     ("ws32", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32)),
     ("ws64", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64)),
-    ("wssq", dict(policy=POD_POLICY_WARPSPEC, prefill_engine=2)),
 ]
 
 

@@ -70,11 +70,9 @@ def test_matches_oracle(name, mode):
     batch = make_batch(pkg.ModelShape(hq, hkv, 128, SCALE), chunk=chunk, offset=off, decode_ctx=dec)
     wl, _, out = _run(batch, mode)
     _check(wl, out)
-    # the warp-specialised one-CTA-per-SM kernel: both pair-engine tile widths with Q in
-    # TMEM, and the Q-in-smem double-buffered 64-key engine
+    # the warp-specialised one-CTA-per-SM kernel, both pair-engine tile widths
     for opts in (pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32),
-                 pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64),
-                 pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_engine=2)):
+                 pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64)):
         wl, _, out = _run(batch, mode, options=opts, wl=wl)
         _check(wl, out)
 
@@ -90,7 +88,7 @@ def test_fast_precision_bf16_p_within_loose_bound():
 
 
 @pytest.mark.parametrize("precision", [POD_PRECISION_F16PV, POD_PRECISION_SPLIT])
-@pytest.mark.parametrize("kernel", ["complement", 32, 64, "sq"])
+@pytest.mark.parametrize("kernel", ["complement", 32, 64])
 @pytest.mark.parametrize("q_scale", [1.0, 8.0])
 @pytest.mark.parametrize("name", ["hybrid_gqa4", "page_edges", "gqa8", "mha", "prefill_only"])
 def test_precision_modes_match_oracle(precision, kernel, q_scale, name):
@@ -103,7 +101,6 @@ def test_precision_modes_match_oracle(precision, kernel, q_scale, name):
     hq, hkv, chunk, off, dec = CASES[name]
     batch = make_batch(pkg.ModelShape(hq, hkv, 128, SCALE), chunk=chunk, offset=off, decode_ctx=dec)
     opts = (pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT, precision=precision) if kernel == "complement"
-            else pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_engine=2, precision=precision) if kernel == "sq"
             else pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=kernel, precision=precision))
     wl, _, out = _run(batch, options=opts, q_scale=q_scale)
     _check(wl, out)
@@ -128,14 +125,11 @@ def test_policies_and_reference_tiles(policy):
 
 # the POD kernels: two CTAs per SM (COMPLEMENT) and one warp-specialised CTA per SM with
 # its 32-key (double-S) or 64-key (single-S) pair engine
-# ... and "sq": the warp-specialised kernel's Q-in-smem, double-buffered 64-key S engine
-KERNELS = [POD_POLICY_COMPLEMENT, (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64), (POD_POLICY_WARPSPEC, "sq")]
+KERNELS = [POD_POLICY_COMPLEMENT, (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64)]
 
 
 def _kopts(kernel, **kw):
     """PlanOptions for one entry of KERNELS."""
-    if isinstance(kernel, tuple) and kernel[1] == "sq":
-        return pkg.PlanOptions(policy=kernel[0], prefill_engine=2, **kw)
     if isinstance(kernel, tuple):
         return pkg.PlanOptions(policy=kernel[0], prefill_tile_keys=kernel[1], **kw)
     return pkg.PlanOptions(policy=kernel, **kw)

@@ -32,7 +32,6 @@ def main():
     ap.add_argument("--mode", default="prefill")
     ap.add_argument("--precision", type=int, default=2)
     ap.add_argument("--keys", type=int, default=64)
-    ap.add_argument("--engine", type=int, default=0, help="prefill_engine (2: Q in smem, double-buffered S)")
     ap.add_argument("--chunk", type=int, default=0, help="override the config's chunk (32 rows x G=4 = one M-block)")
     a = ap.parse_args()
     assert os.environ.get("POD_TRACE"), "set POD_TRACE=1 with a POD_TRACE_STAMPS build (POD_LIB)"
@@ -46,8 +45,7 @@ def main():
         import dataclasses
         gpu = dataclasses.replace(gpu, num_sms=hkv)
     op = PodAttention(batch, gpu=gpu,
-                      options=pkg.PlanOptions(policy=7, prefill_tile_keys=0 if a.engine == 2 else a.keys,
-                                              prefill_engine=a.engine, precision=a.precision))
+                      options=pkg.PlanOptions(policy=7, prefill_tile_keys=a.keys, precision=a.precision))
     log = op.enable_role_log(768 * 8)
     out = op.alloc_outputs()
     for _ in range(2):
@@ -58,7 +56,7 @@ def main():
     tr = log.view(-1, 8)[nrec:].cpu().long() & 0xffffffff
     A, B = tr[:384], tr[384:768]
     nt = int((A[:, 1] != 0).sum())
-    print(f"{a.config} chunk {chunk} {a.mode} precision {a.precision} keys {a.keys} engine {op.info.prefill_engine}: "
+    print(f"{a.config} chunk {chunk} {a.mode} precision {a.precision} keys {a.keys}: "
           f"{nt} tiles traced")
     if nt < 40:
         return
@@ -71,7 +69,7 @@ def main():
     def d(x, y):  # y - x with 32-bit wrap
         return (y - x) & 0xffffffff
 
-    if a.keys == 32 and a.engine != 2:  # the 32-key double-S engine's stamps (pod_sm.cuh)
+    if a.keys == 32:  # the 32-key double-S engine's stamps (pod_sm.cuh)
         rng = range(16, min(nt, 128) - 16)
         rows32 = {
             "period per 32-key tile (S_A(t) ready -> S_A(t+1) ready)": [d(A[t, 1], A[t + 1, 1]) for t in rng],
@@ -93,7 +91,6 @@ def main():
         "A arrive(w3) -> MMA sees P_A": [d(A[t, 3], A[t, 4]) for t in rng],
         "MMA issue PV_A + QK_A": [d(A[t, 4], A[t, 5]) for t in rng],
         "QK_A(t+1) issued -> S_A(t+1) ready": [d(A[t, 5], A[t + 1, 1]) for t in rng],
-        "(engine 2) QK_A(t+2) issued -> S_A(t+2) ready": [d(A[t, 5], A[t + 2, 1]) for t in rng],
         "A waits S (k0 -> k1)": [d(A[t, 0], A[t, 1]) for t in rng],
         "  A: S ready -> S in registers (tcgen05.ld)": [d(A[t, 1], A[t, 6]) for t in rng],
         "  A: max, rescale check, exp, P pack + tcgen05.st": [d(A[t, 6], A[t, 7]) for t in rng],
