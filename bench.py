@@ -646,6 +646,9 @@ def main():
         "serial_best": {k: {"us": round(v[0] * 1000, 2), "kernel": v[1]} for k, v in r["best"].items()},
         "combined_roofline_us": round(roof_us, 2), "combined_roofline_frac": round(roof_us / us, 4),
         "prefill_tensor_frac_alone": round(t_pf_roof / max(r["t_pf"] * 1000, 1e-9), 4) if chunk else None,
+        # the same against the fastest prefill-alone of any kernel (serial_best.prefill)
+        "prefill_tensor_frac_best": (round(t_pf_roof / (r["best"]["prefill"][0] * 1000), 4)
+                                     if chunk and "prefill" in r["best"] else None),
         "decode_hbm_frac_alone": round(t_dec_roof / max(r["t_dec"] * 1000, 1e-9), 4) if b else None,
         "tokens_per_s": round((chunk + b) / (us * 1e-6), 1),
         "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
