@@ -177,3 +177,15 @@ def test_baseline_config_full_size_every_kernel(name, kernel):
     op, out = _run(wl, batch, *kernel)
     assert op.info.policy == kernel[0]
     _check_dense(wl, out)
+
+
+@pytest.mark.parametrize("chunk,ctx,nb", [(512, 65536, 8), (4096, 16384, 8)])
+def test_c5_extremes_full_size(chunk, ctx, nb):
+    """C5 sweep corners (BASELINE configs[4]): a 64K context and a 4K chunk, through the
+    kernel AUTO picks, every row / request / head against the dense reference."""
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=chunk, offset=ctx - chunk, decode_ctx=[ctx] * nb)
+    wl = build_workload(batch, device="cuda")
+    op, out = _run(wl, batch)
+    worst = _check_dense(wl, out)
+    print(f"{chunk}@{ctx}+{nb}: policy {op.info.policy} keys {op.info.prefill_tile_keys} worst {worst}")
