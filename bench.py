@@ -344,6 +344,64 @@ def serial_candidates(batch):
     return pf, dc
 
 
+def bench_oproj(wl, gb, world, rank, dev, timed, hq, d=128, seed=7):
+    """The o_proj consumer on this rank's attention output: a row-
+    parallel GEMM Y += O_rank W_rank with the reduce-scatter fused into its epilogue
+    (tp.oproj -> pod_oproj_run), timed like the layer.  N = 1: the plain GEMM, beside
+    torch.matmul (cuBLAS).  N > 1: every rank reduces into the row owners' Y through
+    peer-mapped symmetric memory (no all-gather of O at all); rank 0 checks its rows."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_18038_b200.tp import oproj
+
+    hidden = hq * d
+    o = torch.cat([t for t in (gb.outputs.o_prefill, gb.outputs.o_decode) if t is not None]).reshape(gb.tokens, -1)
+    o = o.to(torch.bfloat16).contiguous()
+    kr = o.shape[1]
+    g = torch.Generator(device=dev).manual_seed(seed)
+    w_full = ((torch.rand(hidden, hidden, generator=g, device=dev) * 2 - 1) / 64).to(torch.bfloat16)
+    w = w_full[rank * kr:(rank + 1) * kr].contiguous()
+    flops = 2.0 * gb.tokens * kr * hidden
+    if world == 1:
+        y = torch.empty(gb.tokens, hidden, device=dev)
+        t, _ = timed(lambda: oproj(o, w, [y]), 10, 3)
+        t_ref, _ = timed(lambda: torch.matmul(o, w), 10, 3)
+        torch.cuda.synchronize()
+        err = float((y - o.float() @ w.float()).abs().max() / (o.float() @ w.float()).abs().max())
+        return {"us": round(t * 1000, 2), "tflops": round(flops / (t * 1e-3) / 1e12, 1),
+                "torch_matmul_us": round(t_ref * 1000, 2), "rel_err_vs_torch_fp32": err,
+                "shape": f"[{gb.tokens}][{kr}] x [{kr}][{hidden}] bf16 -> fp32", "fused_reduce_scatter": False}
+    if dist.get_backend() != "nccl":
+        return {"skipped": "peer-mapped symmetric memory needs the NCCL / CUDA backend"}
+    import torch.distributed._symmetric_memory as symm_mem
+
+    rows = (gb.tokens + world - 1) // world
+    y = symm_mem.empty(rows, hidden, dtype=torch.float32, device=dev)
+    hdl = symm_mem.rendezvous(y, dist.group.WORLD)
+    ptrs = [int(hdl.buffer_ptrs[r]) for r in range(world)]
+
+    def step():
+        oproj(o, w, ptrs, rows_per_rank=rows, accumulate=True)
+
+    y.zero_()
+    dist.barrier()
+    step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    check = None
+    o_all = torch.empty(world * gb.tokens * kr, dtype=torch.bfloat16, device=dev)  # (the check only)
+    dist.all_gather_into_tensor(o_all, o.reshape(-1))
+    o_full = o_all.view(world, gb.tokens, kr).permute(1, 0, 2).reshape(gb.tokens, world * kr)
+    if rank == 0:
+        ref = (o_full.float() @ w_full.float())[:rows]
+        check = float((y[:min(rows, gb.tokens)] - ref).abs().max() / ref.abs().max())
+    t, _ = timed(step, 10, 3)  # (the reductions accumulate across steps: timing only)
+    return {"us": round(t * 1000, 2), "tflops_per_rank": round(flops / (t * 1e-3) / 1e12, 1),
+            "shape": f"[{gb.tokens}][{kr}] x [{kr}][{hidden}] per rank, fused reduce-scatter over {world} ranks",
+            "fused_reduce_scatter": True, "rank0_rel_err": check}
+
+
 def run_pod(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -501,6 +559,13 @@ def run_pod(args, rank, world, local_rank):
     if world > 1:
         t_e2e = _max_over_ranks(t_e2e, dev)
 
+    oproj_res = None
+    if not args.no_oproj:
+        try:
+            oproj_res = bench_oproj(wl, gbs[0], world, rank, dev, timed, hq)
+        except Exception as e:  # reported, never fatal for the attention number
+            oproj_res = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     # TP self-check: the assembled layer (every rank's kernel + the all-gather) against a
     # TP1 run of the same seeded layer on rank 0 (north-star tolerance, 2e-3)
     tp_check = None
@@ -524,6 +589,7 @@ def run_pod(args, rank, world, local_rank):
     launches_per_step = 1 + (1 if (info.num_merge_rows_prefill or info.num_merge_rows_decode) else 0)  # one merge launch
     res = dict(t_fused=t_fused, ms_fused=ms_fused, t_serial=t_serial, t_pf=t_pf, t_dec=t_dec, t_e2e=t_e2e,
                t_attn=t_attn, t_append=t_append, append_bytes=append_bytes, best=best, tp_check=tp_check,
+               oproj=oproj_res,
                clocks=clocks, info=info, launches=launches_per_step, h2d=h2d, d2h=d2h, hq_r=hq_r, hkv_r=hkv_r)
     return res
 
@@ -545,6 +611,7 @@ def main():
     ap.add_argument("--split-wave-cap", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-oproj", action="store_true", help="skip the o_proj consumer measurement")
     ap.add_argument("--no-serial-search", action="store_true",
                     help="skip the search for the fastest prefill-alone / decode-alone (serial_best_us)")
     args = ap.parse_args()
@@ -667,6 +734,7 @@ def main():
                 "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": r["launches"] * args.steps,
         "tp_check": r["tp_check"],
+        "oproj": r["oproj"],
         "attention_only_us": round(r["t_attn"] * 1000, 2),
         "clocks": r["clocks"],
     }

@@ -259,6 +259,20 @@ pod_status pod_attn_gather_probe(const pod_plan* plan, const void* kv_pool, int6
                                  const int32_t* page_indptr, const int32_t* page_indices,
                                  int32_t req, int64_t ctx, uint16_t* out, void* stream);
 
+/* o_proj consumer of the attention output (the reference has no
+ * projection, its hot path ends at the attention output): Y += O W with O [tokens][K]
+ * bf16 (this rank's q heads, K = Hq/T x d: the o_prefill / o_decode rows as bf16,
+ * POD_OUT_BF16), W [K][N] bf16 (the W_o rows of those heads), fp32 accumulate.
+ * Under KV-head-group TP the projection is row-parallel, so no all-gather of O is
+ * needed: with accumulate = 1 every 128 x 128 output tile is reduced into the row
+ * owner's fp32 Y (y_parts[t] holds rows [t*rows_per_rank, (t+1)*rows_per_rank), mapped
+ * peer memory for t != this rank) while the GEMM runs -- a GEMM with a fused
+ * reduce-scatter.  accumulate = 0 (world = 1) stores instead.  Y must be zeroed before
+ * the reducing launches.  K % 64 == 0, N % 128 == 0.  Stream-ordered. */
+pod_status pod_oproj_run(const void* o, const void* w, int64_t tokens, int64_t k, int64_t n,
+                         void* const* y_parts, int32_t world, int64_t rows_per_rank,
+                         int32_t accumulate, void* stream);
+
 /* Benchmark utility: overwrites `bytes` of device memory (a buffer larger than the
  * 126 MB L2) with zeros, evicting the L2 between timed layers.  The kernel prefers
  * the max-shared-memory L1 carve-out, the one the POD kernels use, so the flush does

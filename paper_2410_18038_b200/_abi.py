@@ -105,6 +105,8 @@ SYMBOLS = [
                                     _vp, _vp]),
     ("pod_attn_set_role_log", C.c_int, [_vp, _vp]),
     ("pod_attn_l2_flush", C.c_int, [_vp, C.c_int64, _vp]),
+    ("pod_oproj_run", C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.c_int64, C.POINTER(_vp), C.c_int32, C.c_int64,
+                                C.c_int32, _vp]),
     ("pod_attn_gather_probe", C.c_int, [_vp, _vp, C.c_int64, _vp, _vp, C.c_int32, C.c_int64, _vp, _vp]),
     ("pod_attn_append_kv", C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int64, _vp, _vp, _vp, _vp]),
     ("pod_attn_occupancy", C.c_int, [_vp, _i32p, _i32p, _i32p]),

@@ -1293,6 +1293,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 #include "pod_sm.cuh"
+#include "pod_oproj.cuh"
 
 __global__ void __launch_bounds__(256) l2_flush_kernel(uint4* __restrict__ buf, size_t n16) {
     const uint4 z = make_uint4(0u, 0u, 0u, 0u);
@@ -1806,6 +1807,81 @@ pod_status pod_attn_append_kv(const pod_plan* plan, const void* k_new_prefill, c
         chunk > 0 ? static_cast<int>(plan->batch.prefill.position_offset) : 0, ndec, hkv, plan->batch.kv_layout);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "append_kv launch");
+    return POD_OK;
+}
+
+pod_status pod_oproj_run(const void* o, const void* w, int64_t tokens, int64_t k, int64_t n, void* const* y_parts,
+                         int32_t world, int64_t rows_per_rank, int32_t accumulate, void* stream) {
+    if (!o || !w || !y_parts || tokens < 1 || k < 1 || n < 1 || world < 1 || world > oproj::kMaxWorld)
+        return POD_ERR_INVALID_ARGUMENT;
+    if (k % oproj::kBK || n % oproj::kBN) {
+        set_last_error("pod_oproj_run: K must be a multiple of 64 and N of 128");
+        return POD_ERR_UNSUPPORTED;
+    }
+    if (!accumulate && world != 1) {
+        set_last_error("pod_oproj_run: world > 1 needs accumulate = 1 (the reduce-scatter epilogue)");
+        return POD_ERR_INVALID_ARGUMENT;
+    }
+    if (accumulate && (rows_per_rank < 1 || rows_per_rank * world < tokens)) {
+        set_last_error("pod_oproj_run: rows_per_rank * world must cover the token rows");
+        return POD_ERR_INVALID_ARGUMENT;
+    }
+    OprojParams p{};
+    for (int r = 0; r < world; ++r) {
+        if (!y_parts[r]) return POD_ERR_INVALID_ARGUMENT;
+        p.y[r] = static_cast<float*>(y_parts[r]);
+    }
+    p.world = world;
+    p.accumulate = accumulate;
+    p.rows_per_rank = accumulate ? rows_per_rank : tokens;
+    p.tokens = tokens;
+    p.k = k;
+    p.n = n;
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) {
+        set_last_error("cuTensorMapEncodeTiled unavailable");
+        return POD_ERR_CUDA;
+    }
+    CUtensorMap ta, tb;
+    const cuuint32_t estr[2] = {1, 1};
+    {  // A = O [tokens][K]: box 64 K x 128 rows, SW128 (rows past `tokens` read as zero)
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(tokens)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * 2};
+        const cuuint32_t box[2] = {64, oproj::kBM};
+        if (enc(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(o), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            set_last_error("cuTensorMapEncodeTiled(o_proj A) failed");
+            return POD_ERR_CUDA;
+        }
+    }
+    {  // B = W [K][N]: box 64 N x 64 K rows, SW128 (MN-major operand)
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(k)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n) * 2};
+        const cuuint32_t box[2] = {64, oproj::kBK};
+        if (enc(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            set_last_error("cuTensorMapEncodeTiled(o_proj B) failed");
+            return POD_ERR_CUDA;
+        }
+    }
+    {  // per device: the large dynamic shared memory limit
+        constexpr int kMaxDev = 64;
+        static std::once_flag once[kMaxDev];
+        static cudaError_t err[kMaxDev];
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess || dev < 0 || dev >= kMaxDev) return cuda_fail(e, "cudaGetDevice");
+        std::call_once(once[dev], [&] {
+            err[dev] = cudaFuncSetAttribute(oproj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, oproj::kSmem);
+        });
+        if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "o_proj attributes");
+    }
+    const dim3 grid(static_cast<unsigned>(n / oproj::kBN), static_cast<unsigned>((tokens + oproj::kBM - 1) / oproj::kBM));
+    oproj_kernel<<<grid, oproj::kThreads, oproj::kSmem, static_cast<cudaStream_t>(stream)>>>(p, ta, tb);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "o_proj launch");
     return POD_OK;
 }
 

@@ -165,3 +165,35 @@ def layer_error(o: torch.Tensor, lse: torch.Tensor, o_ref: torch.Tensor, lse_ref
     fin = torch.isfinite(lse_ref)
     el = float((lse.float() - lse_ref.float())[fin].abs().max()) if bool(fin.any()) else 0.0
     return eo, el
+
+
+def oproj(o: torch.Tensor, w: torch.Tensor, y_parts, rows_per_rank: int = 0, accumulate: bool = False,
+          stream=None) -> None:
+    """pod_oproj_run: Y (+)= O W on the GPU (the o_proj consumer).
+
+    o: [tokens][K] bf16 (this rank's heads), w: [K][N] bf16 (their W_o rows).  y_parts:
+    one fp32 [rows_per_rank][N] tensor -- or raw device address, e.g. a peer-mapped
+    symmetric-memory buffer -- per rank.  accumulate=True reduces every output tile into
+    the row owner's Y (the reduce-scatter half of row-parallel TP; Y zeroed beforehand);
+    False stores (one rank)."""
+    import ctypes as C
+
+    from ._abi import lib
+    from .pod import _check
+
+    if o.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or not o.is_contiguous() or not w.is_contiguous():
+        raise ValueError("oproj: o and w must be contiguous bf16")
+    tokens, k = o.shape
+    if w.shape[0] != k:
+        raise ValueError("oproj: o is [tokens][K], w is [K][N]")
+    n = w.shape[1]
+    ptrs = [p if isinstance(p, int) else p.data_ptr() for p in y_parts]
+    for p in y_parts:
+        if isinstance(p, torch.Tensor) and (p.dtype != torch.float32 or not p.is_contiguous()):
+            raise ValueError("oproj: y parts must be contiguous fp32")
+    arr = (C.c_void_p * len(ptrs))(*ptrs)
+    st = stream or torch.cuda.current_stream(o.device)
+    with torch.cuda.device(o.device):
+        _check(lib().pod_oproj_run(C.c_void_p(o.data_ptr()), C.c_void_p(w.data_ptr()), tokens, k, n, arr, len(ptrs),
+                                   rows_per_rank or tokens, 1 if accumulate else 0, C.c_void_p(st.cuda_stream)),
+               "pod_oproj_run")
