@@ -560,7 +560,10 @@ def run_pod(args, rank, world, local_rank):
         t_e2e = _max_over_ranks(t_e2e, dev)
 
     oproj_res = None
-    if not args.no_oproj:
+    if world > 1 and not args.oproj_tp:
+        oproj_res = {"skipped": "the multi-rank reduce-scatter run is opt-in (--oproj-tp): symmetric-memory "
+                                "peers are unvalidated on this one-GPU development setup"}
+    elif not args.no_oproj:
         try:
             oproj_res = bench_oproj(wl, gbs[0], world, rank, dev, timed, hq)
         except Exception as e:  # reported, never fatal for the attention number
@@ -612,6 +615,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--no-oproj", action="store_true", help="skip the o_proj consumer measurement")
+    ap.add_argument("--oproj-tp", action="store_true",
+                    help="at N > 1 also run the o_proj consumer's fused reduce-scatter over symmetric-memory peers")
     ap.add_argument("--no-serial-search", action="store_true",
                     help="skip the search for the fastest prefill-alone / decode-alone (serial_best_us)")
     args = ap.parse_args()
