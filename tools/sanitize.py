@@ -49,6 +49,17 @@ def main():
     ]
     for batch, opts, modes in cases:
         run(batch, opts, modes)
+    # the o_proj consumer: store and reduce-scatter epilogues (virtual ranks)
+    from paper_2410_18038_b200.tp import oproj
+    o = (torch.rand(200, 512, device="cuda") - 0.5).to(torch.bfloat16)
+    w = (torch.rand(512, 256, device="cuda") - 0.5).to(torch.bfloat16)
+    oproj(o, w, [torch.empty(200, 256, device="cuda")])
+    ys = [torch.zeros(100, 256, device="cuda") for _ in range(2)]
+    for r in range(2):
+        oproj(o[:, 256 * r:256 * (r + 1)].contiguous(), w[256 * r:256 * (r + 1)].contiguous(), ys, rows_per_rank=100,
+              accumulate=True)
+    torch.cuda.synchronize()
+    print("ok o_proj")
     print("sanitize driver done")
 
 
