@@ -131,7 +131,7 @@ struct RunParams {
     int32_t policy;
     int32_t p_split;  // prefill P as bf16 hi + lo (two PV MMAs)
     int32_t p_f16;    // POD_PRECISION_F16PV: P as fp16, V stages converted to fp16 in smem (bf16 data)
-    int32_t pf_keys;  // warp-specialised kernel: pair-engine tile width (32, 64 or 128 keys)
+    int32_t pf_tn64;  // warp-specialised kernel: 64-key single-S pair engine (prefill-dominant plans)
     const int32_t* dec_nsplit;  // KV splits of each decode request (min(splits, ctx), pod_plan.cpp)
     int32_t trace;         // debug builds (POD_TRACE_STAMPS): per-tile cycle stamps after the role log
     int32_t trace_mode;    // debug builds: 2 = serialise MMA issue with completion (execution latency probe)
@@ -1374,7 +1374,7 @@ pod_status cuda_fail(cudaError_t e, const char* where) {
 }
 
 int64_t fused_smem_bytes() { return kSmemBytes; }
-int64_t sm_smem_bytes(int keys) { return keys == 128 ? SmLay<1>::kSmem : SmLay<0>::kSmem; }
+int64_t sm_smem_bytes() { return sm3::kSmem; }
 
 struct Maps {
     CUtensorMap q, k, v;  // prefill role: SW128 boxes of 64 d x 16 tokens, Q boxes of 64 d x 128 rows
@@ -1492,7 +1492,7 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.policy = plan->opts.policy;
     p.p_split = plan->opts.precision == POD_PRECISION_SPLIT ? 1 : 0;
     p.p_f16 = plan->opts.precision == POD_PRECISION_F16PV ? 1 : 0;
-    p.pf_keys = plan->pf_keys;
+    p.pf_tn64 = plan->pf_tn64 ? 1 : 0;
     p.out_fmt = plan->opts.out_dtype;
     p.dec_nsplit = reinterpret_cast<const int32_t*>(ws + plan->ws.off_dec_nsplit);
 #if POD_TRACE_STAMPS
@@ -1548,11 +1548,7 @@ pod_status set_kernel_attributes() {
             r = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
         if (r == cudaSuccess)
-            r = cudaFuncSetAttribute(pod_sm_kernel<G, kFmt, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     SmLay<0>::kSmem);
-        if (r == cudaSuccess)
-            r = cudaFuncSetAttribute(pod_sm_kernel<G, kFmt, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     SmLay<1>::kSmem);
+            r = cudaFuncSetAttribute(pod_sm_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3::kSmem);
         err[dev] = r;
     });
     if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
@@ -1569,12 +1565,7 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
         const int items = q.num_pctas + q.num_dctas;
         if (items <= 0) return;
         if (q.policy == POD_POLICY_WARPSPEC) {
-            if (q.pf_keys == 128)
-                pod_sm_kernel<G, kFmt, 1><<<nsm, sm_threads<1>(), SmLay<1>::kSmem, s>>>(q, maps.k, maps.v, maps.dk,
-                                                                                      maps.dv);
-            else
-                pod_sm_kernel<G, kFmt, 0><<<nsm, sm_threads<0>(), SmLay<0>::kSmem, s>>>(q, maps.k, maps.v, maps.dk,
-                                                                                      maps.dv);
+            pod_sm_kernel<G, kFmt><<<nsm, sm3::kThreads, sm3::kSmem, s>>>(q, maps.k, maps.v, maps.dk, maps.dv);
         } else {
             const int grid = std::min(items, 2 * nsm);  // persistent: 2 resident CTAs per SM
             pod_fused_kernel<G, kFmt><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk, maps.dv);

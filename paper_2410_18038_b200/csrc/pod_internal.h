@@ -88,7 +88,7 @@ struct pod_plan {
     std::vector<int32_t> tile_splits;
     std::vector<int32_t> dec_pos;  // context_len - 1 per decode (KV append)
     std::vector<int32_t> dec_nsplit;  // KV splits per decode request (min(splits, ctx))
-    int32_t pf_keys = 0;           // warp-specialised: pair-engine tile width, 32 / 64 / 128 keys (pod_plan.cpp)
+    bool pf_tn64 = false;          // warp-specialised: 64-key pair engine (see pod_plan.cpp)
     int64_t decode_splits = 1;     // largest split count (partials' stride)
     int64_t dec_split_base = 1;    // splits of requests [0, dec_tail_start)
     int64_t dec_tail_start = 0;    // first request with decode_splits splits
@@ -113,6 +113,6 @@ namespace pod {
 // Dynamic shared memory of the fused / prefill kernel (defined in pod_attn.cu).
 int64_t fused_smem_bytes();
 // Dynamic shared memory of the warp-specialised one-CTA-per-SM kernel.
-int64_t sm_smem_bytes(int keys);
+int64_t sm_smem_bytes();
 void set_last_error(const std::string& s);
 }  // namespace pod

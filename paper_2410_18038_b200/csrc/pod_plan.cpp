@@ -285,7 +285,7 @@ void lower(pod_plan& p) {
     // so they serve batches with a decode share below 0.57.
     {
         const int32_t keys = p.opts.prefill_tile_keys;
-        p.pf_keys = !(warpspec && p.batch.has_prefill) ? 0 : keys != 0 ? keys : decode_share(p) < 0.57 ? 64 : 32;
+        p.pf_tn64 = warpspec && p.batch.has_prefill && (keys == 64 || (keys == 0 && decode_share(p) < 0.57));
     }
     // Whole waves (warp-specialised kernel): the decode items are claimed in id order
     // (request-major) by one decode group per SM, so a count that is not a multiple of
@@ -432,7 +432,7 @@ pod_tile_config b200_tile_config(const pod_plan& p) {
     const int rows = (two_blocks ? 2 : 1) * pod::kMBlock;
     c.prefill_tile_q = std::max(1, rows / group);
     c.tile_kv = pod::kKvTile;
-    c.shared_mem_per_cta = static_cast<double>(p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes(0)
+    c.shared_mem_per_cta = static_cast<double>(p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes()
                                                                                    : pod::fused_smem_bytes());
     c.virtual_decode = 1;
     return c;
@@ -514,7 +514,7 @@ void build(pod_plan& p) {
     if (!p.decode_ctx.empty()) decompose_decode(p);
     lower(p);
     scheduler_ratio(p);
-    p.smem_bytes = p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes(p.pf_keys) : pod::fused_smem_bytes();
+    p.smem_bytes = p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes() : pod::fused_smem_bytes();
     layout_workspace(p);
 }
 
@@ -577,11 +577,8 @@ pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const p
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: precision must be a POD_PRECISION_* value");
         if (p->opts.out_dtype < POD_OUT_F32 || p->opts.out_dtype > POD_OUT_F16)
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: out_dtype must be a POD_OUT_* value");
-        {
-            const int32_t k = p->opts.prefill_tile_keys;
-            if (k != 0 && k != 32 && k != 64 && k != 128)
-                fail(POD_ERR_INVALID_ARGUMENT, "pod_options: prefill_tile_keys must be 0, 32, 64 or 128");
-        }
+        if (p->opts.prefill_tile_keys != 0 && p->opts.prefill_tile_keys != 32 && p->opts.prefill_tile_keys != 64)
+            fail(POD_ERR_INVALID_ARGUMENT, "pod_options: prefill_tile_keys must be 0, 32 or 64");
         build(*p);
         p->opts.tile_override = nullptr;  // do not keep caller pointers
         *out = p;
@@ -616,7 +613,7 @@ pod_status pod_attn_plan_get_info(const pod_plan* p, pod_plan_info* out) {
     out->num_merge_rows_prefill = p->merge_rows_prefill;
     out->num_merge_rows_decode = p->merge_rows_decode;
     out->policy = p->opts.policy;
-    out->prefill_tile_keys = p->opts.policy == POD_POLICY_WARPSPEC && p->batch.has_prefill ? p->pf_keys : 0;
+    out->prefill_tile_keys = p->opts.policy == POD_POLICY_WARPSPEC && p->batch.has_prefill ? (p->pf_tn64 ? 64 : 32) : 0;
     return POD_OK;
 }
 

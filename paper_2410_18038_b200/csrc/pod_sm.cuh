@@ -18,7 +18,7 @@
 // traffic per row), ping-ponging the tensor core between the blocks' softmax.
 // Two tile widths share the layout: 32-key tiles with double-buffered S
 // (prefill_item_sm, decode-dominant plans) and 64-key tiles with one S buffer per
-// block (prefill_item_sm64, prefill-dominant plans; RunParams::pf_keys).
+// block (prefill_item_sm64, prefill-dominant plans; RunParams::pf_tn64).
 //
 // Role binding is still SM-aware and dynamic: every SM hosts both roles for as
 // long as both pools have work (the placement the POD scheduler aims for,
@@ -28,20 +28,6 @@
 
 #ifndef POD_SM_SOFTMAX_HIGH
 #define POD_SM_SOFTMAX_HIGH 0
-#endif
-// the 128-key pair engine's kernel instance (prefill_item_sm128): K / V ring stages and
-// its decode group (warps x ring stages per warp)
-#ifndef POD_SM128_KSTAGES
-#define POD_SM128_KSTAGES 1
-#endif
-#ifndef POD_SM128_VSTAGES
-#define POD_SM128_VSTAGES 2
-#endif
-#ifndef POD_SM128_DEC_WARPS
-#define POD_SM128_DEC_WARPS 4
-#endif
-#ifndef POD_SM128_DEC_STAGES
-#define POD_SM128_DEC_STAGES 2
 #endif
 #ifndef POD_SM_MERGED_EMPTY
 #define POD_SM_MERGED_EMPTY 1
@@ -569,7 +555,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
 
 // ---------------------------------------------------------------------------
 // The pair engine over 64-key K/V tiles with ONE S buffer per block (plans with
-// pf_keys == 64: prefill-dominant batches, pod_plan.cpp).
+// pf_tn64: prefill-dominant batches, pod_plan.cpp).
 // TMEM keeps the same columns (Q_A | Q_B | S_A | S_B | O_A | O_B, S now 64 keys
 // wide): per 64 keys a block issues 8 QK (N = 64) + 8 PV MMAs instead of 2 x 12,
 // and half the barrier hops.  With S single-buffered, QK_X(t+1) follows PV_X(t)
@@ -881,358 +867,6 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
     }
 }
 
-// ---------------------------------------------------------------------------
-// The pair engine over 128-key K/V tiles (plans with pf_keys == 128: prefill-dominant
-// batches; its own kernel instance, pod_sm_kernel<G, kFmt, 1>, with a smaller decode
-// group).  Per 64-key tile pair the 64-key engine pays ~1000 cycles of softmax fixed
-// cost and two barrier hops per block against 1024 cycles of MMA; a
-// 128-key tile halves both per key.  TMEM cannot hold Q next to two 128-key S buffers
-// and two O accumulators, so Q moves to shared memory and QK^T becomes an SS-MMA:
-//   TMEM  S_A [0,128) | S_B [128,256) | O_A [256,384) | O_B [384,512); P (16-bit)
-//         over S: keys 0-63 in columns [0,32), keys 64-127 in [64,96) (lo parts of
-//         POD_PRECISION_SPLIT 32 columns after each)
-//   smem  Q_A | Q_B (32 KB each, SW128 K-major, written by the softmax warps),
-//         K ring (32 KB stages, [d-half][128 keys][64 d]), V ring (32 KB stages,
-//         page-major), then the decode group's rings.
-// The softmax holds 64 scores at a time (the register budget of a 448-thread CTA):
-// the row max reads S in two halves, the exponentials run on the upper half first
-// (still in registers, P to columns [64,96)) and then re-read the lower half (P to
-// [0,32), which only overwrites columns already read).
-namespace sm128 {
-constexpr int kTN = 128;
-constexpr int kNSK = POD_SM128_KSTAGES, kNSV = POD_SM128_VSTAGES;
-constexpr uint32_t kQBytes = kMBlock * kHeadDim * 2;       // 32 KB per block
-constexpr uint32_t kStage = kTN * kHeadDim * 2;            // 32 KB
-constexpr uint32_t kOffQ = 0, kOffK = 2 * kQBytes, kOffV = kOffK + kNSK * kStage;
-constexpr uint32_t kPfBytes = kOffV + kNSV * kStage;
-constexpr uint32_t kSA = 0, kSB = 128, kOA = 256, kOB = 384;
-static_assert(kNSK <= sm3::kNS && kNSV <= sm3::kNS, "stage barriers");
-__device__ __forceinline__ void load_tile128(const RunParams& p, const CUtensorMap* tm, uint32_t dst, uint32_t bar,
-                                             int kt, int kv_head, const PageIds& ids) {
-    int ph[8];
-#pragma unroll
-    for (int pg = 0; pg < 8; ++pg) ph[pg] = ids.get(min(kt / 16 + pg, ids.n - 1));
-#pragma unroll
-    for (int pg = 0; pg < 8; ++pg) {
-#pragma unroll
-        for (int dh = 0; dh < 2; ++dh) {
-            const uint32_t d = dst + dh * (kTN * 128) + pg * 2048;
-            if (p.kv_layout == POD_KV_HND)
-                ptx::tma_load_4d_elect(d, tm, bar, dh * 64, 0, kv_head, ph[pg]);
-            else
-                ptx::tma_load_4d_elect(d, tm, bar, dh * 64, kv_head, 0, ph[pg]);
-        }
-    }
-}
-template <int kFmt>
-__device__ __forceinline__ void issue_qk128(uint32_t tmem_s, uint32_t sQ, uint32_t sK) {
-    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kTN, 0);
-    ptx::umma_ss_k128_elect<kMBlock * 128, kTN * 128>(tmem_s, ptx::sw128_desc(sQ, 16, 1024),
-                                                      ptx::sw128_desc(sK, 16, 1024), idesc);
-}
-// O (+)= P V over 128 keys: two 64-key halves (P columns +0 and +64, V pages 0-3 and 4-7)
-template <bool kSplit, int kPvFmt>
-__device__ __forceinline__ void issue_pv128(uint32_t tmem_o, uint32_t tmem_p, uint32_t sV, bool accumulate) {
-    constexpr uint32_t idesc = ptx::idesc_f16(kPvFmt, kMBlock, kHeadDim, 1);
-    ptx::umma_pv64_elect<kSplit>(tmem_o, tmem_p, ptx::sw128_desc(sV, 2048, 1024), idesc, accumulate ? 1u : 0u);
-    ptx::umma_pv64_elect<kSplit>(tmem_o, tmem_p + 64, ptx::sw128_desc(sV + 4 * 4096, 2048, 1024), idesc, 1u);
-}
-}  // namespace sm128
-
-template <int kFmt, uint32_t kOffBars>
-__device__ void prefill_item_sm128(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv /* 5-D page map */,
-                                   int item, uint32_t sbase, uint32_t tmem, sm3::PfState& ps, int warp, int lane) {
-    using namespace sm3;
-    using sm128::kTN;
-    using sm128::kNSK;
-    using sm128::kNSV;
-    using sm128::kStage;
-    const PrefillCta job = p.pctas[item];
-    const int G = p.group;
-    const int rpb = kMBlock / G;
-    const int nblocks = (job.rows + rpb - 1) / rpb;  // 1 or 2
-    const bool hasB = nblocks > 1;
-    const BlockRange rA = prefill_block(p, job, 0);
-    const BlockRange rB = hasB ? prefill_block(p, job, 1) : rA;
-    const int kv_hi = min(job.kv_end, p.offset + (hasB ? rB.r0 + rB.nrows : rA.r0 + rA.nrows));
-    const int kt0 = rA.kt0;
-    const int nt = kv_hi > job.kv_begin ? (kv_hi - kt0 + kTN - 1) / kTN : 0;
-    const PfState s0 = uniform(ps);
-    if (nt > 0) {  // g: K/V tiles through the rings; n: S / P completions; npv[X][0]: PV commits
-        ps.g += nt;
-        ps.n[0] += nt;
-        ps.nq[0] += 1;
-        ps.npv[0][0] += 1;
-        if (hasB) {
-            ps.n[1] += nt;
-            ps.nq[1] += 1;
-            ps.npv[1][0] += 1;
-        }
-    }
-    const int pbeg = p.page_indptr[0];
-    const int npages = p.page_indptr[1] - pbeg;
-    const uint32_t bar0 = sbase + kOffBars;
-    auto bar = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
-    const uint32_t sQ = sbase + sm128::kOffQ, sK = sbase + sm128::kOffK, sV = sbase + sm128::kOffV;
-    // debug trace (POD_TRACE_STAMPS builds), as in prefill_item_sm64
-    const int first = s0.n[0] == 0 ? 0 : 1;
-    auto rowB = [&](int t) { return t < 384 ? 384 + t : 9999; };
-
-    if (warp == kProdWarp) {
-        // ------------------------------------------------ TMA producer --
-        // V runs one tile ahead of K in the issue order: K(t+1) waits for both QK(t) to
-        // finish with the K stage, V(t+1) only for PV(t-1) -- it lands early enough for
-        // block A's softmax warps to convert it to fp16 (F16PV) off the P -> PV path.
-        PageIds ids;
-        ids.init(p.page_indices + pbeg, npages, kt0 / 16);
-        auto load_k = [&](int t) {
-            const int gg = s0.g + t, sk = gg % kNSK;
-            if (gg >= kNSK) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarKE + sk), ((gg / kNSK) - 1) & 1);
-            ptx::mbar_arrive_expect_tx_elect(bar(kBarKF + sk), kStage);
-            sm128::load_tile128(p, tmk, sK + sk * kStage, bar(kBarKF + sk), kt0 + t * kTN, job.kv_head, ids);
-            if (lane == 0) trace_stamp(p, first, rowB(t), 6);
-        };
-        auto load_v = [&](int t) {
-            const int gg = s0.g + t, st = gg % kNSV;
-            if (gg >= kNSV) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarVE + st), ((gg / kNSV) - 1) & 1);
-            ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
-            prefill_load_v_pages<8>(tmv, sV + st * kStage, bar(kBarVF + st), kt0 + t * kTN, job.kv_head, ids);
-            if (lane == 0) trace_stamp(p, first, rowB(t), 7);
-        };
-        if (nt > 0 && kNSV >= 2) {
-            load_k(0);
-            load_v(0);
-            if (nt > 1) load_v(1);
-            for (int t = 1; t < nt; ++t) {
-                load_k(t);
-                if (t + 1 < nt) load_v(t + 1);
-            }
-        } else {  // one V stage: V(t+1) can only follow PV(t), after K(t+1)
-            for (int t = 0; t < nt; ++t) {
-                load_k(t);
-                load_v(t);
-            }
-        }
-    } else if (warp == kMmaWarp) {
-        // -------------------------------------------------- MMA issuer --
-        auto mma_issuer = [&](auto pv_c) {  // kPv as in prefill_item_sm
-            constexpr int kPv = decltype(pv_c)::value;
-            constexpr bool kSplit = kPv == 0;
-            constexpr int kPvFmt = kPv == 2 ? 0 : kFmt;
-            if (nt == 0) return;
-            ptx::mbar_wait(bar(0), s0.nq[0] & 1);
-            if (hasB) ptx::mbar_wait(bar(1), s0.nq[1] & 1);
-            {
-                const int gg = s0.g, sk = gg % kNSK;
-                ptx::mbar_wait(bar(kBarKF + sk), (gg / kNSK) & 1);
-                ptx::tc_fence_after();
-                sm128::issue_qk128<kFmt>(tmem + sm128::kSA, sQ, sK + sk * kStage);
-                ptx::umma_commit_elect(bar(kBarS + 0));
-                if (hasB) {
-                    sm128::issue_qk128<kFmt>(tmem + sm128::kSB, sQ + sm128::kQBytes, sK + sk * kStage);
-                    ptx::umma_commit_elect(bar(kBarS + 1));
-                }
-                ptx::umma_commit_elect(bar(kBarKE + sk));
-            }
-            for (int t = 0; t < nt; ++t) {
-                const int gg = s0.g + t, st = gg % kNSV;
-                const int g1 = gg + 1, sk1 = g1 % kNSK;
-                const bool more = t + 1 < nt, last = t + 1 == nt;
-#pragma unroll
-                for (int X = 0; X < 2; ++X) {
-                    if (X == 1 && !hasB) break;
-                    const int n = s0.n[X] + t;
-                    sm64::wait_mma(bar(kBarP + X), n & 1);
-                    if (lane == 0) trace_stamp(p, first, X ? rowB(t) : t, 4);
-                    if (X == 0) ptx::mbar_wait(bar(kBarVF + st), (gg / kNSV) & 1);
-                    ptx::tc_fence_after();
-                    sm128::issue_pv128<kSplit, kPvFmt>(tmem + (X ? sm128::kOB : sm128::kOA),
-                                                       tmem + (X ? sm128::kSB : sm128::kSA), sV + st * kStage, t > 0);
-                    if (last) ptx::umma_commit_elect(bar(kBarPV + X));
-                    if (more) {
-                        if (X == 0) {
-                            ptx::mbar_wait(bar(kBarKF + sk1), (g1 / kNSK) & 1);
-                            ptx::tc_fence_after();
-                        }
-                        sm128::issue_qk128<kFmt>(tmem + (X ? sm128::kSB : sm128::kSA), sQ + X * sm128::kQBytes,
-                                                 sK + sk1 * kStage);
-                        ptx::umma_commit_elect(bar(kBarS + X));
-                    }
-                    if (lane == 0) trace_stamp(p, first, X ? rowB(t) : t, 5);
-                }
-                ptx::umma_commit_elect(bar(kBarVE + st));           // V(t): both PVs issued above
-                if (more) ptx::umma_commit_elect(bar(kBarKE + sk1));  // K(t+1): both QKs
-            }
-        };
-        if (kFmt == 1 && p.p_f16)
-            mma_issuer(std::integral_constant<int, 2>{});
-        else if (p.p_split != 0)
-            mma_issuer(std::integral_constant<int, 0>{});
-        else
-            mma_issuer(std::integral_constant<int, 1>{});
-    } else if (warp < kProdWarp) {
-        // ------------------------------------ softmax (4 warps per block) --
-        const int X = warp >> 2;  // block
-        if (X == 1 && !hasB) return;
-        const int q = warp & 3;   // TMEM lane quadrant
-        const BlockRange br = X ? rB : rA;
-        const int m = q * 32 + lane;
-        const int my_r = br.r0 + m / G;
-        const bool row_ok = (m / G) < br.nrows;
-        const int vis = p.offset + my_r;
-        const int qhead = job.kv_head * G + m % G;
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        const uint32_t o_addr = lane_base + (X ? sm128::kOB : sm128::kOA);
-        const uint32_t s_addr = lane_base + (X ? sm128::kSB : sm128::kSA);
-        ORow orow;
-        float* lrow;
-        if (job.n_splits == 1) {
-            orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim, p.out_fmt);
-            lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
-        } else {
-            const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
-            orow = out_row(p.ppart_o, row * kHeadDim, 0);
-            lrow = p.ppart_lse + row;
-        }
-        if (nt == 0) {
-            if (row_ok) {
-                for (int c = 0; c < kHeadDim; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
-                *lrow = -INFINITY;
-            }
-            return;
-        }
-        {  // Q row -> shared memory, SW128 K-major (A operand of the SS QK^T); rows past the chunk are zero
-            const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(p.q_prefill) +
-                                                              (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim);
-            const uint32_t dst = sQ + X * sm128::kQBytes + static_cast<uint32_t>(m) * 128u;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint4 v = row_ok ? __ldg(src + j) : make_uint4(0u, 0u, 0u, 0u);
-                const uint32_t a = dst + (j >> 3) * (kMBlock * 128u) + ((static_cast<uint32_t>(j & 7) ^ (m & 7)) << 4);
-                asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                             : "memory");
-            }
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(bar(X));
-        }
-        // POD_PRECISION_F16PV: block A converts V(t+1) after handing over P(t)
-        auto v_to_f16 = [&](int t) {
-            const int gg = s0.g + t, st = gg % kNSV;
-            ptx::mbar_wait(bar(kBarVF + st), (gg / kNSV) & 1);
-            v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
-        };
-        if (kFmt == 1 && p.p_f16 && X == 0) v_to_f16(0);
-        float m_run = -INFINITY, l_run = 0.f;
-        for (int t = 0; t < nt; ++t) {
-            const int n = s0.n[X] + t;
-            if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 0);
-            sm64::wait_softmax(bar(kBarS + X), n & 1);  // also: PV_X(t-1) complete
-            if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 1);
-            ptx::tc_fence_after();
-            const int kb = kt0 + t * kTN;
-            const int lo = max(job.kv_begin - kb, 0);
-            const int hi = row_ok ? min(min(job.kv_end, vis + 1) - kb, kTN) : 0;
-            const bool full = __all_sync(0xffffffffu, lo == 0 && hi == kTN);
-            float s[64];
-            auto load_half = [&](int h) {
-                ptx::tmem_ld32(s_addr + 64 * h, *reinterpret_cast<float(*)[32]>(&s[0]));
-                ptx::tmem_ld32(s_addr + 64 * h + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
-                ptx::tmem_wait_ld();
-                if (!full) {
-#pragma unroll
-                    for (int c = 0; c < 64; ++c)
-                        if (64 * h + c < lo || 64 * h + c >= hi) s[c] = -INFINITY;
-                }
-            };
-            load_half(0);
-            const float max0 = row_max<64>(s);
-            load_half(1);
-            const float tmax = fmaxf(max0, row_max<64>(s));
-            if (lane == 0 && q == 0 && X == 0) trace_stamp(p, first, t, 6);
-            const float m_new = fmaxf(m_run, tmax * p.sl2);
-            const bool need = m_new > m_run + 8.f;  // lazy rescale (see prefill_item)
-            const float m_use = need ? m_new : m_run;
-            const float factor = need ? ptx::ex2(m_run - m_new) : 1.f;
-            l_run *= factor;
-            m_run = m_use;
-            if (t > 0 && __any_sync(0xffffffffu, need)) {
-#pragma unroll 1
-                for (int ch = 0; ch < kHeadDim / 32; ++ch) {
-                    float o[32];
-                    ptx::tmem_ld32(o_addr + ch * 32, o);
-                    ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int c = 0; c < 32; ++c) o[c] *= factor;
-                    ptx::tmem_st32(o_addr + ch * 32, o);
-                }
-            }
-            const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
-            auto p_half = [&](uint32_t addr) {
-                if (kFmt == 1 && p.p_f16)
-                    return softmax_p_row<kFmt, 3, 64>(s, p.sl2, neg_m, addr);
-                else if (kFmt == 1 && p.p_split)
-                    return softmax_p_row<kFmt, 1, 64>(s, p.sl2, neg_m, addr);
-                else if (p.p_split)
-                    return softmax_p_row<kFmt, 2, 64>(s, p.sl2, neg_m, addr);
-                else
-                    return softmax_p_row<kFmt, 0, 64>(s, p.sl2, neg_m, addr);
-            };
-            float lsum = p_half(s_addr + 64);  // keys 64-127 (in registers) -> columns [64, 96)
-            load_half(0);                      // keys 0-63 again -> columns [0, 32)
-            lsum += p_half(s_addr);
-            l_run += lsum;
-            if (lane == 0 && q == 0 && X == 0) trace_stamp(p, first, t, 7);
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 2);
-            if (lane == 0 && q == 3) trace_stamp(p, first, X ? rowB(t) : t, 3);
-            if (lane == 0) ptx::mbar_arrive(bar(kBarP + X));
-            if (kFmt == 1 && p.p_f16 && X == 0 && t + 1 < nt) v_to_f16(t + 1);  // off the P(t) -> PV(t) path
-        }
-        ptx::mbar_wait(bar(kBarPV + X), s0.npv[X][0] & 1);  // the last PV (commit covers all)
-        ptx::tc_fence_after();
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll 1
-        for (int ch = 0; ch < kHeadDim / 32; ++ch) {
-            float o[32];
-            ptx::tmem_ld32(o_addr + ch * 32, o);
-            ptx::tmem_wait_ld();
-            if (row_ok) {
-#pragma unroll
-                for (int c = 0; c < 32; c += 4)
-                    store4(orow, ch * 32 + c,
-                           make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
-            }
-        }
-        if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
-        ptx::tc_fence_before();
-    }
-}
-
-// Shared-memory layout of the two kernel instances: kE = 0 (32- / 64-key engines, six
-// decode warps x 3 stages) and kE = 1 (128-key engine: Q in smem, a smaller decode group).
-template <int kE>
-struct SmLay {
-    static constexpr int kDW = sm3::kDW, kDS = sm3::kDS;
-    static constexpr uint32_t kOffDec = sm3::kOffDec, kOffBars = sm3::kOffBars, kOffDecBars = sm3::kOffDecBars,
-                              kOffMisc = sm3::kOffMisc, kSmem = sm3::kSmem;
-};
-template <>
-struct SmLay<1> {
-    static constexpr int kDW = POD_SM128_DEC_WARPS, kDS = POD_SM128_DEC_STAGES;
-    static constexpr uint32_t kOffDec = sm128::kPfBytes;
-    static constexpr uint32_t kOffBars = kOffDec + kDW * kDS * kDecStageBytes;
-    static constexpr uint32_t kOffDecBars = kOffBars + sm3::kNumBars * 8;
-    static constexpr uint32_t kOffMisc = kOffDecBars + kDW * kDS * 8;
-    static constexpr uint32_t kSmem = kOffMisc + 64;
-    static_assert(kSmem <= 232448, "one CTA per SM: <= 227 KB dynamic smem");
-    static_assert(kOffDec % 1024 == 0, "SW128 stages are 1024-aligned");
-};
-template <int kE>
-constexpr int sm_threads() { return (sm3::kDecWarp0 + SmLay<kE>::kDW) * 32; }
-
 __device__ __forceinline__ void sm_log_claim(const RunParams& p, int op, int id, int32_t* slot_out) {
     *slot_out = -1;
     if (!p.role_log || id < 0) return;
@@ -1250,16 +884,12 @@ __device__ __forceinline__ void sm_log_claim(const RunParams& p, int op, int id,
 }
 
 // One CTA per SM; both engines bind items from their pools until drained.
-template <int G, int kFmt, int kE>
-__global__ void __launch_bounds__(sm_threads<kE>(), 1)
+template <int G, int kFmt>
+__global__ void __launch_bounds__(sm3::kThreads, 1)
     pod_sm_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmk,
                   const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tdk,
                   const __grid_constant__ CUtensorMap tdv) {
     using namespace sm3;
-    using L = SmLay<kE>;
-    constexpr int kDW = L::kDW, kDS = L::kDS;
-    constexpr uint32_t kOffDec = L::kOffDec, kOffBars = L::kOffBars, kOffDecBars = L::kOffDecBars,
-                       kOffMisc = L::kOffMisc;
     extern __shared__ __align__(1024) uint8_t smem[];
     // Logical warp roles (0-7 softmax, 8 producer, 9 MMA, 10.. decode).  With
     // POD_SM_SOFTMAX_HIGH the decode group takes the lowest hardware warp ids and the
@@ -1270,7 +900,7 @@ __global__ void __launch_bounds__(sm_threads<kE>(), 1)
     const int hw_warp = POD_SM_UNIFORM_WARP ? __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0)
                                             : static_cast<int>(threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    static_assert(!POD_SM_SOFTMAX_HIGH || (kDecWarp0 == 10 && sm_threads<kE>() == 512), "role remap layout");
+    static_assert(!POD_SM_SOFTMAX_HIGH || (kDecWarp0 == 10 && sm3::kThreads == 512), "role remap layout");
     const int warp = !POD_SM_SOFTMAX_HIGH ? hw_warp
                      : hw_warp >= 8       ? hw_warp - 8    // softmax: hardware warps 8-15 (quadrant = hw % 4)
                      : hw_warp >= 6       ? hw_warp + 2    // producer, MMA: hardware warps 6, 7
@@ -1328,9 +958,7 @@ __global__ void __launch_bounds__(sm_threads<kE>(), 1)
             const int id = wuni(misc[2]);
             prev_slot = misc[3];
             if (id < 0) break;
-            if constexpr (kE == 1)
-                prefill_item_sm128<kFmt, kOffBars>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);
-            else if (p.pf_keys == 64)
+            if (p.pf_tn64)
                 prefill_item_sm64<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);
             else
                 prefill_item_sm<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);

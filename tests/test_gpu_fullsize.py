@@ -168,8 +168,7 @@ def test_baseline_config_full_size_peaky(name):
 
 
 @pytest.mark.parametrize("name", ["c2_b16", "c4"])
-@pytest.mark.parametrize("kernel", [(POD_POLICY_COMPLEMENT, 0), (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64),
-                                    (POD_POLICY_WARPSPEC, 128)])
+@pytest.mark.parametrize("kernel", [(POD_POLICY_COMPLEMENT, 0), (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64)])
 def test_baseline_config_full_size_every_kernel(name, kernel):
     """Both POD kernels (and both pair-engine widths) forced at C2 B=16 and C4."""
     _need_gpu()

@@ -29,7 +29,6 @@ KERNELS = [
     ("complement", dict(policy=POD_POLICY_COMPLEMENT)),
     ("ws32", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32)),
     ("ws64", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64)),
-    ("ws128", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=128)),
 ]
 
 

@@ -70,10 +70,9 @@ def test_matches_oracle(name, mode):
     batch = make_batch(pkg.ModelShape(hq, hkv, 128, SCALE), chunk=chunk, offset=off, decode_ctx=dec)
     wl, _, out = _run(batch, mode)
     _check(wl, out)
-    # the warp-specialised one-CTA-per-SM kernel, every pair-engine tile width
+    # the warp-specialised one-CTA-per-SM kernel, both pair-engine tile widths
     for opts in (pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32),
-                 pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64),
-                 pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=128)):
+                 pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64)):
         wl, _, out = _run(batch, mode, options=opts, wl=wl)
         _check(wl, out)
 
@@ -89,7 +88,7 @@ def test_fast_precision_bf16_p_within_loose_bound():
 
 
 @pytest.mark.parametrize("precision", [POD_PRECISION_F16PV, POD_PRECISION_SPLIT])
-@pytest.mark.parametrize("kernel", ["complement", 32, 64, 128])
+@pytest.mark.parametrize("kernel", ["complement", 32, 64])
 @pytest.mark.parametrize("q_scale", [1.0, 8.0])
 @pytest.mark.parametrize("name", ["hybrid_gqa4", "page_edges", "gqa8", "mha", "prefill_only"])
 def test_precision_modes_match_oracle(precision, kernel, q_scale, name):
@@ -125,8 +124,8 @@ def test_policies_and_reference_tiles(policy):
 
 
 # the POD kernels: two CTAs per SM (COMPLEMENT) and one warp-specialised CTA per SM with
-# its 32-key (double-S), 64-key (single-S) or 128-key (Q in smem) pair engine
-KERNELS = [POD_POLICY_COMPLEMENT, (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64), (POD_POLICY_WARPSPEC, 128)]
+# its 32-key (double-S) or 64-key (single-S) pair engine
+KERNELS = [POD_POLICY_COMPLEMENT, (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64)]
 
 
 def _kopts(kernel, **kw):
