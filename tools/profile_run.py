@@ -30,15 +30,22 @@ def main():
     ap.add_argument("--roles", default="")
     ap.add_argument("--precision", type=int, default=0)
     ap.add_argument("--split-wave-cap", type=int, default=0)
+    ap.add_argument("--prefill-balance", type=int, default=0)
+    ap.add_argument("--nsm", type=int, default=0, help="plan for this many SMs (the grid)")
     a = ap.parse_args()
     hq, hkv, chunk, off, b, ctx = CONFIGS[a.config]
     b_ = b
     shape = pkg.ModelShape(hq, hkv, 128, math.sqrt(128))
     batch = make_batch(shape, chunk=chunk, offset=off, decode_ctx=[ctx] * b)
     wl = build_workload(batch, device="cuda")
-    op = PodAttention(batch, options=pkg.PlanOptions(policy=a.policy, tile_mode=a.tile_mode,
+    import dataclasses
+    gpu = pkg.GpuSpec.from_device(0)
+    if a.nsm:
+        gpu = dataclasses.replace(gpu, num_sms=a.nsm)
+    op = PodAttention(batch, gpu=gpu, options=pkg.PlanOptions(policy=a.policy, tile_mode=a.tile_mode,
                                                      decode_splits=a.decode_splits, precision=a.precision,
-                                                     split_wave_cap=a.split_wave_cap))
+                                                     split_wave_cap=a.split_wave_cap,
+                                                     prefill_balance=a.prefill_balance))
     log = op.enable_role_log(768 * 8 + 1024) if a.roles else None
     out = op.alloc_outputs()
     evs = []
@@ -92,6 +99,27 @@ def main():
                       f"dur[p10,p50,p90]=({dur[len(dur)//10]:.1f},{dur[len(dur)//2]:.1f},{dur[9*len(dur)//10]:.1f})")
         ds = [r for r in rows if r["op"] == 1]
         ps = [r for r in rows if r["op"] == 0]
+        if ps:  # per-SM prefill item durations in claim order
+            import collections as _c
+            seq = _c.defaultdict(list)
+            for r in sorted(ps, key=lambda r: r["start_us"]):
+                seq[r["sm"]].append(round(r["end_us"] - r["start_us"], 1))
+            k = [v for v in seq.values() if len(v) >= 2]
+            if k:
+                f, s2 = sorted(v[0] for v in k), sorted(v[1] for v in k)
+                print(f"SMs with >= 2 items: {len(k)}; 1st item p50 {f[len(f)//2]} us, 2nd item p50 {s2[len(s2)//2]} us; "
+                      f"sample {k[:4]}")
+        if ps:  # per-SM prefill busy time and item count
+            import collections as _c
+            busy, cnt, last = _c.defaultdict(float), _c.Counter(), _c.defaultdict(float)
+            for r in ps:
+                busy[r["sm"]] += r["end_us"] - r["start_us"]
+                cnt[r["sm"]] += 1
+                last[r["sm"]] = max(last[r["sm"]], r["end_us"])
+            bl, el = sorted(busy.values()), sorted(last.values())
+            print(f"prefill per SM: {len(busy)} SMs, items {dict(_c.Counter(cnt.values()))}, busy us "
+                  f"p0/p50/p100 = {bl[0]:.1f}/{bl[len(bl)//2]:.1f}/{bl[-1]:.1f}, last end p0/p50/p100 = "
+                  f"{el[0]:.1f}/{el[len(el)//2]:.1f}/{el[-1]:.1f}")
         if ds:
             item_bytes = b_ * ctx * hkv * 128 * 4 / len(ds)  # bf16 K + V of one decode item
             rate = sorted(item_bytes / (r["end_us"] - r["start_us"]) / 1e3 for r in ds)
