@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define POD_ATTN_ABI_VERSION 2
+#define POD_ATTN_ABI_VERSION 1
 
 /* Mirrors the exception classes of the reference (include/attnsim/types.hpp:12-15,
  * attention.hpp:113-116,155-163,249,304; work_decomp.hpp:33-47,151-152). */
@@ -150,15 +150,7 @@ typedef struct pod_options {
     int32_t precision;       /* POD_PRECISION_* for the prefill P operand            */
     int32_t out_dtype;       /* POD_OUT_*: element type of o_prefill / o_decode (LSE stays fp32) */
     int32_t prefill_tile_keys; /* warp-specialised pair engine: 0 = by decode share, 32 or 64 forces */
-    int32_t prefill_balance;   /* warp-specialised kernel: POD_BALANCE_* (how prefill work meets the SMs) */
 } pod_options;
-
-enum {
-    POD_BALANCE_AUTO = 0,    /* balanced pieces when whole items would leave SMs without prefill work */
-    POD_BALANCE_DYNAMIC = 1, /* whole (q tile, kv head, split) items claimed at run time (atomic tickets) */
-    POD_BALANCE_PIECES = 2   /* the items' KV tiles cut into one contiguous, equal share per SM (each item
-                                in <= a few KV pieces, merged by LSE like any split); static per-SM lists */
-};
 
 enum {
     POD_OUT_F32 = 0,  /* fp32 outputs (default; the reference's AttentionPartial.o, attention.hpp:86-93) */
@@ -193,7 +185,6 @@ typedef struct pod_plan_info {
     int32_t num_merge_rows_decode;
     int32_t policy;             /* the POD_POLICY_* the plan runs (POD_POLICY_AUTO resolved) */
     int32_t prefill_tile_keys;  /* keys per prefill K/V tile of the warp-specialised pair engine (32 or 64; 0 otherwise) */
-    int32_t prefill_balanced;   /* 1: prefill work lowered to balanced per-SM pieces (POD_BALANCE_PIECES) */
 } pod_plan_info;
 
 typedef struct pod_plan pod_plan;

@@ -26,7 +26,6 @@ POD_POLICY_WARPSPEC, POD_POLICY_AUTO = 7, 8
 POD_TILE_REFERENCE, POD_TILE_B200 = 0, 1
 POD_PRECISION_SPLIT, POD_PRECISION_FAST, POD_PRECISION_F16PV = 0, 1, 2
 POD_OUT_F32, POD_OUT_BF16, POD_OUT_F16 = 0, 1, 2
-POD_BALANCE_AUTO, POD_BALANCE_DYNAMIC, POD_BALANCE_PIECES = 0, 1, 2
 
 
 class pod_shape(C.Structure):
@@ -71,8 +70,7 @@ class pod_options(C.Structure):
     _fields_ = [("policy", C.c_int32), ("tile_mode", C.c_int32), ("ctas_per_sm", C.c_int32),
                 ("virtual_decode", C.c_int32), ("split_wave_cap", C.c_int32),
                 ("decode_splits", C.c_int32), ("tile_override", C.POINTER(pod_tile_config)),
-                ("precision", C.c_int32), ("out_dtype", C.c_int32), ("prefill_tile_keys", C.c_int32),
-                ("prefill_balance", C.c_int32)]
+                ("precision", C.c_int32), ("out_dtype", C.c_int32), ("prefill_tile_keys", C.c_int32)]
 
 
 class pod_plan_info(C.Structure):
@@ -82,8 +80,7 @@ class pod_plan_info(C.Structure):
                 ("decode_splits", C.c_int64), ("prefill_ratio", C.c_int64),
                 ("decode_ratio", C.c_int64), ("smem_bytes", C.c_int64),
                 ("workspace_bytes", C.c_int64), ("num_merge_rows_prefill", C.c_int32),
-                ("num_merge_rows_decode", C.c_int32), ("policy", C.c_int32), ("prefill_tile_keys", C.c_int32),
-                ("prefill_balanced", C.c_int32)]
+                ("num_merge_rows_decode", C.c_int32), ("policy", C.c_int32), ("prefill_tile_keys", C.c_int32)]
 
 
 # (name, restype, argtypes) for every symbol include/pod_attn.h declares.

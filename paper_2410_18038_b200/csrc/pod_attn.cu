@@ -133,7 +133,6 @@ struct RunParams {
     int32_t p_f16;    // POD_PRECISION_F16PV: P as fp16, V stages converted to fp16 in smem (bf16 data)
     int32_t pf_tn64;  // warp-specialised kernel: 64-key single-S pair engine (prefill-dominant plans)
     const int32_t* dec_nsplit;  // KV splits of each decode request (min(splits, ctx), pod_plan.cpp)
-    const int32_t* pf_piece_ptr;  // POD_BALANCE_PIECES: CTA j runs prefill items [ptr[j], ptr[j + 1]); null: claims
     int32_t trace;         // debug builds (POD_TRACE_STAMPS): per-tile cycle stamps after the role log
     int32_t trace_mode;    // debug builds: 2 = serialise MMA issue with completion (execution latency probe)
     int64_t num_pages;
@@ -1126,7 +1125,7 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
     ORow out_o;
     float* out_l;
     if (mode == 0) {
-        n = tile_splits[(r / tile_q) * (p.hq / p.group) + qh / p.group];  // KV pieces of the (q tile, kv head)
+        n = tile_splits[r / tile_q];
         if (n <= 1) return;
         const size_t row = static_cast<size_t>(r) * p.hq + qh;
         po = p.ppart_o + row * kHeadDim;
@@ -1496,8 +1495,6 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.pf_tn64 = plan->pf_tn64 ? 1 : 0;
     p.out_fmt = plan->opts.out_dtype;
     p.dec_nsplit = reinterpret_cast<const int32_t*>(ws + plan->ws.off_dec_nsplit);
-    p.pf_piece_ptr = plan->pf_piece_ptr.empty() ? nullptr
-                                                : reinterpret_cast<const int32_t*>(ws + plan->ws.off_pf_piece_ptr);
 #if POD_TRACE_STAMPS
     {  // debug builds only: POD_TRACE=1 (stamps) / 2 (serialised MMA issue) after the role log
         static const char* trace_env = std::getenv("POD_TRACE");
@@ -1719,12 +1716,9 @@ pod_status pod_attn_workspace_init(const pod_plan* plan, void* workspace, void* 
     if (e == cudaSuccess && !plan->dec_nsplit.empty())
         e = cudaMemcpyAsync(ws + plan->ws.off_dec_nsplit, plan->dec_nsplit.data(),
                             plan->dec_nsplit.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && !plan->item_splits.empty())
-        e = cudaMemcpyAsync(ws + plan->ws.off_tile_splits, plan->item_splits.data(),
-                            plan->item_splits.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && !plan->pf_piece_ptr.empty())
-        e = cudaMemcpyAsync(ws + plan->ws.off_pf_piece_ptr, plan->pf_piece_ptr.data(),
-                            plan->pf_piece_ptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && !plan->tile_splits.empty())
+        e = cudaMemcpyAsync(ws + plan->ws.off_tile_splits, plan->tile_splits.data(),
+                            plan->tile_splits.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "pod_attn_workspace_init");
     return POD_OK;

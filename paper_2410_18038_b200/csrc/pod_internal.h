@@ -60,8 +60,7 @@ struct WorkspaceLayout {
     size_t off_counters = 0;
     size_t off_pctas = 0;
     size_t off_dctas = 0;
-    size_t off_tile_splits = 0;   // int32 per (prefill q tile, kv head): KV pieces of the item (item_splits)
-    size_t off_pf_piece_ptr = 0;  // int32 [num_sms + 1]: per-CTA prefill item lists (balanced plans)
+    size_t off_tile_splits = 0;   // int32 per prefill q tile: eff_splits
     size_t off_ppart_o = 0;       // [max_splits][chunk][Hq][d] fp32 (only if splits > 1)
     size_t off_ppart_lse = 0;     // [max_splits][chunk][Hq]
     size_t off_dpart_o = 0;       // [num_decodes][splits][Hq][d]
@@ -87,8 +86,6 @@ struct pod_plan {
     std::vector<pod::PrefillCta> pctas;
     std::vector<pod::DecodeCta> dctas;
     std::vector<int32_t> tile_splits;
-    std::vector<int32_t> item_splits;   // KV pieces per (q tile, kv head): the merge's split counts
-    std::vector<int32_t> pf_piece_ptr;  // POD_BALANCE_PIECES: CSR of prefill items per CTA (empty: dynamic)
     std::vector<int32_t> dec_pos;  // context_len - 1 per decode (KV append)
     std::vector<int32_t> dec_nsplit;  // KV splits per decode request (min(splits, ctx))
     bool pf_tn64 = false;          // warp-specialised: 64-key pair engine (see pod_plan.cpp)

@@ -220,104 +220,6 @@ void decompose_prefill(pod_plan& p) {
 // Lower tasks to the kernels' physical CTA tables.
 double decode_share(const pod_plan& p);
 
-// POD_BALANCE_PIECES (warp-specialised kernel): whole prefill items claimed at run time
-// leave SMs without prefill work when their count is not a multiple of the SM count
-// (C2: 128 items of 256 KV tiles on 148 SMs -> 20 idle prefill engines, 13.5 % of the
-// machine).  Instead the items' KV tiles, concatenated in item order, are cut into one
-// contiguous share of total / num_sms tiles per CTA ("stream-K" over the KV axis): an
-// item then spans <= a few CTAs as KV pieces, each piece a split of its (q tile, kv
-// head) with its own partial O / LSE, merged in KV order by the split merge.  Cuts
-// closer than kMinTiles to an item boundary snap to it (no tiny pieces).  CTA j runs
-// pieces [pf_piece_ptr[j], pf_piece_ptr[j + 1]) in order.
-int64_t prefill_item_tiles(const pod_plan& p, const pod::PrefillCta& c) {
-    const int64_t kt0 = (c.kv_begin / 16) * 16;
-    const int64_t kv_hi = std::min<int64_t>(c.kv_end, p.batch.prefill.position_offset + c.row_begin + c.rows);
-    return kv_hi > c.kv_begin ? ceil_div(kv_hi - kt0, int64_t(64)) : 0;
-}
-
-void balance_prefill(pod_plan& p) {
-    const pod_shape& s = p.shape;
-    p.pf_piece_ptr.clear();
-    const int hkv = s.num_kv_heads;
-    p.item_splits.assign(static_cast<size_t>(p.prefill_q_tiles) * hkv, 1);
-    for (const pod::PrefillCta& c : p.pctas) p.item_splits[static_cast<size_t>(c.q_tile) * hkv + c.kv_head] = c.n_splits;
-    const bool warpspec = p.opts.policy == POD_POLICY_WARPSPEC;
-    if (!warpspec || !p.batch.has_prefill || p.pctas.empty() || p.opts.prefill_balance == POD_BALANCE_DYNAMIC) return;
-    const int64_t nsm = p.dev.num_sms;
-    std::vector<int64_t> nt(p.pctas.size());
-    int64_t total = 0;
-    for (size_t i = 0; i < p.pctas.size(); ++i) total += nt[i] = prefill_item_tiles(p, p.pctas[i]);
-    constexpr int64_t kMinTiles = 8;
-    if (p.opts.prefill_balance != POD_BALANCE_PIECES) {
-        // AUTO: only where whole items leave a tenth of the machine's prefill engines idle
-        // in the last wave and every CTA's share stays well above the per-piece cost
-        const int64_t items = static_cast<int64_t>(p.pctas.size());
-        const double waves = static_cast<double>(items) / nsm;
-        const double eff = waves / std::ceil(waves);
-        if (eff > 0.9 || total < 4 * kMinTiles * nsm || decode_share(p) >= 0.57) return;
-    }
-    // cut points c_j = round(j * total / nsm), snapped to item boundaries when close
-    std::vector<int64_t> start(p.pctas.size() + 1, 0);
-    for (size_t i = 0; i < p.pctas.size(); ++i) start[i + 1] = start[i] + nt[i];
-    std::vector<int64_t> cut(nsm + 1);
-    size_t it = 0;
-    for (int64_t j = 0; j <= nsm; ++j) {
-        int64_t c = (j * total + nsm / 2) / nsm;
-        while (it + 1 < start.size() && start[it + 1] <= c) ++it;  // c in [start[it], start[it+1])
-        if (it + 1 < start.size()) {
-            const int64_t lo = start[it], hi = start[it + 1];
-            if (c - lo < kMinTiles) c = lo;
-            else if (hi - c < kMinTiles) c = hi;
-        }
-        cut[j] = std::max<int64_t>(c, j ? cut[j - 1] : 0);
-    }
-    cut[nsm] = total;
-    // pieces in CTA order
-    std::vector<pod::PrefillCta> pieces;
-    // split indices per (q tile, kv head) in KV order: items of one pair (decompose_prefill's
-    // own splits) are consecutive and KV-ordered, and so are their pieces
-    auto key = [&](const pod::PrefillCta& c) { return static_cast<size_t>(c.q_tile) * hkv + c.kv_head; };
-    std::vector<int32_t> nsplit(p.item_splits.size(), 0);
-    std::vector<int32_t> owner;  // split index per piece
-    p.pf_piece_ptr.assign(nsm + 1, 0);
-    size_t item = 0;
-    for (int64_t j = 0; j < nsm; ++j) {
-        p.pf_piece_ptr[j] = static_cast<int32_t>(pieces.size());
-        int64_t a = cut[j];
-        const int64_t e = cut[j + 1];
-        while (a < e) {
-            while (start[item + 1] <= a) ++item;
-            const int64_t b = std::min(e, start[item + 1]);
-            const pod::PrefillCta& src = p.pctas[item];
-            const int64_t kt0 = (src.kv_begin / 16) * 16;
-            pod::PrefillCta c = src;
-            const int64_t ta = a - start[item], tb = b - start[item];
-            c.kv_begin = ta == 0 ? src.kv_begin : static_cast<int32_t>(kt0 + 64 * ta);
-            c.kv_end = tb == nt[item] ? src.kv_end : static_cast<int32_t>(kt0 + 64 * tb);
-            owner.push_back(nsplit[key(src)]++);
-            pieces.push_back(c);
-            a = b;
-        }
-    }
-    p.pf_piece_ptr[nsm] = static_cast<int32_t>(pieces.size());
-    // items without tiles (nothing visible) keep one piece: they still write O = 0, LSE = -inf
-    for (size_t i = 0; i < p.pctas.size(); ++i)
-        if (nt[i] == 0) {
-            pieces.push_back(p.pctas[i]);
-            owner.push_back(nsplit[key(p.pctas[i])]++);
-            p.pf_piece_ptr[nsm] = static_cast<int32_t>(pieces.size());
-        }
-    p.max_prefill_splits = 1;
-    for (size_t k = 0; k < pieces.size(); ++k) {
-        const size_t i = key(pieces[k]);
-        pieces[k].split = owner[k];
-        pieces[k].n_splits = nsplit[i];
-        p.max_prefill_splits = std::max(p.max_prefill_splits, nsplit[i]);
-        p.item_splits[i] = nsplit[i];
-    }
-    p.pctas = std::move(pieces);
-}
-
 void lower(pod_plan& p) {
     const pod_shape& s = p.shape;
     p.pctas.clear();
@@ -437,13 +339,14 @@ void lower(pod_plan& p) {
             }
         }
     }
-    balance_prefill(p);
     p.merge_rows_prefill = 0;
-    {
-        const int group = s.num_q_heads / s.num_kv_heads;
-        for (const pod::PrefillCta& c : p.pctas)
-            if (c.n_splits > 1 && c.split == 0) p.merge_rows_prefill += c.rows * group;
-    }
+    if (p.batch.has_prefill)
+        for (long tile = 0; tile < p.prefill_q_tiles; ++tile)
+            if (p.tile_splits[tile] > 1) {
+                const long rows = std::min<long>(p.cfg.prefill_tile_q,
+                                                 p.batch.prefill.chunk_size - tile * p.cfg.prefill_tile_q);
+                p.merge_rows_prefill += static_cast<int32_t>(rows * s.num_q_heads);
+            }
     p.merge_rows_decode = 0;
     for (size_t r = 0; r < p.decode_ctx.size(); ++r)
         if (std::min<int64_t>(splits_of(r), p.decode_ctx[r]) > 1)
@@ -498,9 +401,7 @@ void layout_workspace(pod_plan& p) {
     p.ws.off_dctas = off;
     off = align(off + p.dctas.size() * sizeof(pod::DecodeCta));
     p.ws.off_tile_splits = off;
-    off = align(off + p.item_splits.size() * sizeof(int32_t));
-    p.ws.off_pf_piece_ptr = off;
-    off = align(off + p.pf_piece_ptr.size() * sizeof(int32_t));
+    off = align(off + p.tile_splits.size() * sizeof(int32_t));
     const int64_t chunk = p.batch.has_prefill ? p.batch.prefill.chunk_size : 0;
     const size_t pp = p.max_prefill_splits > 1 ? static_cast<size_t>(p.max_prefill_splits) * chunk * s.num_q_heads : 0;
     p.ws.off_ppart_o = off;
@@ -644,7 +545,6 @@ void pod_options_default(pod_options* out) {
     out->precision = POD_PRECISION_F16PV;
     out->out_dtype = POD_OUT_F32;
     out->prefill_tile_keys = 0;
-    out->prefill_balance = POD_BALANCE_AUTO;
 }
 
 pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const pod_device* dev,
@@ -677,8 +577,6 @@ pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const p
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: precision must be a POD_PRECISION_* value");
         if (p->opts.out_dtype < POD_OUT_F32 || p->opts.out_dtype > POD_OUT_F16)
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: out_dtype must be a POD_OUT_* value");
-        if (p->opts.prefill_balance < POD_BALANCE_AUTO || p->opts.prefill_balance > POD_BALANCE_PIECES)
-            fail(POD_ERR_INVALID_ARGUMENT, "pod_options: prefill_balance must be a POD_BALANCE_* value");
         if (p->opts.prefill_tile_keys != 0 && p->opts.prefill_tile_keys != 32 && p->opts.prefill_tile_keys != 64)
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: prefill_tile_keys must be 0, 32 or 64");
         build(*p);
@@ -716,7 +614,6 @@ pod_status pod_attn_plan_get_info(const pod_plan* p, pod_plan_info* out) {
     out->num_merge_rows_decode = p->merge_rows_decode;
     out->policy = p->opts.policy;
     out->prefill_tile_keys = p->opts.policy == POD_POLICY_WARPSPEC && p->batch.has_prefill ? (p->pf_tn64 ? 64 : 32) : 0;
-    out->prefill_balanced = p->pf_piece_ptr.empty() ? 0 : 1;
     return POD_OK;
 }
 

@@ -943,18 +943,11 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
         constexpr uint32_t tmem = 0u;
         PfState ps;
         int prev_slot = -1;
-        // balanced plans (POD_BALANCE_PIECES): this CTA's own contiguous list of KV pieces
-        int piece = p.pf_piece_ptr ? p.pf_piece_ptr[blockIdx.x] : 0;
-        const int piece_end = p.pf_piece_ptr ? p.pf_piece_ptr[blockIdx.x + 1] : 0;
         while (p.num_pctas > 0) {
             ptx::named_bar_sync(1, kPrefillThreads);  // the previous item is complete in every warp
             if (warp == kProdWarp && lane == 0) {
                 if (prev_slot >= 0) p.role_log[8 * prev_slot + 6] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
-                int id;
-                if (p.pf_piece_ptr)
-                    id = piece < piece_end ? piece++ : -1;
-                else
-                    id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[0], 1u));
+                int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[0], 1u));
                 if (id >= p.num_pctas) id = -1;
                 int32_t slot;
                 sm_log_claim(p, 0, id, &slot);

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     l = _abi.lib()
-    assert l.pod_attn_abi_version() == 2
+    assert l.pod_attn_abi_version() == 1
     for code, name in _abi.STATUS_NAMES.items():
         assert l.pod_status_string(code).decode() == name
 

@@ -29,7 +29,6 @@ KERNELS = [
     ("complement", dict(policy=POD_POLICY_COMPLEMENT)),
     ("ws32", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32)),
     ("ws64", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64)),
-    ("ws_pieces", dict(policy=POD_POLICY_WARPSPEC, prefill_balance=2)),
 ]
 
 

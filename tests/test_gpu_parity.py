@@ -283,35 +283,6 @@ def test_short_decode_contexts_with_more_splits_than_keys(policy):
         _check(wl, out)
 
 
-@pytest.mark.parametrize("hq,hkv,chunk,offset,ctx,nsm", [
-    (32, 8, 256, 3840, [1000, 77], 148),   # 32 items -> pieces across 148 CTAs (4-5 per item)
-    (32, 8, 512, 1536, [2048] * 8, 148),   # C1: decompose_prefill's own 2 splits, then pieces
-    (32, 8, 300, 0, [17, 600], 37),        # causal from key 0: items of unequal length, ragged chunk
-    (8, 8, 200, 900, [], 23),              # MHA prefill only
-    (16, 2, 96, 4000, [5000], 11),         # one block per item (G = 8), long KV
-])
-@pytest.mark.parametrize("keys", [32, 64])
-def test_balanced_prefill_pieces_match_oracle(hq, hkv, chunk, offset, ctx, nsm, keys):
-    """POD_BALANCE_PIECES: the prefill items' KV tiles cut into one equal contiguous share
-    per CTA (items span several CTAs as KV pieces, merged by LSE in KV order).  Against
-    the oracle, fused and serial, for plans on `nsm` SMs (the grid), both tile widths."""
-    _need_gpu()
-    import dataclasses
-
-    batch = make_batch(pkg.ModelShape(hq, hkv, 128, SCALE), chunk=chunk, offset=offset, decode_ctx=ctx)
-    gpu = dataclasses.replace(pkg.GpuSpec.from_device(0), num_sms=nsm)
-    from paper_2410_18038_b200.hybrid import PodAttention
-
-    wl = build_workload(batch, device="cuda")
-    opts = pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=keys, prefill_balance=2)
-    op = PodAttention(batch, gpu=gpu, options=opts)
-    assert op.info.prefill_balanced == 1 and op.info.num_prefill_ctas >= 1
-    for mode in ("fused", "serial"):
-        out = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, mode=mode)
-        torch.cuda.synchronize()
-        _check(wl, out)
-
-
 @pytest.mark.parametrize("chunk,offset,ctx,keys", [(256, 1000, [300, 90], 64), (16, 100, [4096] * 8, 32)])
 def test_pair_engine_tile_widths_match_oracle(chunk, offset, ctx, keys):
     """Warp-specialised kernel: prefill-dominant plans run the 64-key single-S pair

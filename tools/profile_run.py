@@ -30,7 +30,6 @@ def main():
     ap.add_argument("--roles", default="")
     ap.add_argument("--precision", type=int, default=0)
     ap.add_argument("--split-wave-cap", type=int, default=0)
-    ap.add_argument("--prefill-balance", type=int, default=0)
     ap.add_argument("--nsm", type=int, default=0, help="plan for this many SMs (the grid)")
     a = ap.parse_args()
     hq, hkv, chunk, off, b, ctx = CONFIGS[a.config]
@@ -44,8 +43,7 @@ def main():
         gpu = dataclasses.replace(gpu, num_sms=a.nsm)
     op = PodAttention(batch, gpu=gpu, options=pkg.PlanOptions(policy=a.policy, tile_mode=a.tile_mode,
                                                      decode_splits=a.decode_splits, precision=a.precision,
-                                                     split_wave_cap=a.split_wave_cap,
-                                                     prefill_balance=a.prefill_balance))
+                                                     split_wave_cap=a.split_wave_cap))
     log = op.enable_role_log(768 * 8 + 1024) if a.roles else None
     out = op.alloc_outputs()
     evs = []
