@@ -102,6 +102,7 @@ constexpr int kNS = POD_SM_STAGES;                             // K and V ring s
 constexpr uint32_t kStage = kTN * kHeadDim * 2;                // 8 KB: [d-half][32 keys][64 d], SW128
 constexpr uint32_t kOffKs = 0;
 constexpr uint32_t kOffVs = kNS * kStage;
+static_assert(kNS * kStage >= 8 * 4096, "the epilogue's 8 warp tiles (store_o_rows) fit the K ring");
 #ifndef POD_SM64_BATCHED_PV
 #define POD_SM64_BATCHED_PV 1  // 64-key engine: the 8 PV MMAs of a tile in one elected asm block
 #endif
@@ -191,6 +192,51 @@ __device__ __forceinline__ void load_tile32(const RunParams& p, const CUtensorMa
     }
 }
 }  // namespace sm3
+
+// Epilogue of one softmax warp (its 32 rows of a block): O (TMEM, 128 fp32 columns) x inv
+// to the rows' outputs.  A lane owns a row, so direct stores scatter every instruction over
+// 32 rows (16 B pieces 512 B - 16 KB apart); measured at C1 the item epilogues all run at
+// once and took ~11k cycles.  Instead each 32-column chunk goes through a warp-private 4 KB
+// smem tile (XOR-swizzled 16 B chunks: conflict-free both ways) and leaves as whole 128 B row
+// segments, 4 rows per store instruction.  `tile` is in the K ring, idle once the item's
+// last PV of this block completed (every QK of the item was issued before it).
+__device__ __forceinline__ void store_o_rows(uint32_t o_addr, float inv, const ORow& orow, bool row_ok,
+                                             uint32_t tile, int lane) {
+    // destination of the 8 rows this lane writes: rows 4i + lane / 8
+    char* dst[8];
+    bool ok[8];
+    const unsigned long long mine = reinterpret_cast<unsigned long long>(orow.ptr);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = 4 * i + (lane >> 3);
+        dst[i] = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, mine, r));
+        ok[i] = __shfl_sync(0xffffffffu, row_ok ? 1 : 0, r) != 0;
+    }
+    const int c4 = lane & 7;  // the 16 B column chunk this lane writes
+#pragma unroll 1
+    for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+        float o[32];
+        ptx::tmem_ld32(o_addr + ch * 32, o);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t a = tile + lane * 128u + ((static_cast<uint32_t>(c) ^ (lane & 7)) << 4);
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(o[4 * c] * inv),
+                         "f"(o[4 * c + 1] * inv), "f"(o[4 * c + 2] * inv), "f"(o[4 * c + 3] * inv)
+                         : "memory");
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int r = 4 * i + (lane >> 3);
+            const uint32_t a = tile + r * 128u + ((static_cast<uint32_t>(c4) ^ (r & 7)) << 4);
+            float4 v;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+            if (ok[i]) store4(ORow{dst[i], orow.fmt}, ch * 32 + 4 * c4, v);
+        }
+        __syncwarp();
+    }
+}
 
 // One prefill item of the warp-specialised engine: up to two 128-row M-blocks of
 // one (q tile, KV head, KV split) CtaTask over the same 32-key K/V tiles.
@@ -535,18 +581,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         }
         ptx::tc_fence_after();
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll 1
-        for (int ch = 0; ch < kHeadDim / 32; ++ch) {
-            float o[32];
-            ptx::tmem_ld32(o_addr + ch * 32, o);
-            ptx::tmem_wait_ld();
-            if (row_ok) {
-#pragma unroll
-                for (int c = 0; c < 32; c += 4)
-                    store4(orow, ch * 32 + c,
-                           make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
-            }
-        }
+        store_o_rows(o_addr, inv, orow, row_ok, sbase + kOffKs + static_cast<uint32_t>(warp) * 4096u, lane);
         if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
         ptx::tc_fence_before();
     }
@@ -587,6 +622,7 @@ constexpr int kNSK = POD_SM64_KSTAGES;      // K stages
 constexpr uint32_t kStage = kTN * kHeadDim * 2;  // 16 KB: [d-half][64 keys][64 d], SW128
 static_assert((kNS + kNSK) * kStage <= sm3::kPfRingBytes, "the prefill ring region holds both rings");
 static_assert(kNSK <= sm3::kNS, "K stage barriers");
+static_assert(kNSK * kStage >= 8 * 4096, "the epilogue's 8 warp tiles (store_o_rows) fit the K ring");
 __device__ __forceinline__ void load_tile64(const RunParams& p, const CUtensorMap* tm, uint32_t dst, uint32_t bar,
                                             int kt, int kv_head, const PageIds& ids) {
     int ph[4];
@@ -847,21 +883,13 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             if (lane == 0) ptx::mbar_arrive(bar(kBarP + X));
             if (kFmt == 1 && p.p_f16 && X == 0 && t + 1 < nt) v_to_f16(t + 1);  // off the P(t) -> PV(t) path
         }
+        if (lane == 0 && warp == 0) trace_stamp(p, first, 766, 0);
         ptx::mbar_wait(bar(kBarPV + X), s0.npv[X][0] & 1);  // the last PV (commit covers all)
+        if (lane == 0 && warp == 0) trace_stamp(p, first, 766, 1);
         ptx::tc_fence_after();
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll 1
-        for (int ch = 0; ch < kHeadDim / 32; ++ch) {
-            float o[32];
-            ptx::tmem_ld32(o_addr + ch * 32, o);
-            ptx::tmem_wait_ld();
-            if (row_ok) {
-#pragma unroll
-                for (int c = 0; c < 32; c += 4)
-                    store4(orow, ch * 32 + c,
-                           make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
-            }
-        }
+        store_o_rows(o_addr, inv, orow, row_ok, sbase + kOffKs + static_cast<uint32_t>(warp) * 4096u, lane);
+        if (lane == 0 && warp == 0) trace_stamp(p, first, 766, 2);
         if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
         ptx::tc_fence_before();
     }
@@ -910,6 +938,7 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
     int32_t* cta_t = POD_TRACE_STAMPS && p.trace && p.role_log ? p.role_log + p.trace + 768 * 8 + 2 * blockIdx.x
                                                                : nullptr;
     if (cta_t && tid == 0) cta_t[0] = static_cast<int32_t>(ptx::globaltimer() & 0x7fffffff);
+    if (tid == 0) trace_stamp(p, 0, 767, 0);  // debug trace: CTA entry (clock64, row 767)
     const uint32_t sbase = ptx::smem_u32(smem);
     volatile int32_t* misc = reinterpret_cast<volatile int32_t*>(smem + kOffMisc);  // [0] tmem, [2..3] pf, [4..5] dec
     if (tid == 0) {
@@ -959,7 +988,13 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
             prev_slot = misc[3];
             if (id < 0) break;
             if (p.pf_tn64)
+            {
+                const int fi = ps.n[0] == 0 ? 0 : 1;  // debug trace: the CTA's first item
+                if (tid == 0) trace_stamp(p, fi, 767, 1);
                 prefill_item_sm64<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);
+                if (lane == 0 && (warp == 0 || warp == kProdWarp || warp == kMmaWarp))
+                    trace_stamp(p, fi, 767, warp == 0 ? 2 : warp == kProdWarp ? 3 : 4);  // role done
+            }
             else
                 prefill_item_sm<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);
         }

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--mode", default="prefill")
     ap.add_argument("--precision", type=int, default=2)
     ap.add_argument("--keys", type=int, default=64)
+    ap.add_argument("--raw", action="store_true", help="print the first tiles' raw stamps")
     ap.add_argument("--chunk", type=int, default=0, help="override the config's chunk (32 rows x G=4 = one M-block)")
     a = ap.parse_args()
     assert os.environ.get("POD_TRACE"), "set POD_TRACE=1 with a POD_TRACE_STAMPS build (POD_LIB)"
@@ -58,8 +59,21 @@ def main():
     nt = int((A[:, 1] != 0).sum())
     print(f"{a.config} chunk {chunk} {a.mode} precision {a.precision} keys {a.keys}: "
           f"{nt} tiles traced")
-    if nt < 40:
-        return
+    if nt < 40 or a.raw:
+        # raw timeline of the first tiles, cycles from block A's first S wait:
+        # A: k0 wait S, k1 S ready, k2 w0 arrive P, k4 MMA saw P_A, k5 MMA issued; B: same; producer K / V issue
+        base = int(A[0, 0])
+        rel = lambda x: ((int(x) - base) & 0xffffffff) if int(x) else None  # noqa: E731
+        for t in sorted(set(range(min(nt, 4))) | set(range(max(nt - 3, 0), nt))):
+            print(f"  t{t}: A {[rel(A[t, k]) for k in (0, 1, 2, 4, 5)]} B {[rel(B[t, k]) for k in (0, 1, 2, 4, 5)]} "
+                  f"prod K/V {[rel(B[t, 6]), rel(B[t, 7])]}")
+        F = tr[766]
+        print(f"  epilogue w0: before PV wait {rel(F[0])}, PV done {rel(F[1])}, chunk lds {[rel(F[k]) for k in range(2, 6)]}")
+        E = tr[767]
+        print(f"  CTA entry {rel(E[0])}, item claimed {rel(E[1])}, softmax w0 done {rel(E[2])}, "
+              f"producer done {rel(E[3])}, MMA done {rel(E[4])}")
+        if nt < 40:
+            return
     rng = range(16, nt - 16)
 
     def med(xs):
