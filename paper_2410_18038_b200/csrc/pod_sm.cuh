@@ -236,6 +236,7 @@ __device__ __forceinline__ void store_o_rows(uint32_t o_addr, float inv, const O
         }
         __syncwarp();
     }
+    ptx::fence_proxy_async_smem();  // the next item's TMA loads (async proxy) reuse the tile's bytes
 }
 
 // One prefill item of the warp-specialised engine: up to two 128-row M-blocks of
@@ -578,6 +579,11 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         {  // the last PV's commit covers every earlier MMA of this thread
             const int nl = s0.n[X] + nt - 1;
             ptx::mbar_wait(bar(kBarPV + 2 * X + (nl & 1)), POD_SM_LAZY_PV ? s0.npv[X][nl & 1] & 1 : (nl >> 1) & 1);
+            // the other S buffer's PV barrier completed its phase for tile nt-2 (implied by the
+            // wait above, in-order pipe); observing it keeps every phase waited before the
+            // next item commits to the barrier again (compute-sanitizer synccheck)
+            if (POD_SM_LAZY_PV && nt >= 2)
+                ptx::mbar_wait(bar(kBarPV + 2 * X + ((nl - 1) & 1)), s0.npv[X][(nl - 1) & 1] & 1);
         }
         ptx::tc_fence_after();
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;

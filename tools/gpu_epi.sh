@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-for i in 1 2 3 4; do bash tools/exp.sh c1 2:0; done
-POD_LIB=tools/micro/libpod_trace.so POD_TRACE=1 timeout 300 python tools/trace64.py --config c1 --mode prefill --keys 64 --raw | head -4
-timeout 300 python tools/graph_vs_eager.py --config c1 --mode fused
+CS=/usr/local/cuda/bin/compute-sanitizer
+timeout 900 $CS --tool synccheck --print-limit 20 python tools/sanitize.py > gpurun_out/sanitize_synccheck.log 2>&1; echo "synccheck rc=$?" >> gpurun_out/sanitize_synccheck.log; tail -3 gpurun_out/sanitize_synccheck.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -x -q 2>&1 | tail -2

@@ -4,7 +4,8 @@
     compute-sanitizer --tool synccheck python tools/sanitize.py
     compute-sanitizer --tool racecheck python tools/sanitize.py
 
-Covers the warp-specialised kernel (both pair-engine tile widths), the two-CTA
+Covers the warp-specialised kernel (both pair-engine tile widths, also on a 3-CTA grid
+where every CTA runs several prefill items back to back), the two-CTA
 kernel, the decode split merge, the prefill split merge, serial mode, and the
 KV append.  Outputs are checked loosely (finite) -- parity is the test suite's job;
 this script only drives the kernels under the sanitizer.
@@ -24,9 +25,14 @@ from paper_2410_18038_b200.hybrid import PodAttention  # noqa: E402
 from paper_2410_18038_b200.workload import build_workload, make_batch  # noqa: E402
 
 
-def run(batch, opts, modes=("fused",)):
+def run(batch, opts, modes=("fused",), nsm=0):
+    import dataclasses
+
     wl = build_workload(batch, device="cuda")
-    op = PodAttention(batch, options=opts)
+    gpu = pkg.GpuSpec.from_device(0)
+    if nsm:  # a small grid: every CTA runs several items back to back (ring / epilogue-tile reuse)
+        gpu = dataclasses.replace(gpu, num_sms=nsm)
+    op = PodAttention(batch, gpu=gpu, options=opts)
     for mode in modes:
         out = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices, mode=mode)
         torch.cuda.synchronize()
@@ -49,6 +55,9 @@ def main():
     ]
     for batch, opts, modes in cases:
         run(batch, opts, modes)
+    many = make_batch(shape, chunk=256, offset=200, decode_ctx=[300, 64, 5])
+    for keys in (32, 64):
+        run(many, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=keys), ("fused",), nsm=3)
     # the o_proj consumer: store and reduce-scatter epilogues (virtual ranks)
     from paper_2410_18038_b200.tp import oproj
     o = (torch.rand(200, 512, device="cuda") - 0.5).to(torch.bfloat16)
