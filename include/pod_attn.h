@@ -46,7 +46,8 @@ typedef enum pod_status {
 typedef struct pod_shape {
     int32_t num_q_heads;
     int32_t num_kv_heads;
-    int32_t head_dim;
+    int32_t head_dim;     /* kernels: 8..128 in steps of 8 (below 128 run zero-padded); others plan
+                             fine but pod_attn_run* report POD_ERR_UNSUPPORTED */
     double scale;
 } pod_shape;
 

@@ -120,6 +120,7 @@ struct RunParams {
     int32_t prefill_ratio;
     int32_t decode_ratio;
     int32_t hq;
+    int32_t hd;  // head dim of the tensors (8..128, multiple of 8); the kernels compute at 128, zero-padded
     int32_t hkv;
     int32_t group;
     int32_t chunk;
@@ -617,16 +618,16 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
             ORow orow;
             float* lrow;
             if (job.n_splits == 1) {
-                orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim, p.out_fmt);
+                orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * p.hd, p.out_fmt);
                 lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
             } else {
                 const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
-                orow = out_row(p.ppart_o, row * kHeadDim, 0);
+                orow = out_row(p.ppart_o, row * p.hd, 0);
                 lrow = p.ppart_lse + row;
             }
             if (br.nt == 0) {
                 if (row_ok) {
-                    for (int c = 0; c < kHeadDim; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
+                    for (int c = 0; c < p.hd; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
                     *lrow = -INFINITY;
                 }
                 continue;
@@ -721,8 +722,9 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                 if (row_ok) {
 #pragma unroll
                     for (int c = 0; c < 32; c += 4)
-                        store4(orow, ch * 32 + c,
-                               make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
+                        if (ch * 32 + c < p.hd)
+                            store4(orow, ch * 32 + c,
+                                   make_float4(o[c] * inv, o[c + 1] * inv, o[c + 2] * inv, o[c + 3] * inv));
                 }
             }
             if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
@@ -842,11 +844,12 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
     uint32_t qb[8][2];
     {
         const elem_t* q = static_cast<const elem_t*>(p.q_decode) +
-                          (static_cast<size_t>(job.request) * p.hq + h * G + gq) * kHeadDim;
+                          (static_cast<size_t>(job.request) * p.hq + h * G + gq) * p.hd;
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-            qb[ks][0] = gq < G ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 2 * tq) : 0u;
-            qb[ks][1] = gq < G ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 8 + 2 * tq) : 0u;
+        for (int ks = 0; ks < 8; ++ks) {  // d past hd: zero (the K pages read zeros there too)
+            qb[ks][0] = gq < G && 16 * ks + 2 * tq < p.hd ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 2 * tq) : 0u;
+            qb[ks][1] = gq < G && 16 * ks + 8 + 2 * tq < p.hd ? *reinterpret_cast<const uint32_t*>(q + 16 * ks + 8 + 2 * tq)
+                                                               : 0u;
         }
     }
     float m0 = -INFINITY, m1 = -INFINITY;  // running max of heads 2t, 2t+1 (log2 domain)
@@ -1037,8 +1040,8 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
         }
     }
     ptx::named_bar_sync(bar_id, kW * 32);
-    for (int idx = tid; idx < G * kHeadDim; idx += kW * 32) {
-        const int g = idx / kHeadDim, d = idx % kHeadDim;
+    for (int idx = tid; idx < G * p.hd; idx += kW * 32) {  // the tensor's d columns (hd <= 128)
+        const int g = idx / p.hd, d = idx % p.hd;
         float mw[kW], M = -INFINITY;
 #pragma unroll
         for (int w = 0; w < kW; ++w) {
@@ -1057,12 +1060,12 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
         const float out = acc / L;
         const float lse = (M + ptx::lg2(L)) * kLn2;
         if (job.n_splits == 1) {
-            store1(out_row(p.o_decode, (static_cast<size_t>(job.request) * p.hq + qhead) * kHeadDim, p.out_fmt), d,
+            store1(out_row(p.o_decode, (static_cast<size_t>(job.request) * p.hq + qhead) * p.hd, p.out_fmt), d,
                    out);
             if (d == 0) p.lse_decode[static_cast<size_t>(job.request) * p.hq + qhead] = lse;
         } else {
             const size_t row = (static_cast<size_t>(job.request) * p.decode_splits + job.split) * p.hq + qhead;
-            p.dpart_o[row * kHeadDim + d] = out;
+            p.dpart_o[row * p.hd + d] = out;
             if (d == 0) p.dpart_lse[row] = lse;
         }
     }
@@ -1078,12 +1081,14 @@ __device__ void decode_item(const RunParams& p, const CUtensorMap* tk, const CUt
 // order.  Partials are read through L2 (ld.global.cg): they were written by other
 // SMs during this launch (in-kernel merge) or the previous one.
 __device__ __forceinline__ void merge_row(const float* po, const float* pl, size_t stride_o, size_t stride_l, int n,
-                                          const ORow& out_o, float* out_l, int lane) {
+                                          const ORow& out_o, float* out_l, int lane, int hd) {
     float M = -INFINITY;
     for (int i = 0; i < n; ++i) M = fmaxf(M, __ldcg(pl + i * stride_l));
     float tot = 0.f;
     for (int i = 0; i < n; ++i) tot += ptx::ex2((__ldcg(pl + i * stride_l) - M) * kLog2e);
     const float lse_tot = M + ptx::lg2(tot) * kLn2;
+    if (lane == 0) *out_l = lse_tot;
+    if (lane * 4 >= hd) return;  // columns past the head dim
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int i = 0; i < n; ++i) {
         const float w = ptx::ex2((__ldcg(pl + i * stride_l) - lse_tot) * kLog2e);
@@ -1094,7 +1099,6 @@ __device__ __forceinline__ void merge_row(const float* po, const float* pl, size
         acc.w += w * v.w;
     }
     store4(out_o, lane * 4, acc);
-    if (lane == 0) *out_l = lse_tot;
 }
 
 
@@ -1128,24 +1132,24 @@ __global__ void __launch_bounds__(256) merge_kernel(RunParams p, const int32_t* 
         n = tile_splits[r / tile_q];
         if (n <= 1) return;
         const size_t row = static_cast<size_t>(r) * p.hq + qh;
-        po = p.ppart_o + row * kHeadDim;
+        po = p.ppart_o + row * p.hd;
         pl = p.ppart_lse + row;
         stride_l = static_cast<size_t>(p.chunk) * p.hq;
-        stride_o = stride_l * kHeadDim;
-        out_o = out_row(p.o_prefill, row * kHeadDim, p.out_fmt);
+        stride_o = stride_l * p.hd;
+        out_o = out_row(p.o_prefill, row * p.hd, p.out_fmt);
         out_l = p.lse_prefill + row;
     } else {
         n = p.dec_nsplit[r];  // this request's own split count (min(splits, ctx), whole waves)
         if (n <= 1) return;
         const size_t row = static_cast<size_t>(r) * p.decode_splits * p.hq + qh;
-        po = p.dpart_o + row * kHeadDim;
+        po = p.dpart_o + row * p.hd;
         pl = p.dpart_lse + row;
         stride_l = p.hq;
-        stride_o = stride_l * kHeadDim;
-        out_o = out_row(p.o_decode, (static_cast<size_t>(r) * p.hq + qh) * kHeadDim, p.out_fmt);
+        stride_o = stride_l * p.hd;
+        out_o = out_row(p.o_decode, (static_cast<size_t>(r) * p.hq + qh) * p.hd, p.out_fmt);
         out_l = p.lse_decode + static_cast<size_t>(r) * p.hq + qh;
     }
-    merge_row(po, pl, stride_o, stride_l, n, out_o, out_l, lane);
+    merge_row(po, pl, stride_o, stride_l, n, out_o, out_l, lane, p.hd);
 }
 
 // ============================================================ kernels ===
@@ -1303,21 +1307,22 @@ __global__ void __launch_bounds__(256) l2_flush_kernel(uint4* __restrict__ buf, 
 }
 
 __global__ void gather_probe_kernel(const uint16_t* pool, int layout, int hkv, const int32_t* indptr,
-                                    const int32_t* indices, int req, int ctx, uint16_t* out) {
-    const size_t n = static_cast<size_t>(ctx) * hkv * (kHeadDim / 8);
+                                    const int32_t* indices, int req, int ctx, int hd, uint16_t* out) {
+    const int nc = hd / 8;  // 16-byte chunks per row
+    const size_t n = static_cast<size_t>(ctx) * hkv * nc;
     for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int chunk = static_cast<int>(i % (kHeadDim / 8));
-        const int h = static_cast<int>((i / (kHeadDim / 8)) % hkv);
-        const int t = static_cast<int>(i / (kHeadDim / 8) / hkv);
+        const int chunk = static_cast<int>(i % nc);
+        const int h = static_cast<int>((i / nc) % hkv);
+        const int t = static_cast<int>(i / nc / hkv);
         const int phys = indices[indptr[req] + t / 16];
         const int slot = t % 16;
         size_t src;
         if (layout == POD_KV_HND)
-            src = ((static_cast<size_t>(phys) * hkv + h) * 16 + slot) * kHeadDim;
+            src = ((static_cast<size_t>(phys) * hkv + h) * 16 + slot) * hd;
         else
-            src = ((static_cast<size_t>(phys) * 16 + slot) * hkv + h) * kHeadDim;
+            src = ((static_cast<size_t>(phys) * 16 + slot) * hkv + h) * hd;
         const uint4 v = *reinterpret_cast<const uint4*>(pool + src + chunk * 8);
-        *reinterpret_cast<uint4*>(out + (static_cast<size_t>(t) * hkv + h) * kHeadDim + chunk * 8) = v;
+        *reinterpret_cast<uint4*>(out + (static_cast<size_t>(t) * hkv + h) * hd + chunk * 8) = v;
     }
 }
 
@@ -1329,7 +1334,7 @@ __global__ void __launch_bounds__(256) append_kv_kernel(const uint4* __restrict_
                                                         const uint4* __restrict__ kd, const uint4* __restrict__ vd,
                                                         uint4* k_pool, uint4* v_pool, const int32_t* indptr,
                                                         const int32_t* indices, const int32_t* dec_pos, int chunk,
-                                                        int offset, int ndec, int hkv, int layout) {
+                                                        int offset, int ndec, int hkv, int layout, int kVecs) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int rows = (chunk + ndec) * hkv;
     if (warp >= rows) return;
@@ -1339,11 +1344,12 @@ __global__ void __launch_bounds__(256) append_kv_kernel(const uint4* __restrict_
     const int pos = is_pf ? offset + tok : __ldg(dec_pos + (tok - chunk));
     const int phys = __ldg(indices + __ldg(indptr + req) + pos / 16);
     const int slot = pos % 16;
-    constexpr int kVecs = kHeadDim * 2 / 16;  // 16 x uint4 per row
+    // kVecs: 16-byte vectors per row (16 at d = 128)
     const size_t src = (static_cast<size_t>(is_pf ? tok : tok - chunk) * hkv + h) * kVecs;
     const size_t dst = (layout == POD_KV_HND ? ((static_cast<size_t>(phys) * hkv + h) * 16 + slot)
                                              : ((static_cast<size_t>(phys) * 16 + slot) * hkv + h)) * kVecs;
     const int c = lane & 15;
+    if (c >= kVecs) return;
     const uint4* in = lane < 16 ? (is_pf ? kp : kd) : (is_pf ? vp : vd);
     uint4* out = lane < 16 ? k_pool : v_pool;
     out[dst + c] = __ldg(in + src + c);
@@ -1393,18 +1399,19 @@ pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_
                                                                        : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     const int hkv = plan->shape.num_kv_heads, hq = plan->shape.num_q_heads;
     const int G = hq / hkv;
+    const cuuint64_t hd = static_cast<cuuint64_t>(plan->shape.head_dim);  // boxes past hd read zeros
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     {
         cuuint64_t dims[4], strides[3];
         cuuint32_t box[4];
         if (plan->batch.kv_layout == POD_KV_HND) {
-            dims[0] = kHeadDim; dims[1] = 16; dims[2] = hkv; dims[3] = num_pages;
-            strides[0] = kHeadDim * 2; strides[1] = 16ull * kHeadDim * 2; strides[2] = 16ull * hkv * kHeadDim * 2;
+            dims[0] = hd; dims[1] = 16; dims[2] = hkv; dims[3] = num_pages;
+            strides[0] = hd * 2; strides[1] = 16ull * hd * 2; strides[2] = 16ull * hkv * hd * 2;
             box[0] = 64; box[1] = 16; box[2] = 1; box[3] = 1;
         } else {
-            dims[0] = kHeadDim; dims[1] = hkv; dims[2] = 16; dims[3] = num_pages;
-            strides[0] = kHeadDim * 2; strides[1] = static_cast<cuuint64_t>(hkv) * kHeadDim * 2;
-            strides[2] = 16ull * hkv * kHeadDim * 2;
+            dims[0] = hd; dims[1] = hkv; dims[2] = 16; dims[3] = num_pages;
+            strides[0] = hd * 2; strides[1] = static_cast<cuuint64_t>(hkv) * hd * 2;
+            strides[2] = 16ull * hkv * hd * 2;
             box[0] = 64; box[1] = 1; box[2] = 16; box[3] = 1;
         }
         for (int which = 0; which < 2; ++which) {
@@ -1421,12 +1428,12 @@ pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_
             // image as two SW128 boxes (TMA issue rate, not bytes, bounds small boxes).
             cuuint64_t d5[5], s5[4];
             const cuuint32_t box5[5] = {64, 16, 2, 1, 1}, estr5[5] = {1, 1, 1, 1, 1};
-            d5[0] = 64; d5[1] = 16; d5[2] = 2; d5[3] = hkv; d5[4] = num_pages;
+            d5[0] = hd < 64 ? hd : 64; d5[1] = 16; d5[2] = (hd + 63) / 64; d5[3] = hkv; d5[4] = num_pages;
             if (plan->batch.kv_layout == POD_KV_HND) {
-                s5[0] = kHeadDim * 2; s5[1] = 128; s5[2] = 16ull * kHeadDim * 2; s5[3] = 16ull * hkv * kHeadDim * 2;
+                s5[0] = hd * 2; s5[1] = 128; s5[2] = 16ull * hd * 2; s5[3] = 16ull * hkv * hd * 2;
             } else {
-                s5[0] = static_cast<cuuint64_t>(hkv) * kHeadDim * 2; s5[1] = 128; s5[2] = kHeadDim * 2;
-                s5[3] = 16ull * hkv * kHeadDim * 2;
+                s5[0] = static_cast<cuuint64_t>(hkv) * hd * 2; s5[1] = 128; s5[2] = hd * 2;
+                s5[3] = 16ull * hkv * hd * 2;
             }
             r = enc(which == 0 ? &m->dk : &m->dv, dt, 5, const_cast<void*>(which == 0 ? k_pool : v_pool), d5, s5,
                     box5, estr5, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1438,9 +1445,8 @@ pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_
         }
     }
     if (plan->batch.has_prefill) {
-        cuuint64_t dims[3] = {kHeadDim, static_cast<cuuint64_t>(hq),
-                              static_cast<cuuint64_t>(plan->batch.prefill.chunk_size)};
-        cuuint64_t strides[2] = {kHeadDim * 2, static_cast<cuuint64_t>(hq) * kHeadDim * 2};
+        cuuint64_t dims[3] = {hd, static_cast<cuuint64_t>(hq), static_cast<cuuint64_t>(plan->batch.prefill.chunk_size)};
+        cuuint64_t strides[2] = {hd * 2, static_cast<cuuint64_t>(hq) * hd * 2};
         cuuint32_t box[3] = {64, static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(kMBlock / G)};
         CUresult r = enc(&m->q, dt, 3, const_cast<void*>(q_prefill), dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1481,6 +1487,7 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.prefill_ratio = static_cast<int32_t>(plan->prefill_ratio);
     p.decode_ratio = static_cast<int32_t>(plan->decode_ratio);
     p.hq = plan->shape.num_q_heads;
+    p.hd = plan->shape.head_dim;
     p.hkv = plan->shape.num_kv_heads;
     p.group = p.hq / p.hkv;
     p.chunk = plan->batch.has_prefill ? static_cast<int32_t>(plan->batch.prefill.chunk_size) : 0;
@@ -1508,9 +1515,14 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     return p;
 }
 
+// head dims below 128 run through the d = 128 kernels zero-padded: TMA boxes past the
+// tensor's d are zero-filled (K, V, and the two-CTA kernel's Q), Q rows loaded by threads
+// are zero past d, and only d columns of O are stored.  16-byte TMA strides need d % 8 == 0.
+bool head_dim_ok(int d) { return d >= 8 && d <= kHeadDim && d % 8 == 0; }
+
 pod_status check_supported(const pod_plan* plan) {
-    if (plan->shape.head_dim != kHeadDim) {
-        set_last_error("only head_dim 128 is compiled for sm_100a");
+    if (!head_dim_ok(plan->shape.head_dim)) {
+        set_last_error("head_dim must be a multiple of 8 in [8, 128]");
         return POD_ERR_UNSUPPORTED;
     }
     const int G = plan->shape.num_q_heads / plan->shape.num_kv_heads;
@@ -1772,10 +1784,10 @@ pod_status pod_attn_gather_probe(const pod_plan* plan, const void* kv_pool, int6
                                  int64_t ctx, uint16_t* out, void* stream) {
     (void)num_pages;
     if (!plan || !kv_pool || !page_indptr || !page_indices || !out || ctx < 1) return POD_ERR_INVALID_ARGUMENT;
-    if (plan->shape.head_dim != kHeadDim || plan->batch.page_size != 16) return POD_ERR_UNSUPPORTED;
+    if (!head_dim_ok(plan->shape.head_dim) || plan->batch.page_size != 16) return POD_ERR_UNSUPPORTED;
     gather_probe_kernel<<<148, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint16_t*>(kv_pool), plan->batch.kv_layout, plan->shape.num_kv_heads, page_indptr,
-        page_indices, req, static_cast<int>(ctx), out);
+        page_indices, req, static_cast<int>(ctx), plan->shape.head_dim, out);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "gather_probe");
     return POD_OK;
@@ -1787,8 +1799,8 @@ pod_status pod_attn_append_kv(const pod_plan* plan, const void* k_new_prefill, c
                               void* workspace, void* stream) {
     (void)num_pages;
     if (!plan || !k_pool || !v_pool || !page_indptr || !page_indices || !workspace) return POD_ERR_INVALID_ARGUMENT;
-    if (plan->shape.head_dim != kHeadDim || plan->batch.page_size != 16) {
-        set_last_error("append_kv: only head_dim 128 / page_size 16 are compiled");
+    if (!head_dim_ok(plan->shape.head_dim) || plan->batch.page_size != 16) {
+        set_last_error("append_kv: head_dim must be a multiple of 8 in [8, 128], page_size 16");
         return POD_ERR_UNSUPPORTED;
     }
     const int chunk = plan->batch.has_prefill ? static_cast<int>(plan->batch.prefill.chunk_size) : 0;
@@ -1804,7 +1816,8 @@ pod_status pod_attn_append_kv(const pod_plan* plan, const void* k_new_prefill, c
         static_cast<const uint4*>(k_new_prefill), static_cast<const uint4*>(v_new_prefill),
         static_cast<const uint4*>(k_new_decode), static_cast<const uint4*>(v_new_decode), static_cast<uint4*>(k_pool),
         static_cast<uint4*>(v_pool), page_indptr, page_indices, dec_pos, chunk,
-        chunk > 0 ? static_cast<int>(plan->batch.prefill.position_offset) : 0, ndec, hkv, plan->batch.kv_layout);
+        chunk > 0 ? static_cast<int>(plan->batch.prefill.position_offset) : 0, ndec, hkv, plan->batch.kv_layout,
+        plan->shape.head_dim / 8);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "append_kv launch");
     return POD_OK;

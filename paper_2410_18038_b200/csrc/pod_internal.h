@@ -12,7 +12,7 @@
 namespace pod {
 
 // Fixed by the sm_100a kernels.
-constexpr int kHeadDim = 128;       // only d = 128 is compiled (all BASELINE configs)
+constexpr int kHeadDim = 128;       // the compiled head dim (all BASELINE configs); d < 128 runs zero-padded
 constexpr int kMBlock = 128;        // tcgen05 M: packed (row, q-head) rows per prefill block
 constexpr int kKvTile = 64;         // prefill keys per tcgen05 N tile (4 pages of 16)
 constexpr int kDecodeWarps = 4;     // virtual decode CTAs per physical CTA

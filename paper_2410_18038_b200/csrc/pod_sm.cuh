@@ -201,7 +201,7 @@ __device__ __forceinline__ void load_tile32(const RunParams& p, const CUtensorMa
 // segments, 4 rows per store instruction.  `tile` is in the K ring, idle once the item's
 // last PV of this block completed (every QK of the item was issued before it).
 __device__ __forceinline__ void store_o_rows(uint32_t o_addr, float inv, const ORow& orow, bool row_ok,
-                                             uint32_t tile, int lane) {
+                                             uint32_t tile, int lane, int hd) {
     // destination of the 8 rows this lane writes: rows 4i + lane / 8
     char* dst[8];
     bool ok[8];
@@ -232,7 +232,7 @@ __device__ __forceinline__ void store_o_rows(uint32_t o_addr, float inv, const O
             const uint32_t a = tile + r * 128u + ((static_cast<uint32_t>(c4) ^ (r & 7)) << 4);
             float4 v;
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-            if (ok[i]) store4(ORow{dst[i], orow.fmt}, ch * 32 + 4 * c4, v);
+            if (ok[i] && ch * 32 + 4 * c4 < hd) store4(ORow{dst[i], orow.fmt}, ch * 32 + 4 * c4, v);
         }
         __syncwarp();
     }
@@ -459,16 +459,16 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         ORow orow;
         float* lrow;
         if (job.n_splits == 1) {
-            orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim, p.out_fmt);
+            orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * p.hd, p.out_fmt);
             lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
         } else {
             const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
-            orow = out_row(p.ppart_o, row * kHeadDim, 0);
+            orow = out_row(p.ppart_o, row * p.hd, 0);
             lrow = p.ppart_lse + row;
         }
         if (nt == 0) {
             if (row_ok) {
-                for (int c = 0; c < kHeadDim; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
+                for (int c = 0; c < p.hd; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
                 *lrow = -INFINITY;
             }
             return;
@@ -476,14 +476,15 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         // ---- Q row -> TMEM (A operand of QK^T); rows past the chunk are zero
         {
             const uint32_t* src = reinterpret_cast<const uint32_t*>(static_cast<const uint16_t*>(p.q_prefill) +
-                                                                    (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim);
+                                                                    (static_cast<size_t>(my_r) * p.hq + qhead) * p.hd);
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
                 float qv[32];
 #pragma unroll
-                for (int c = 0; c < 32; c += 4) {
-                    const uint4 v = row_ok ? __ldg(reinterpret_cast<const uint4*>(src + 32 * hf + c))
-                                           : make_uint4(0u, 0u, 0u, 0u);
+                for (int c = 0; c < 32; c += 4) {  // (32 hf + c) pairs = d 64 hf + 2c; zero past the head dim
+                    const uint4 v = row_ok && 64 * hf + 2 * c < p.hd
+                                        ? __ldg(reinterpret_cast<const uint4*>(src + 32 * hf + c))
+                                        : make_uint4(0u, 0u, 0u, 0u);
                     qv[c] = __uint_as_float(v.x);
                     qv[c + 1] = __uint_as_float(v.y);
                     qv[c + 2] = __uint_as_float(v.z);
@@ -587,7 +588,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
         }
         ptx::tc_fence_after();
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        store_o_rows(o_addr, inv, orow, row_ok, sbase + kOffKs + static_cast<uint32_t>(warp) * 4096u, lane);
+        store_o_rows(o_addr, inv, orow, row_ok, sbase + kOffKs + static_cast<uint32_t>(warp) * 4096u, lane, p.hd);
         if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
         ptx::tc_fence_before();
     }
@@ -788,30 +789,31 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
         ORow orow;
         float* lrow;
         if (job.n_splits == 1) {
-            orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim, p.out_fmt);
+            orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * p.hd, p.out_fmt);
             lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
         } else {
             const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
-            orow = out_row(p.ppart_o, row * kHeadDim, 0);
+            orow = out_row(p.ppart_o, row * p.hd, 0);
             lrow = p.ppart_lse + row;
         }
         if (nt == 0) {
             if (row_ok) {
-                for (int c = 0; c < kHeadDim; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
+                for (int c = 0; c < p.hd; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
                 *lrow = -INFINITY;
             }
             return;
         }
         {  // Q row -> TMEM (A operand of QK^T); rows past the chunk are zero
             const uint32_t* src = reinterpret_cast<const uint32_t*>(static_cast<const uint16_t*>(p.q_prefill) +
-                                                                    (static_cast<size_t>(my_r) * p.hq + qhead) * kHeadDim);
+                                                                    (static_cast<size_t>(my_r) * p.hq + qhead) * p.hd);
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
                 float qv[32];
 #pragma unroll
-                for (int c = 0; c < 32; c += 4) {
-                    const uint4 v = row_ok ? __ldg(reinterpret_cast<const uint4*>(src + 32 * hf + c))
-                                           : make_uint4(0u, 0u, 0u, 0u);
+                for (int c = 0; c < 32; c += 4) {  // (32 hf + c) pairs = d 64 hf + 2c; zero past the head dim
+                    const uint4 v = row_ok && 64 * hf + 2 * c < p.hd
+                                        ? __ldg(reinterpret_cast<const uint4*>(src + 32 * hf + c))
+                                        : make_uint4(0u, 0u, 0u, 0u);
                     qv[c] = __uint_as_float(v.x);
                     qv[c + 1] = __uint_as_float(v.y);
                     qv[c + 2] = __uint_as_float(v.z);
@@ -894,7 +896,7 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
         if (lane == 0 && warp == 0) trace_stamp(p, first, 766, 1);
         ptx::tc_fence_after();
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        store_o_rows(o_addr, inv, orow, row_ok, sbase + kOffKs + static_cast<uint32_t>(warp) * 4096u, lane);
+        store_o_rows(o_addr, inv, orow, row_ok, sbase + kOffKs + static_cast<uint32_t>(warp) * 4096u, lane, p.hd);
         if (lane == 0 && warp == 0) trace_stamp(p, first, 766, 2);
         if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
         ptx::tc_fence_before();

@@ -87,9 +87,12 @@ def test_error_codes_cross_the_boundary_as_statuses():
 
 
 def test_unsupported_shapes_are_reported_not_faked():
-    # head_dim 64 plans fine (host semantics) but the sm_100a kernels only cover d = 128
-    b = HybridBatchSpec(decodes=[DecodeSpec(100)], shape=ModelShape(8, 2, 64, 8.0))
-    p = Plan(b, GpuSpec.b200())
-    st = _abi.lib().pod_attn_run(p.handle, None, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16), 1, C.c_void_p(16),
-                                 C.c_void_p(16), None, None, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16), None)
-    assert st == 7  # POD_ERR_UNSUPPORTED
+    # any head_dim plans (host semantics); the sm_100a kernels run d = 8..128 in steps of 8
+    # (zero-padded to 128: 16-byte TMA row strides), so d = 4, 12 or 256 is reported, before CUDA
+    for d in (4, 12, 256):
+        b = HybridBatchSpec(decodes=[DecodeSpec(100)], shape=ModelShape(8, 2, d, 8.0))
+        p = Plan(b, GpuSpec.b200())
+        st = _abi.lib().pod_attn_run(p.handle, None, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16), 1,
+                                     C.c_void_p(16), C.c_void_p(16), None, None, C.c_void_p(16), C.c_void_p(16),
+                                     C.c_void_p(16), None)
+        assert st == 7, d  # POD_ERR_UNSUPPORTED

@@ -234,6 +234,59 @@ def test_append_then_attend_matches_oracle():
     _check(wl, out)
 
 
+# head dims of the reference's own attention tests (test_attention.cpp:214, :339 draw d from
+# {4, 8, 64}) and others below 128: the d = 128 kernels run them zero-padded (TMA boxes past
+# d read zeros, Q rows are zero past d, only d columns of O are stored)
+@pytest.mark.parametrize("d", [8, 16, 64, 96])
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_head_dims_below_128_match_oracle(d, kernel):
+    _need_gpu()
+    batch = make_batch(pkg.ModelShape(16, 4, d, math.sqrt(d)), chunk=100, offset=300, decode_ctx=[500, 33, 1])
+    for mode in ("fused", "serial"):
+        wl, _, out = _run(batch, mode, options=_kopts(kernel, decode_splits=2))
+        _check(wl, out)
+
+
+@pytest.mark.parametrize("d", [16, 64])
+def test_head_dims_below_128_append_gather_split_merge(d):
+    """d < 128 through the KV append (then attend), the gather probe (bit-exact) and the
+    prefill / decode split merges (KV splits of both roles)."""
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+    from tests.common import new_token_rows, token_slots
+
+    batch = make_batch(pkg.ModelShape(32, 8, d, math.sqrt(d)), chunk=96, offset=1600, decode_ctx=[3000, 77, 1024])
+    wl = build_workload(batch, device="cuda")
+    kp, vp, kd, vd = (torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16).cuda() for x in new_token_rows(wl))
+    for page, slot in token_slots(wl):
+        wl.k_pool[page, :, slot, :] = 0
+        wl.v_pool[page, :, slot, :] = 0
+    op = PodAttention(batch, options=pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT, split_wave_cap=8, decode_splits=3))
+    op.append_kv(kp, vp, kd, vd, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+    assert op.info.num_merge_rows_prefill > 0 and op.info.num_merge_rows_decode > 0
+    out = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+    torch.cuda.synchronize()
+    _check(wl, out)
+    pool = wl.k_pool.view(torch.int16)
+    for req, ctx in enumerate(wl.kv_lens):
+        got = op.gather_probe(pool, wl.page_indptr, wl.page_indices, req, ctx).cpu()
+        ref = O.gather_pages(pool.cpu().numpy().view(np.uint16), 0, wl.page_indptr.cpu().numpy(),
+                             wl.page_indices.cpu().numpy(), req, ctx)
+        assert np.array_equal(got.numpy().view(np.uint16), _bf16_bits(ref))
+
+
+def test_head_dim_4_is_unsupported():
+    """d = 4 (one of the reference test dims) cannot be a TMA tensor (8-byte rows; strides
+    must be multiples of 16 B): run reports unsupported instead of misreading the pool."""
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+
+    batch = make_batch(pkg.ModelShape(8, 2, 4, 2.0), chunk=16, offset=0, decode_ctx=[20])
+    wl = build_workload(batch, device="cuda")
+    with pytest.raises(pkg.Unsupported):
+        PodAttention(batch).run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+
+
 @pytest.mark.parametrize("policy", KERNELS)
 def test_causality_is_bitwise(policy):
     _need_gpu()

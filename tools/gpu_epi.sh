@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-CS=/usr/local/cuda/bin/compute-sanitizer
-timeout 900 $CS --tool synccheck --print-limit 20 python tools/sanitize.py > gpurun_out/sanitize_synccheck.log 2>&1; echo "synccheck rc=$?" >> gpurun_out/sanitize_synccheck.log; tail -3 gpurun_out/sanitize_synccheck.log
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -x -q 2>&1 | tail -2
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py tests/test_gpu_fullsize.py -x -q 2>&1 | tail -4
+for c in c2_b64 c1; do bash tools/exp.sh $c 2:0; done
