@@ -55,6 +55,9 @@ def main():
     ]
     for batch, opts, modes in cases:
         run(batch, opts, modes)
+    d64 = make_batch(pkg.ModelShape(16, 4, 64, 8.0), chunk=100, offset=300, decode_ctx=[500, 33, 1])
+    run(d64, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC), ("fused",))  # head dim 64, zero-padded
+    run(d64, pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT, decode_splits=2), ("fused",))
     many = make_batch(shape, chunk=256, offset=200, decode_ctx=[300, 64, 5])
     for keys in (32, 64):
         run(many, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=keys), ("fused",), nsm=3)
