@@ -1,0 +1,147 @@
+"""The reference's own randomized attention test instances, through the GPU kernels.
+
+test_attention.cpp draws its instances from the reference Rng (rng.hpp):
+  * "tiled prefill: oracle equivalence across random instances and tiles" (:210-227, seed
+    2024, 25 instances: d in {4, 8, 64}, 1-2 KV heads, group 1-2, chunk 1-64, offset 0-512),
+  * "split-k: random instances, splits 1..8 pairwise consistent" (:337-351, seed 4242, 20
+    instances: d in {4, 8, 64}, context 8-300, group 2).
+The same draws come from the golden-pinned Rng port (workload.Rng, bitwise equal to the
+reference's), in the reference's order (instance parameters, then Q, K, V fills through
+random_prefill_case / random_decode_case, then the tile draws).  Each instance's inputs are
+rounded to bf16 (the kernels' input type), laid into a paged pool through a random block
+table, run through every POD kernel (and, for decode, split counts 1 / 3 / 8), and compared
+with the oracle (oracle/, bitwise equal to the compiled reference) on the same bf16 inputs:
+max |O - O_ref| <= 2e-3 max |O_ref| per KV-head block, |dLSE| <= 2e-3.  d = 4 instances are
+drawn (to keep the stream aligned) but skipped: 8-byte rows cannot be TMA tensors, and
+pod_attn_run reports them unsupported (tests/test_gpu_parity.py::test_head_dim_4_is_unsupported).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2410_18038_b200 as pkg
+from oracle import pyoracle as O
+from paper_2410_18038_b200._abi import POD_POLICY_COMPLEMENT, POD_POLICY_WARPSPEC
+from paper_2410_18038_b200.workload import Rng, build_workload, make_batch
+from tests.common import LSE_TOL, O_TOL, rel_err
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = [dict(policy=POD_POLICY_COMPLEMENT), dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32),
+           dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64)]
+
+
+def _bf16(x: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(torch.bfloat16)
+
+
+def prefill_instances():
+    """(d, kv_heads, q_heads, chunk, offset, context, q, k, v) of test_attention.cpp:210-227."""
+    rng = Rng(2024)
+    out = []
+    for _ in range(25):
+        d = [4, 8, 64][rng.next_long(0, 2)]
+        kvh = rng.next_long(1, 2)
+        qh = kvh * rng.next_long(1, 2)
+        chunk = rng.next_long(1, 64)
+        off = rng.next_long(0, 512)
+        ctx = off + chunk + rng.next_long(0, 64)
+        q = rng.fill_uniform(chunk * qh * d).reshape(chunk, qh, d)   # random_prefill_case: q, k, v
+        k = rng.fill_uniform(ctx * kvh * d).reshape(ctx, kvh, d)
+        v = rng.fill_uniform(ctx * kvh * d).reshape(ctx, kvh, d)
+        rng.next_long(0, 4)  # tq
+        rng.next_long(0, 4)  # tkv
+        out.append((d, kvh, qh, chunk, off, ctx, q, k, v))
+    return out
+
+
+def decode_instances():
+    """(d, kv_heads, q_heads, context, q, k, v) of test_attention.cpp:337-351."""
+    rng = Rng(4242)
+    out = []
+    for _ in range(20):
+        d = [4, 8, 64][rng.next_long(0, 2)]
+        kv = rng.next_long(1, 2)
+        ctx = rng.next_long(8, 300)
+        q = rng.fill_uniform(2 * kv * d).reshape(2 * kv, d)           # random_decode_case: q, k, v
+        k = rng.fill_uniform(ctx * kv * d).reshape(ctx, kv, d)
+        v = rng.fill_uniform(ctx * kv * d).reshape(ctx, kv, d)
+        out.append((d, kv, 2 * kv, ctx, q, k, v))
+    return out
+
+
+def _fill_pool(wl, req: int, k: np.ndarray, v: np.ndarray):
+    """Writes request `req`'s K / V rows [n][Hkv][d] into its pages (HND pools)."""
+    n, hkv, d = k.shape
+    ps = wl.batch.page_size
+    npg = (n + ps - 1) // ps
+    a = int(wl.page_indptr[req])
+    phys = wl.page_indices[a:a + npg].long()
+    for pool, x in ((wl.k_pool, k), (wl.v_pool, v)):
+        padded = torch.zeros(npg * ps, hkv, d, dtype=torch.bfloat16)
+        padded[:n] = _bf16(x)
+        pool[phys] = padded.view(npg, ps, hkv, d).permute(0, 2, 1, 3).to(pool.device)
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+@pytest.mark.parametrize("i", range(25))
+def test_reference_prefill_instance(i):
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+
+    d, kvh, qh, chunk, off, ctx, q, k, v = prefill_instances()[i]
+    if d == 4:
+        pytest.skip("d = 4: not a TMA tensor (reported unsupported)")
+    shape = pkg.ModelShape(qh, kvh, d, math.sqrt(d))
+    batch = make_batch(shape, chunk=chunk, offset=off)
+    wl = build_workload(batch, device="cuda")
+    wl.q_prefill.copy_(_bf16(q).cuda())
+    _fill_pool(wl, 0, k[:off + chunk], v[:off + chunk])  # keys past the chunk's last row are invisible
+    # oracle on the bf16-rounded inputs
+    qr, kr, vr = (_bf16(x).double().numpy() for x in (q, k[:off + chunk], v[:off + chunk]))
+    o_ref = O.tiled_prefill(qr, kr, vr, off, qh, kvh, shape.scale, 64, 64)
+    l_ref = O.prefill_lse(qr, kr, off, qh, kvh, shape.scale)
+    G = qh // kvh
+    for opts in KERNELS:
+        out = PodAttention(batch, options=pkg.PlanOptions(**opts)).run(
+            wl.q_prefill, None, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+        torch.cuda.synchronize()
+        o, lse = out.o_prefill.double().cpu().numpy(), out.lse_prefill.double().cpu().numpy()
+        for h in range(kvh):
+            eo = rel_err(o[:, h * G:(h + 1) * G], o_ref[:, h * G:(h + 1) * G])
+            el = float(np.abs(lse[:, h * G:(h + 1) * G] - l_ref[:, h * G:(h + 1) * G]).max())
+            assert eo <= O_TOL and el <= LSE_TOL, (opts, d, chunk, off, eo, el)
+
+
+@pytest.mark.parametrize("i", range(20))
+def test_reference_decode_instance(i):
+    _need_gpu()
+    from paper_2410_18038_b200.hybrid import PodAttention
+
+    d, kv, qh, ctx, q, k, v = decode_instances()[i]
+    if d == 4:
+        pytest.skip("d = 4: not a TMA tensor (reported unsupported)")
+    shape = pkg.ModelShape(qh, kv, d, math.sqrt(d))
+    batch = make_batch(shape, decode_ctx=[ctx])
+    wl = build_workload(batch, device="cuda")
+    wl.q_decode.copy_(_bf16(q).view(1, qh, d).cuda())
+    _fill_pool(wl, 0, k, v)
+    qr, kr, vr = (_bf16(x).double().numpy() for x in (q, k, v))
+    o_ref, l_ref = O.decode_attention(qr, kr, vr, qh, kv, shape.scale)
+    G = qh // kv
+    for opts in KERNELS:
+        for splits in (1, 3, 8):  # the reference checks splits 1..8 against each other
+            out = PodAttention(batch, options=pkg.PlanOptions(decode_splits=splits, **opts)).run(
+                None, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
+            torch.cuda.synchronize()
+            o, lse = out.o_decode[0].double().cpu().numpy(), out.lse_decode[0].double().cpu().numpy()
+            for h in range(kv):
+                eo = rel_err(o[h * G:(h + 1) * G], o_ref[h * G:(h + 1) * G])
+                el = float(np.abs(lse[h * G:(h + 1) * G] - l_ref[h * G:(h + 1) * G]).max())
+                assert eo <= O_TOL and el <= LSE_TOL, (opts, splits, d, ctx, eo, el)
