@@ -10,7 +10,8 @@ reference's), in the reference's order (instance parameters, then Q, K, V fills 
 random_prefill_case / random_decode_case, then the tile draws).  Each instance's inputs are
 rounded to bf16 (the kernels' input type), laid into a paged pool through a random block
 table, run through every POD kernel (and, for decode, split counts 1 / 3 / 8), and compared
-with the oracle (oracle/, bitwise equal to the compiled reference) on the same bf16 inputs:
+with the oracle (oracle/, bitwise equal to the compiled reference) on the same bf16 inputs
+(plus the file's named fixed-seed instances with d >= 8, NAMED_PREFILL / NAMED_DECODE):
 max |O - O_ref| <= 2e-3 max |O_ref| per KV-head block, |dLSE| <= 2e-3.  d = 4 instances are
 drawn (to keep the stream aligned) but skipped: 8-byte rows cannot be TMA tensors, and
 pod_attn_run reports them unsupported (tests/test_gpu_parity.py::test_head_dim_4_is_unsupported).
@@ -90,12 +91,57 @@ def _need_gpu():
         pytest.skip("needs a CUDA device")
 
 
+# the named fixed-seed instances of test_attention.cpp with d >= 8:
+# (seed, chunk_len, context_len, offset, q_heads, kv_heads, d) for random_prefill_case and
+# (seed, context, q_heads, kv_heads, d) for random_decode_case
+NAMED_PREFILL = [(11, 1, 1, 0, 2, 1, 8),          # :192 degenerate single query
+                 (123, 64, 512, 448, 4, 2, 16),   # :198 chunk of a 512 prompt
+                 (5, 12, 48, 36, 2, 2, 8),        # :204 oversized kv tile
+                 (99, 6, 40, 20, 2, 1, 8),        # :229 causality
+                 (31, 10, 32, 16, 8, 2, 8),       # :252 GQA consistency
+                 (55, 16, 96, 64, 2, 1, 8)]       # :405 single precision path
+NAMED_DECODE = [(8, 24, 4, 2, 8),                 # :293 single split merge
+                (77, 1024, 4, 2, 16),             # :326 split counts agree
+                (21, 37, 4, 2, 8)]                # :381 merge permutation
+
+
+def named_prefill(seed, chunk, ctx, off, qh, kvh, d):
+    rng = Rng(seed)
+    q = rng.fill_uniform(chunk * qh * d).reshape(chunk, qh, d)
+    k = rng.fill_uniform(ctx * kvh * d).reshape(ctx, kvh, d)
+    v = rng.fill_uniform(ctx * kvh * d).reshape(ctx, kvh, d)
+    return d, kvh, qh, chunk, off, ctx, q, k, v
+
+
+def named_decode(seed, ctx, qh, kv, d):
+    rng = Rng(seed)
+    q = rng.fill_uniform(qh * d).reshape(qh, d)
+    k = rng.fill_uniform(ctx * kv * d).reshape(ctx, kv, d)
+    v = rng.fill_uniform(ctx * kv * d).reshape(ctx, kv, d)
+    return d, kv, qh, ctx, q, k, v
+
+
 @pytest.mark.parametrize("i", range(25))
 def test_reference_prefill_instance(i):
     _need_gpu()
+    _check_prefill_instance(*prefill_instances()[i])
+
+
+@pytest.mark.parametrize("case", NAMED_PREFILL)
+def test_reference_named_prefill_case(case):
+    _need_gpu()
+    _check_prefill_instance(*named_prefill(*case))
+
+
+@pytest.mark.parametrize("case", NAMED_DECODE)
+def test_reference_named_decode_case(case):
+    _need_gpu()
+    _check_decode_instance(*named_decode(*case))
+
+
+def _check_prefill_instance(d, kvh, qh, chunk, off, ctx, q, k, v):
     from paper_2410_18038_b200.hybrid import PodAttention
 
-    d, kvh, qh, chunk, off, ctx, q, k, v = prefill_instances()[i]
     if d == 4:
         pytest.skip("d = 4: not a TMA tensor (reported unsupported)")
     shape = pkg.ModelShape(qh, kvh, d, math.sqrt(d))
@@ -122,9 +168,12 @@ def test_reference_prefill_instance(i):
 @pytest.mark.parametrize("i", range(20))
 def test_reference_decode_instance(i):
     _need_gpu()
+    _check_decode_instance(*decode_instances()[i])
+
+
+def _check_decode_instance(d, kv, qh, ctx, q, k, v):
     from paper_2410_18038_b200.hybrid import PodAttention
 
-    d, kv, qh, ctx, q, k, v = decode_instances()[i]
     if d == 4:
         pytest.skip("d = 4: not a TMA tensor (reported unsupported)")
     shape = pkg.ModelShape(qh, kv, d, math.sqrt(d))
