@@ -134,6 +134,7 @@ struct RunParams {
     int32_t p_f16;    // POD_PRECISION_F16PV: P as fp16, V stages converted to fp16 in smem (bf16 data)
     int32_t pf_tn64;  // warp-specialised kernel: 64-key single-S pair engine (prefill-dominant plans)
     const int32_t* dec_nsplit;  // KV splits of each decode request (min(splits, ctx), pod_plan.cpp)
+    int32_t vs_pages;  // > 0: prefill V tiles from the fp16 shadow (logical pages, already converted)
     int32_t trace;         // debug builds (POD_TRACE_STAMPS): per-tile cycle stamps after the role log
     int32_t trace_mode;    // debug builds: 2 = serialise MMA issue with completion (execution latency probe)
     int64_t num_pages;
@@ -394,10 +395,11 @@ __device__ __forceinline__ void prefill_load_kv_tile(const RunParams& p, const C
 // K-steps 4 KB apart), so the page-major image serves it directly.
 template <int kPages>
 __device__ __forceinline__ void prefill_load_v_pages(const CUtensorMap* tdv, uint32_t dst, uint32_t bar, int kt,
-                                                     int kv_head, const PageIds& ids) {
-    int phys[kPages];
+                                                     int kv_head, const PageIds& ids, int vs_pages = 0) {
+    int phys[kPages];  // the fp16 shadow (vs_pages > 0) is indexed by logical page
 #pragma unroll
-    for (int pg = 0; pg < kPages; ++pg) phys[pg] = ids.get(min(kt / 16 + pg, ids.n - 1));
+    for (int pg = 0; pg < kPages; ++pg)
+        phys[pg] = vs_pages ? min(kt / 16 + pg, vs_pages - 1) : ids.get(min(kt / 16 + pg, ids.n - 1));
 #pragma unroll
     for (int pg = 0; pg < kPages; ++pg) ptx::tma_load_5d_elect(dst + pg * 4096, tdv, bar, 0, 0, 0, kv_head, phys[pg]);
 }
@@ -535,11 +537,14 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                     }
                     if (t > 0) {  // V of tile t-1
                         const int gg = g + t - 1, st = gg & 1;
+                        // the fp16 V shadow is written by the kernel launched just before this
+                        // one (programmatic dependent launch): wait for it at the first V load
+                        if (p.vs_pages && t == 1) ptx::griddep_wait();
                         if (gg >= 2) ptx::mbar_wait_relaxed<>(b_vempty + 8 * st, ((gg >> 1) - 1) & 1);
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t - 1, 6);
                         ptx::mbar_arrive_expect_tx_elect(b_vfull + 8 * st, kKvStageBytes);
                         prefill_load_v_pages<kKvTile / 16>(tmv, sV + st * kKvStageBytes, b_vfull + 8 * st,
-                                                           br.kt0 + (t - 1) * kKvTile, job.kv_head, pvi);
+                                                           br.kt0 + (t - 1) * kKvTile, job.kv_head, pvi, p.vs_pages);
                         trace_stamp(p, ps.items - 1 + (b > 0 ? 1 : 0), 256 + t - 1, 7);
                     }
                 }
@@ -679,7 +684,7 @@ __device__ void prefill_item(const RunParams& p, const CUtensorMap* tmq, const C
                 else
                     lsum = softmax_p_row<kFmt, 0>(s, p.sl2, neg_m, s_addr);
                 l_run += lsum;
-                if (kFmt == 1 && p.p_f16) {  // V(t) -> fp16 before P(t) is handed to the MMA issuer
+                if (kFmt == 1 && p.p_f16 && !p.vs_pages) {  // V(t) -> fp16 before P(t) goes to the MMA issuer
                     ptx::mbar_wait(b_vfull + 8 * st, (gg >> 1) & 1);
                     v_stage_to_f16<kKvStageBytes, 128>(sV + st * kKvStageBytes, tid);
                 }
@@ -1258,7 +1263,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncthreads();  // role[] is rewritten by the next claim
         if (op < 0) break;
         if (op == 0) {
-            prefill_item<kFmt>(p, &tmq, &tmk, &tdv, id, smem, tmem, ps);
+            prefill_item<kFmt>(p, &tmq, &tmk, p.vs_pages ? &tmv : &tdv, id, smem, tmem, ps);
         } else {
             if (warp < kDecWarpsK)
                 decode_item<G, kFmt, kDecWarpsK, kDecStages>(p, &tdk, &tdv, id, warp, sbase, sbase + kOffDecBar,
@@ -1355,6 +1360,34 @@ __global__ void __launch_bounds__(256) append_kv_kernel(const uint4* __restrict_
     out[dst + c] = __ldg(in + src + c);
 }
 
+// POD_PRECISION_F16PV, plans with vs_pages (pod_plan.cpp): the prefill request's V
+// converted bf16 -> fp16 once per launch into a dense shadow [logical page][Hkv][16][d]
+// (the decode role's 5-D page view with logical page ids), so the prefill CTAs stream V
+// tiles that are already the PV MMA's fp16 B operand.  HBM-bound: 2 B read + 2 B written
+// per element, grid-stride over 16-byte vectors.
+__global__ void __launch_bounds__(256) v_shadow_kernel(const uint4* __restrict__ v_pool, uint4* __restrict__ shadow,
+                                                       const int32_t* __restrict__ indptr,
+                                                       const int32_t* __restrict__ indices, int pages, int hkv,
+                                                       int vecs /* 16-byte vectors per row: d / 8 */, int layout) {
+    const size_t per_page = static_cast<size_t>(hkv) * 16 * vecs;
+    const size_t n = static_cast<size_t>(pages) * per_page;
+    ptx::griddep_launch_dependents();  // the POD kernel may launch now (its prefill waits for us)
+    const int32_t* row = indices + __ldg(indptr);  // request 0 = the prefill
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int lp = static_cast<int>(i / per_page);
+        const size_t rem = i % per_page;
+        const int h = static_cast<int>(rem / (16 * vecs));
+        const int slot = static_cast<int>((rem / vecs) % 16), c = static_cast<int>(rem % vecs);
+        const size_t phys = static_cast<size_t>(__ldg(row + lp));
+        const size_t src = (layout == POD_KV_HND ? ((phys * hkv + h) * 16 + slot) : ((phys * 16 + slot) * hkv + h)) *
+                               vecs + c;
+        const uint4 w = __ldg(v_pool + src);
+        shadow[i] = make_uint4(bf16x2_to_f16x2(w.x), bf16x2_to_f16x2(w.y), bf16x2_to_f16x2(w.z),
+                               bf16x2_to_f16x2(w.w));
+    }
+}
+
 // ================================================================ host ===
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1385,10 +1418,11 @@ int64_t sm_smem_bytes() { return sm3::kSmem; }
 struct Maps {
     CUtensorMap q, k, v;  // prefill role: SW128 boxes of 64 d x 16 tokens, Q boxes of 64 d x 128 rows
     CUtensorMap dk, dv;   // decode role: one whole head-page per box (5D view, SW128 halves)
+    CUtensorMap vs;       // the fp16 V shadow (plans with vs_pages): dv's view over logical pages
 };
 
 pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_pool, const void* v_pool,
-                     int64_t num_pages, Maps* m) {
+                     int64_t num_pages, void* workspace, Maps* m) {
     std::memset(m, 0, sizeof(*m));
     EncodeTiledFn enc = encode_fn();
     if (!enc) {
@@ -1456,6 +1490,22 @@ pod_status make_maps(const pod_plan* plan, const void* q_prefill, const void* k_
             return POD_ERR_CUDA;
         }
     }
+    if (plan->vs_pages > 0) {  // the fp16 V shadow: dense [logical page][Hkv][16][d], dv's 5-D view
+        cuuint64_t d5[5], s5[4];
+        const cuuint32_t box5[5] = {64, 16, 2, 1, 1}, estr5[5] = {1, 1, 1, 1, 1};
+        d5[0] = hd < 64 ? hd : 64; d5[1] = 16; d5[2] = (hd + 63) / 64; d5[3] = hkv; d5[4] = plan->vs_pages;
+        s5[0] = hd * 2; s5[1] = 128; s5[2] = 16ull * hd * 2; s5[3] = 16ull * hkv * hd * 2;
+        CUresult r = enc(&m->vs, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5,
+                         static_cast<uint8_t*>(workspace) + plan->ws.off_vshadow, d5, s5, box5, estr5,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_last_error("cuTensorMapEncodeTiled(v shadow) failed: " + std::to_string(static_cast<int>(r)));
+            return POD_ERR_CUDA;
+        }
+    } else {
+        m->vs = m->v;  // (unused)
+    }
     return POD_OK;
 }
 
@@ -1502,6 +1552,7 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.pf_tn64 = plan->pf_tn64 ? 1 : 0;
     p.out_fmt = plan->opts.out_dtype;
     p.dec_nsplit = reinterpret_cast<const int32_t*>(ws + plan->ws.off_dec_nsplit);
+    p.vs_pages = plan->vs_pages;
 #if POD_TRACE_STAMPS
     {  // debug builds only: POD_TRACE=1 (stamps) / 2 (serialised MMA issue) after the role log
         static const char* trace_env = std::getenv("POD_TRACE");
@@ -1573,14 +1624,54 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
     pod_status st = set_kernel_attributes<G, kFmt>();
     if (st != POD_OK) return st;
     const int nsm = plan->dev.num_sms;
+    const bool shadow = p.vs_pages > 0 && mode != 3;
+    if (shadow) {
+        const uint8_t* ws = reinterpret_cast<const uint8_t*>(p.ctr) - plan->ws.off_counters;
+        const size_t n = static_cast<size_t>(p.vs_pages) * p.hkv * 16 * (p.hd / 8);
+        v_shadow_kernel<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 8 * nsm)), 256, 0, s>>>(
+            static_cast<const uint4*>(p.v_pool), reinterpret_cast<uint4*>(const_cast<uint8_t*>(ws) + plan->ws.off_vshadow),
+            p.page_indptr, p.page_indices, p.vs_pages, p.hkv, p.hd / 8, p.kv_layout);
+    }
+    const CUtensorMap& pf_v = shadow ? maps.vs : maps.v;  // the prefill role's V map argument
+    bool pdl = shadow;  // only the launch right after v_shadow_kernel is its programmatic dependent
     auto launch = [&](const RunParams& q) {
         const int items = q.num_pctas + q.num_dctas;
         if (items <= 0) return;
+        const bool dep = pdl;
+        pdl = false;
         if (q.policy == POD_POLICY_WARPSPEC) {
-            pod_sm_kernel<G, kFmt><<<nsm, sm3::kThreads, sm3::kSmem, s>>>(q, maps.k, maps.v, maps.dk, maps.dv);
+            if (dep) {  // a programmatic dependent of v_shadow_kernel (prefill waits at its first V load)
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = dim3(nsm);
+                cfg.blockDim = dim3(sm3::kThreads);
+                cfg.dynamicSmemBytes = sm3::kSmem;
+                cfg.stream = s;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                cudaLaunchKernelEx(&cfg, pod_sm_kernel<G, kFmt>, q, maps.k, pf_v, maps.dk, maps.dv);
+            } else {
+                pod_sm_kernel<G, kFmt><<<nsm, sm3::kThreads, sm3::kSmem, s>>>(q, maps.k, pf_v, maps.dk, maps.dv);
+            }
         } else {
             const int grid = std::min(items, 2 * nsm);  // persistent: 2 resident CTAs per SM
-            pod_fused_kernel<G, kFmt><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, maps.v, maps.dk, maps.dv);
+            if (dep) {  // a programmatic dependent of v_shadow_kernel (prefill waits at its first V load)
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = dim3(grid);
+                cfg.blockDim = dim3(kThreads);
+                cfg.dynamicSmemBytes = kSmemBytes;
+                cfg.stream = s;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                cudaLaunchKernelEx(&cfg, pod_fused_kernel<G, kFmt>, q, maps.q, maps.k, pf_v, maps.dk, maps.dv);
+            } else {
+                pod_fused_kernel<G, kFmt><<<grid, kThreads, kSmemBytes, s>>>(q, maps.q, maps.k, pf_v, maps.dk, maps.dv);
+            }
         }
     };
     if (mode == 0) {
@@ -1664,15 +1755,16 @@ pod_status run_mode(const pod_plan* plan, int mode, const void* q_prefill, const
         pod_plan* mp = const_cast<pod_plan*>(plan);
         std::lock_guard<std::mutex> lock(mp->map_mu);
         if (mp->map_key[0] == q_prefill && mp->map_key[1] == k_pool && mp->map_key[2] == v_pool &&
-            mp->map_pages == num_pages) {
+            mp->map_key[3] == workspace && mp->map_pages == num_pages) {
             std::memcpy(&maps, mp->map_blob, sizeof(Maps));
         } else {
-            st = make_maps(plan, q_prefill, k_pool, v_pool, num_pages, &maps);
+            st = make_maps(plan, q_prefill, k_pool, v_pool, num_pages, workspace, &maps);
             if (st != POD_OK) return st;
             std::memcpy(mp->map_blob, &maps, sizeof(Maps));
             mp->map_key[0] = q_prefill;
             mp->map_key[1] = k_pool;
             mp->map_key[2] = v_pool;
+            mp->map_key[3] = workspace;
             mp->map_pages = num_pages;
         }
     }

@@ -67,6 +67,7 @@ struct WorkspaceLayout {
     size_t off_dpart_lse = 0;     // [num_decodes][splits][Hq]
     size_t off_dec_pos = 0;       // int32 per decode: position of its new token (context_len - 1)
     size_t off_dec_nsplit = 0;    // int32 per decode: its KV split count (the merge reads it)
+    size_t off_vshadow = 0;       // fp16 copy of the prefill request's V, [logical page][Hkv][16][d] (vs_pages)
     size_t total = 0;
 };
 
@@ -90,6 +91,7 @@ struct pod_plan {
     std::vector<int32_t> dec_nsplit;  // KV splits per decode request (min(splits, ctx))
     bool pf_tn64 = false;          // warp-specialised: 64-key pair engine (see pod_plan.cpp)
     int64_t decode_splits = 1;     // largest split count (partials' stride)
+    int32_t vs_pages = 0;          // > 0: prefill V read from an fp16 shadow of these many pages (pod_plan.cpp)
     int64_t dec_split_base = 1;    // splits of requests [0, dec_tail_start)
     int64_t dec_tail_start = 0;    // first request with decode_splits splits
     int64_t prefill_ratio = 1;
@@ -104,9 +106,9 @@ struct pod_plan {
     // the Q / K / V pointers or the pool size change: host launch cost per run.
     // Guarded by map_mu (concurrent pod_attn_run calls on one plan).
     std::mutex map_mu;
-    const void* map_key[3] = {nullptr, nullptr, nullptr};
+    const void* map_key[4] = {nullptr, nullptr, nullptr, nullptr};  // q, k, v, workspace
     int64_t map_pages = -1;
-    alignas(64) unsigned char map_blob[5 * 128];
+    alignas(64) unsigned char map_blob[6 * 128];
 };
 
 namespace pod {

@@ -417,6 +417,8 @@ void layout_workspace(pod_plan& p) {
     off = align(off + p.decode_ctx.size() * sizeof(int32_t));
     p.ws.off_dec_nsplit = off;
     off = align(off + p.decode_ctx.size() * sizeof(int32_t));
+    p.ws.off_vshadow = off;
+    off = align(off + static_cast<size_t>(p.vs_pages) * s.num_kv_heads * p.batch.page_size * s.head_dim * 2);
     p.ws.total = off;
     p.dec_pos.clear();
     for (int64_t c : p.decode_ctx) p.dec_pos.push_back(static_cast<int32_t>(c - 1));
@@ -515,6 +517,20 @@ void build(pod_plan& p) {
     lower(p);
     scheduler_ratio(p);
     p.smem_bytes = p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes() : pod::fused_smem_bytes();
+    // POD_PRECISION_F16PV on bf16 data needs V in fp16.  The two-CTA kernel's prefill CTA
+    // converting every V tile it streams sits on its softmax warps' critical path (S is
+    // double-buffered there): prefill-alone at C2 is 327 us with it, 256 us without (bf16 P,
+    // same MMA count).  Its plans convert the prefill request's V once per launch into a
+    // dense fp16 shadow in the workspace instead (pod_attn.cu, v_shadow_kernel; the POD
+    // kernel is its programmatic dependent and waits at its first V load).  The pair engines
+    // hide most of the conversion behind their single-buffered S: the shadow pays on the
+    // prefill-dominant 64-key plans (fused C2 B=8 365 -> 354 us, B=16 388 -> 370) and not
+    // on the decode-dominant 32-key ones (C2 B=64 686 -> 693: one more HBM pass).
+    p.vs_pages = 0;
+    if (p.batch.has_prefill && p.batch.dtype == POD_DTYPE_BF16 && p.opts.precision == POD_PRECISION_F16PV &&
+        (p.opts.policy == POD_POLICY_COMPLEMENT || (p.opts.policy == POD_POLICY_WARPSPEC && p.pf_tn64)))
+        p.vs_pages = static_cast<int32_t>(
+            ceil_div(p.batch.prefill.position_offset + p.batch.prefill.chunk_size, int64_t(p.batch.page_size)));
     layout_workspace(p);
 }
 

@@ -304,9 +304,10 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
                 if (POD_SM_NOLOAD && gg >= kNS) {
                     if (lane == 0) ptx::mbar_arrive(bar(kBarVF + st));
                 } else {
+                    if (p.vs_pages && t == 1) ptx::griddep_wait();  // the fp16 V shadow (see prefill_item)
                     ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
                     prefill_load_v_pages<2>(tmv, sV + st * kStage, bar(kBarVF + st), kt0 + (t - 1) * kTN, job.kv_head,
-                                            ids);
+                                            ids, p.vs_pages);
                 }
             }
         }
@@ -505,7 +506,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
             v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
         };
-        if (kFmt == 1 && p.p_f16 && X == 0) v_to_f16(0);
+        if (kFmt == 1 && p.p_f16 && !p.vs_pages && X == 0) v_to_f16(0);
         float m_run = -INFINITY, l_run = 0.f;
         for (int t = 0; t < nt; ++t) {
             const int n = s0.n[X] + t, b = n & 1;
@@ -574,7 +575,7 @@ __device__ void prefill_item_sm(const RunParams& p, const CUtensorMap* tmk, cons
             if (lane == 0 && q == 0) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 2);
             if (lane == 0 && q == 3) trace_stamp(p, first, X ? (t < 128 ? 384 + t : 9999) : (t < 256 ? t : 9999), 3);
             if (lane == 0) ptx::mbar_arrive(bar(kBarP + 2 * X + b));
-            if (kFmt == 1 && p.p_f16 && X == 0 && t + 1 < nt) v_to_f16(t + 1);  // off the P(t) -> PV(t) path
+            if (kFmt == 1 && p.p_f16 && !p.vs_pages && X == 0 && t + 1 < nt) v_to_f16(t + 1);  // off the P(t) -> PV(t) path
         }
         // ------------------------------------------------- epilogue --
         {  // the last PV's commit covers every earlier MMA of this thread
@@ -705,8 +706,9 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             sm64::load_tile64(p, tmk, sK + sk * kStage, bar(kBarKF + sk), kt0 + t * kTN, job.kv_head, ids);
             if (lane == 0) trace_stamp(p, first, rowB(t), 6);
             if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarVE + st), ((gg / kNS) - 1) & 1);
+            if (p.vs_pages && t == 0) ptx::griddep_wait();  // the fp16 V shadow (see prefill_item)
             ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
-            prefill_load_v_pages<4>(tmv, sV + st * kStage, bar(kBarVF + st), kt0 + t * kTN, job.kv_head, ids);
+            prefill_load_v_pages<4>(tmv, sV + st * kStage, bar(kBarVF + st), kt0 + t * kTN, job.kv_head, ids, p.vs_pages);
             if (lane == 0) trace_stamp(p, first, rowB(t), 7);
         }
     } else if (warp == kMmaWarp) {
@@ -832,7 +834,7 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
             v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
         };
-        if (kFmt == 1 && p.p_f16 && X == 0) v_to_f16(0);
+        if (kFmt == 1 && p.p_f16 && !p.vs_pages && X == 0) v_to_f16(0);
         float m_run = -INFINITY, l_run = 0.f;
         for (int t = 0; t < nt; ++t) {
             const int n = s0.n[X] + t;
@@ -889,7 +891,7 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
             if (lane == 0 && q == 0) trace_stamp(p, first, X ? rowB(t) : t, 2);
             if (lane == 0 && q == 3) trace_stamp(p, first, X ? rowB(t) : t, 3);
             if (lane == 0) ptx::mbar_arrive(bar(kBarP + X));
-            if (kFmt == 1 && p.p_f16 && X == 0 && t + 1 < nt) v_to_f16(t + 1);  // off the P(t) -> PV(t) path
+            if (kFmt == 1 && p.p_f16 && !p.vs_pages && X == 0 && t + 1 < nt) v_to_f16(t + 1);  // off the P(t) -> PV(t) path
         }
         if (lane == 0 && warp == 0) trace_stamp(p, first, 766, 0);
         ptx::mbar_wait(bar(kBarPV + X), s0.npv[X][0] & 1);  // the last PV (commit covers all)
@@ -999,12 +1001,12 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
             {
                 const int fi = ps.n[0] == 0 ? 0 : 1;  // debug trace: the CTA's first item
                 if (tid == 0) trace_stamp(p, fi, 767, 1);
-                prefill_item_sm64<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);
+                prefill_item_sm64<kFmt>(p, &tmk, p.vs_pages ? &tmv : &tdv, id, sbase, tmem, ps, warp, lane);
                 if (lane == 0 && (warp == 0 || warp == kProdWarp || warp == kMmaWarp))
                     trace_stamp(p, fi, 767, warp == 0 ? 2 : warp == kProdWarp ? 3 : 4);  // role done
             }
             else
-                prefill_item_sm<kFmt>(p, &tmk, &tdv, id, sbase, tmem, ps, warp, lane);
+                prefill_item_sm<kFmt>(p, &tmk, p.vs_pages ? &tmv : &tdv, id, sbase, tmem, ps, warp, lane);
         }
         ptx::tc_fence_before();
         ptx::named_bar_sync(1, kPrefillThreads);
