@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define POD_ATTN_ABI_VERSION 1
+#define POD_ATTN_ABI_VERSION 2
 
 /* Mirrors the exception classes of the reference (include/attnsim/types.hpp:12-15,
  * attention.hpp:113-116,155-163,249,304; work_decomp.hpp:33-47,151-152). */
@@ -151,6 +151,8 @@ typedef struct pod_options {
     int32_t precision;       /* POD_PRECISION_* for the prefill P operand            */
     int32_t out_dtype;       /* POD_OUT_*: element type of o_prefill / o_decode (LSE stays fp32) */
     int32_t prefill_tile_keys; /* warp-specialised pair engine: 0 = by decode share, 32 or 64 forces */
+    int32_t prefill_s_buffers; /* 64-key pair engine: 0 = by decode share, 1 = one S buffer per block (Q in
+                                  TMEM), 2 = two S buffers per block (Q in smem, 2-stage decode rings) */
 } pod_options;
 
 enum {
@@ -186,6 +188,7 @@ typedef struct pod_plan_info {
     int32_t num_merge_rows_decode;
     int32_t policy;             /* the POD_POLICY_* the plan runs (POD_POLICY_AUTO resolved) */
     int32_t prefill_tile_keys;  /* keys per prefill K/V tile of the warp-specialised pair engine (32 or 64; 0 otherwise) */
+    int32_t prefill_s_buffers;  /* S buffers per block of that engine (32 keys: 2; 64 keys: 1 or 2; 0 otherwise) */
 } pod_plan_info;
 
 typedef struct pod_plan pod_plan;

@@ -70,7 +70,8 @@ class pod_options(C.Structure):
     _fields_ = [("policy", C.c_int32), ("tile_mode", C.c_int32), ("ctas_per_sm", C.c_int32),
                 ("virtual_decode", C.c_int32), ("split_wave_cap", C.c_int32),
                 ("decode_splits", C.c_int32), ("tile_override", C.POINTER(pod_tile_config)),
-                ("precision", C.c_int32), ("out_dtype", C.c_int32), ("prefill_tile_keys", C.c_int32)]
+                ("precision", C.c_int32), ("out_dtype", C.c_int32), ("prefill_tile_keys", C.c_int32),
+                ("prefill_s_buffers", C.c_int32)]
 
 
 class pod_plan_info(C.Structure):
@@ -80,7 +81,8 @@ class pod_plan_info(C.Structure):
                 ("decode_splits", C.c_int64), ("prefill_ratio", C.c_int64),
                 ("decode_ratio", C.c_int64), ("smem_bytes", C.c_int64),
                 ("workspace_bytes", C.c_int64), ("num_merge_rows_prefill", C.c_int32),
-                ("num_merge_rows_decode", C.c_int32), ("policy", C.c_int32), ("prefill_tile_keys", C.c_int32)]
+                ("num_merge_rows_decode", C.c_int32), ("policy", C.c_int32), ("prefill_tile_keys", C.c_int32),
+                ("prefill_s_buffers", C.c_int32)]
 
 
 # (name, restype, argtypes) for every symbol include/pod_attn.h declares.

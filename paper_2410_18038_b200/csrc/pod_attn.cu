@@ -132,7 +132,8 @@ struct RunParams {
     int32_t policy;
     int32_t p_split;  // prefill P as bf16 hi + lo (two PV MMAs)
     int32_t p_f16;    // POD_PRECISION_F16PV: P as fp16, V stages converted to fp16 in smem (bf16 data)
-    int32_t pf_tn64;  // warp-specialised kernel: 64-key single-S pair engine (prefill-dominant plans)
+    int32_t pf_tn64;  // warp-specialised kernel: 64-key pair engine (prefill-dominant plans)
+    int32_t pf_db;    // ... with two S buffers per block: kernel instance 1 (prefill_item_db)
     const int32_t* dec_nsplit;  // KV splits of each decode request (min(splits, ctx), pod_plan.cpp)
     int32_t vs_pages;  // > 0: prefill V tiles from the fp16 shadow (logical pages, already converted)
     int32_t trace;         // debug builds (POD_TRACE_STAMPS): per-tile cycle stamps after the role log
@@ -1413,7 +1414,7 @@ pod_status cuda_fail(cudaError_t e, const char* where) {
 }
 
 int64_t fused_smem_bytes() { return kSmemBytes; }
-int64_t sm_smem_bytes() { return sm3::kSmem; }
+int64_t sm_smem_bytes(bool db) { return db ? SmLay<1>::kSmem : SmLay<0>::kSmem; }
 
 struct Maps {
     CUtensorMap q, k, v;  // prefill role: SW128 boxes of 64 d x 16 tokens, Q boxes of 64 d x 128 rows
@@ -1550,6 +1551,7 @@ RunParams make_params(const pod_plan* plan, const void* q_prefill, const void* q
     p.p_split = plan->opts.precision == POD_PRECISION_SPLIT ? 1 : 0;
     p.p_f16 = plan->opts.precision == POD_PRECISION_F16PV ? 1 : 0;
     p.pf_tn64 = plan->pf_tn64 ? 1 : 0;
+    p.pf_db = plan->pf_db ? 1 : 0;
     p.out_fmt = plan->opts.out_dtype;
     p.dec_nsplit = reinterpret_cast<const int32_t*>(ws + plan->ws.off_dec_nsplit);
     p.vs_pages = plan->vs_pages;
@@ -1611,7 +1613,11 @@ pod_status set_kernel_attributes() {
             r = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
         if (r == cudaSuccess)
-            r = cudaFuncSetAttribute(pod_sm_kernel<G, kFmt>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3::kSmem);
+            r = cudaFuncSetAttribute(pod_sm_kernel<G, kFmt, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SmLay<0>::kSmem);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(pod_sm_kernel<G, kFmt, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SmLay<1>::kSmem);
         err[dev] = r;
     });
     if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
@@ -1644,16 +1650,24 @@ pod_status launch_all(const pod_plan* plan, int mode, const RunParams& p, const 
                 cudaLaunchConfig_t cfg{};
                 cfg.gridDim = dim3(nsm);
                 cfg.blockDim = dim3(sm3::kThreads);
-                cfg.dynamicSmemBytes = sm3::kSmem;
+                cfg.dynamicSmemBytes = q.pf_db ? SmLay<1>::kSmem : SmLay<0>::kSmem;
                 cfg.stream = s;
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
                 attr[0].val.programmaticStreamSerializationAllowed = 1;
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
-                cudaLaunchKernelEx(&cfg, pod_sm_kernel<G, kFmt>, q, maps.k, pf_v, maps.dk, maps.dv);
+                if (q.pf_db)
+                    cudaLaunchKernelEx(&cfg, pod_sm_kernel<G, kFmt, 1>, q, maps.k, pf_v, maps.dk, maps.dv);
+                else
+                    cudaLaunchKernelEx(&cfg, pod_sm_kernel<G, kFmt, 0>, q, maps.k, pf_v, maps.dk, maps.dv);
             } else {
-                pod_sm_kernel<G, kFmt><<<nsm, sm3::kThreads, sm3::kSmem, s>>>(q, maps.k, pf_v, maps.dk, maps.dv);
+                if (q.pf_db)
+                    pod_sm_kernel<G, kFmt, 1><<<nsm, sm3::kThreads, SmLay<1>::kSmem, s>>>(q, maps.k, pf_v, maps.dk,
+                                                                                         maps.dv);
+                else
+                    pod_sm_kernel<G, kFmt, 0><<<nsm, sm3::kThreads, SmLay<0>::kSmem, s>>>(q, maps.k, pf_v, maps.dk,
+                                                                                         maps.dv);
             }
         } else {
             const int grid = std::min(items, 2 * nsm);  // persistent: 2 resident CTAs per SM

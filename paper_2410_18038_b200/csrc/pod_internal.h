@@ -90,6 +90,7 @@ struct pod_plan {
     std::vector<int32_t> dec_pos;  // context_len - 1 per decode (KV append)
     std::vector<int32_t> dec_nsplit;  // KV splits per decode request (min(splits, ctx))
     bool pf_tn64 = false;          // warp-specialised: 64-key pair engine (see pod_plan.cpp)
+    bool pf_db = false;            // ... with two S buffers per block (prefill_item_db, kernel instance 1)
     int64_t decode_splits = 1;     // largest split count (partials' stride)
     int32_t vs_pages = 0;          // > 0: prefill V read from an fp16 shadow of these many pages (pod_plan.cpp)
     int64_t dec_split_base = 1;    // splits of requests [0, dec_tail_start)
@@ -115,6 +116,6 @@ namespace pod {
 // Dynamic shared memory of the fused / prefill kernel (defined in pod_attn.cu).
 int64_t fused_smem_bytes();
 // Dynamic shared memory of the warp-specialised one-CTA-per-SM kernel.
-int64_t sm_smem_bytes();
+int64_t sm_smem_bytes(bool db);
 void set_last_error(const std::string& s);
 }  // namespace pod

@@ -286,6 +286,11 @@ void lower(pod_plan& p) {
     {
         const int32_t keys = p.opts.prefill_tile_keys;
         p.pf_tn64 = warpspec && p.batch.has_prefill && (keys == 64 || (keys == 0 && decode_share(p) < 0.57));
+        // two S buffers per block (Q in smem, the decode group at 2 ring stages per warp): fused C2
+        // B=8 (decode share 0.17) 356 -> 332 us, B=16 (0.29) 369 -> 365, but C1 (0.32) 56 -> 59 and
+        // B=32 (0.45) 436 -> 555 -- the smaller decode rings cost more than the prefill gains
+        const int32_t sb = p.opts.prefill_s_buffers;
+        p.pf_db = p.pf_tn64 && (sb == 2 || (sb == 0 && decode_share(p) < 0.25));
     }
     // Whole waves (warp-specialised kernel): the decode items are claimed in id order
     // (request-major) by one decode group per SM, so a count that is not a multiple of
@@ -434,7 +439,7 @@ pod_tile_config b200_tile_config(const pod_plan& p) {
     const int rows = (two_blocks ? 2 : 1) * pod::kMBlock;
     c.prefill_tile_q = std::max(1, rows / group);
     c.tile_kv = pod::kKvTile;
-    c.shared_mem_per_cta = static_cast<double>(p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes()
+    c.shared_mem_per_cta = static_cast<double>(p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes(false)
                                                                                    : pod::fused_smem_bytes());
     c.virtual_decode = 1;
     return c;
@@ -516,7 +521,7 @@ void build(pod_plan& p) {
     if (!p.decode_ctx.empty()) decompose_decode(p);
     lower(p);
     scheduler_ratio(p);
-    p.smem_bytes = p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes() : pod::fused_smem_bytes();
+    p.smem_bytes = p.opts.policy == POD_POLICY_WARPSPEC ? pod::sm_smem_bytes(p.pf_db) : pod::fused_smem_bytes();
     // POD_PRECISION_F16PV on bf16 data needs V in fp16.  The two-CTA kernel's prefill CTA
     // converting every V tile it streams sits on its softmax warps' critical path (S is
     // double-buffered there): prefill-alone at C2 is 327 us with it, 256 us without (bf16 P,
@@ -561,6 +566,7 @@ void pod_options_default(pod_options* out) {
     out->precision = POD_PRECISION_F16PV;
     out->out_dtype = POD_OUT_F32;
     out->prefill_tile_keys = 0;
+    out->prefill_s_buffers = 0;
 }
 
 pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const pod_device* dev,
@@ -593,6 +599,8 @@ pod_status pod_attn_plan(const pod_shape* shape, const pod_batch* batch, const p
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: precision must be a POD_PRECISION_* value");
         if (p->opts.out_dtype < POD_OUT_F32 || p->opts.out_dtype > POD_OUT_F16)
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: out_dtype must be a POD_OUT_* value");
+        if (p->opts.prefill_s_buffers < 0 || p->opts.prefill_s_buffers > 2)
+            fail(POD_ERR_INVALID_ARGUMENT, "pod_options: prefill_s_buffers must be 0, 1 or 2");
         if (p->opts.prefill_tile_keys != 0 && p->opts.prefill_tile_keys != 32 && p->opts.prefill_tile_keys != 64)
             fail(POD_ERR_INVALID_ARGUMENT, "pod_options: prefill_tile_keys must be 0, 32 or 64");
         build(*p);
@@ -630,6 +638,7 @@ pod_status pod_attn_plan_get_info(const pod_plan* p, pod_plan_info* out) {
     out->num_merge_rows_decode = p->merge_rows_decode;
     out->policy = p->opts.policy;
     out->prefill_tile_keys = p->opts.policy == POD_POLICY_WARPSPEC && p->batch.has_prefill ? (p->pf_tn64 ? 64 : 32) : 0;
+    out->prefill_s_buffers = out->prefill_tile_keys == 0 ? 0 : (!p->pf_tn64 || p->pf_db) ? 2 : 1;
     return POD_OK;
 }
 

@@ -905,6 +905,301 @@ __device__ void prefill_item_sm64(const RunParams& p, const CUtensorMap* tmk, co
     }
 }
 
+// ---------------------------------------------------------------------------
+// The pair engine over 64-key tiles with DOUBLE-buffered S per block (prefill-dominant
+// plans, pf_tn64; the kE = 1 kernel instance).  The single-S 64-key engine cannot start
+// QK_X(t+1) before the softmax of tile t has handed P over (P lives over S), so each
+// block's chain is softmax -> P hop -> PV + QK -> S hop per tile.  With two
+// S buffers per block QK_X(t+2) runs while the softmax of tile t+1 does, as in the
+// two-CTA kernel's prefill CTA (the fastest prefill engine of the repo) -- but TMEM then
+// has no room for Q (S_A[2] | S_B[2] | O_A | O_B = 512 columns), so Q sits in shared
+// memory and QK^T is an SS-MMA, and the decode group keeps 2 ring stages per warp:
+//   smem  K ring [0, 32K) | V ring [32K, 64K) | Q_A | Q_B (SW128, 32 KB each) | decode
+// V comes from the fp16 shadow (pod_plan::vs_pages) for F16PV plans, so no per-tile
+// conversion sits on the softmax warps either.
+namespace db {
+constexpr int kTN = 64, kNS = 2;
+constexpr uint32_t kStage = kTN * kHeadDim * 2;       // 16 KB: K [d-half][64 keys][64 d]; V page-major
+constexpr uint32_t kQBytes = kMBlock * kHeadDim * 2;  // 32 KB per block
+constexpr uint32_t kOffK = 0, kOffV = kNS * kStage, kOffQ = 2 * kNS * kStage;
+constexpr uint32_t kPfBytes = kOffQ + 2 * kQBytes;    // 128 KB
+constexpr uint32_t kSA = 0, kSB = 128, kOA = 256, kOB = 384;  // S_X[b] at kSX + 64 b
+static_assert(kNS <= sm3::kNS, "stage barriers");
+static_assert(kNS * kStage >= 8 * 4096, "the epilogue's 8 warp tiles (store_o_rows) fit the K ring");
+template <int kFmt>
+__device__ __forceinline__ void issue_qk(uint32_t tmem_s, uint32_t sQ, uint32_t sK) {
+    constexpr uint32_t idesc = ptx::idesc_f16(kFmt, kMBlock, kTN, 0);
+    ptx::umma_ss_k128_elect<kMBlock * 128, kTN * 128>(tmem_s, ptx::sw128_desc(sQ, 16, 1024),
+                                                      ptx::sw128_desc(sK, 16, 1024), idesc);
+}
+}  // namespace db
+
+template <int kFmt, uint32_t kOffBars>
+__device__ void prefill_item_db(const RunParams& p, const CUtensorMap* tmk, const CUtensorMap* tmv /* 5-D page map */,
+                                int item, uint32_t sbase, uint32_t tmem, sm3::PfState& ps, int warp, int lane) {
+    using namespace sm3;
+    using db::kTN;
+    using db::kNS;
+    using db::kStage;
+    const PrefillCta job = p.pctas[item];
+    const int G = p.group;
+    const int rpb = kMBlock / G;
+    const int nblocks = (job.rows + rpb - 1) / rpb;  // 1 or 2
+    const bool hasB = nblocks > 1;
+    const BlockRange rA = prefill_block(p, job, 0);
+    const BlockRange rB = hasB ? prefill_block(p, job, 1) : rA;
+    const int kv_hi = min(job.kv_end, p.offset + (hasB ? rB.r0 + rB.nrows : rA.r0 + rA.nrows));
+    const int kt0 = rA.kt0;
+    const int nt = kv_hi > job.kv_begin ? (kv_hi - kt0 + kTN - 1) / kTN : 0;
+    const PfState s0 = uniform(ps);
+    if (nt > 0) {  // as prefill_item_sm: tiles, S / P completions, Q loads, lazy PV commits
+        ps.g += nt;
+        ps.n[0] += nt;
+        ps.nq[0] += 1;
+        if (hasB) {
+            ps.n[1] += nt;
+            ps.nq[1] += 1;
+        }
+        for (int t = max(0, nt - 2); t < nt; ++t) {
+            ps.npv[0][(s0.n[0] + t) & 1] += 1;
+            if (hasB) ps.npv[1][(s0.n[1] + t) & 1] += 1;
+        }
+    }
+    // PV_X(t) commits only for the last two tiles (one per S buffer); earlier, "PV_X(t-1)
+    // done" is implied by S_X(t+1)'s commit (prefill_item_sm)
+    auto pv_commit = [&](int t) { return t + 2 >= nt; };
+    const int pbeg = p.page_indptr[0];
+    const int npages = p.page_indptr[1] - pbeg;
+    const uint32_t bar0 = sbase + kOffBars;
+    auto bar = [&](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
+    const uint32_t sK = sbase + db::kOffK, sV = sbase + db::kOffV, sQ = sbase + db::kOffQ;
+
+    if (warp == kProdWarp) {
+        // ------------------------------------------------ TMA producer --
+        // K(t), then V(t-1): K stages free after both QK(t) (issued two tiles ahead), V stages
+        // after both PV(t)
+        PageIds ids;
+        ids.init(p.page_indices + pbeg, npages, kt0 / 16);
+        for (int t = 0; t <= nt && nt > 0; ++t) {
+            if (t < nt) {
+                const int gg = s0.g + t, st = gg % kNS;
+                if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarKE + st), ((gg / kNS) - 1) & 1);
+                ptx::mbar_arrive_expect_tx_elect(bar(kBarKF + st), kStage);
+                sm64::load_tile64(p, tmk, sK + st * kStage, bar(kBarKF + st), kt0 + t * kTN, job.kv_head, ids);
+            }
+            if (t > 0) {
+                const int gg = s0.g + t - 1, st = gg % kNS;
+                if (gg >= kNS) ptx::mbar_wait_relaxed<POD_SM_PROD_SLEEP>(bar(kBarVE + st), ((gg / kNS) - 1) & 1);
+                if (p.vs_pages && t == 1) ptx::griddep_wait();  // the fp16 V shadow (see prefill_item)
+                ptx::mbar_arrive_expect_tx_elect(bar(kBarVF + st), kStage);
+                prefill_load_v_pages<4>(tmv, sV + st * kStage, bar(kBarVF + st), kt0 + (t - 1) * kTN, job.kv_head,
+                                        ids, p.vs_pages);
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // -------------------------------------------------- MMA issuer --
+        auto mma_issuer = [&](auto pv_c) {  // kPv as in prefill_item_sm
+            constexpr int kPv = decltype(pv_c)::value;
+            constexpr bool kSplit = kPv == 0;
+            constexpr int kPvFmt = kPv == 2 ? 0 : kFmt;
+            constexpr uint32_t idesc_pv = ptx::idesc_f16(kPvFmt, kMBlock, kHeadDim, 1);
+            if (nt == 0) return;
+            ptx::mbar_wait(bar(0), s0.nq[0] & 1);
+            if (hasB) ptx::mbar_wait(bar(1), s0.nq[1] & 1);
+            for (int j = 0; j < 2 && j < nt; ++j) {
+                const int gg = s0.g + j, st = gg % kNS;
+                ptx::mbar_wait(bar(kBarKF + st), (gg / kNS) & 1);
+                ptx::tc_fence_after();
+                const int bA = (s0.n[0] + j) & 1, bB = (s0.n[1] + j) & 1;
+                db::issue_qk<kFmt>(tmem + db::kSA + 64 * bA, sQ, sK + st * kStage);
+                ptx::umma_commit_elect(bar(kBarS + bA));
+                if (hasB) {
+                    db::issue_qk<kFmt>(tmem + db::kSB + 64 * bB, sQ + db::kQBytes, sK + st * kStage);
+                    ptx::umma_commit_elect(bar(kBarS + 2 + bB));
+                }
+                ptx::umma_commit_elect(bar(kBarKE + st));  // K(j): both QKs issued
+            }
+            for (int t = 0; t < nt; ++t) {
+                const int gg = s0.g + t, st = gg % kNS;
+                const int g2 = gg + 2, st2 = g2 % kNS;
+                const bool more = t + 2 < nt;
+#pragma unroll
+                for (int X = 0; X < 2; ++X) {
+                    if (X == 1 && !hasB) break;
+                    const int n = s0.n[X] + t, b = n & 1;
+                    const uint32_t tS = tmem + (X ? db::kSB : db::kSA) + 64 * b;
+                    ptx::mbar_wait(bar(kBarP + 2 * X + b), (n >> 1) & 1);
+                    if (X == 0) ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
+                    ptx::tc_fence_after();
+                    ptx::umma_pv64_elect<kSplit>(tmem + (X ? db::kOB : db::kOA), tS,
+                                                 ptx::sw128_desc(sV + st * kStage, 2048, 1024), idesc_pv,
+                                                 t > 0 ? 1u : 0u);
+                    if (pv_commit(t)) ptx::umma_commit_elect(bar(kBarPV + 2 * X + b));
+                    if (more) {  // QK_X(t+2) reuses S_X[b] after PV_X(t) read its P (in-order pipe)
+                        if (X == 0) {
+                            ptx::mbar_wait(bar(kBarKF + st2), (g2 / kNS) & 1);
+                            ptx::tc_fence_after();
+                        }
+                        db::issue_qk<kFmt>(tS, sQ + X * db::kQBytes, sK + st2 * kStage);
+                        ptx::umma_commit_elect(bar(kBarS + 2 * X + b));
+                    }
+                }
+                ptx::umma_commit_elect(bar(kBarVE + st));             // V(t): both PVs issued
+                if (more) ptx::umma_commit_elect(bar(kBarKE + st2));  // K(t+2): both QKs issued
+            }
+        };
+        if (kFmt == 1 && p.p_f16)
+            mma_issuer(std::integral_constant<int, 2>{});
+        else if (p.p_split != 0)
+            mma_issuer(std::integral_constant<int, 0>{});
+        else
+            mma_issuer(std::integral_constant<int, 1>{});
+    } else if (warp < kProdWarp) {
+        // ------------------------------------ softmax (4 warps per block) --
+        const int X = warp >> 2;
+        if (X == 1 && !hasB) return;
+        const int q = warp & 3;
+        const BlockRange br = X ? rB : rA;
+        const int m = q * 32 + lane;
+        const int my_r = br.r0 + m / G;
+        const bool row_ok = (m / G) < br.nrows;
+        const int vis = p.offset + my_r;
+        const int qhead = job.kv_head * G + m % G;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        const uint32_t o_addr = lane_base + (X ? db::kOB : db::kOA);
+        ORow orow;
+        float* lrow;
+        if (job.n_splits == 1) {
+            orow = out_row(p.o_prefill, (static_cast<size_t>(my_r) * p.hq + qhead) * p.hd, p.out_fmt);
+            lrow = p.lse_prefill + static_cast<size_t>(my_r) * p.hq + qhead;
+        } else {
+            const size_t row = (static_cast<size_t>(job.split) * p.chunk + my_r) * p.hq + qhead;
+            orow = out_row(p.ppart_o, row * p.hd, 0);
+            lrow = p.ppart_lse + row;
+        }
+        if (nt == 0) {
+            if (row_ok) {
+                for (int c = 0; c < p.hd; c += 4) store4(orow, c, make_float4(0.f, 0.f, 0.f, 0.f));
+                *lrow = -INFINITY;
+            }
+            return;
+        }
+        {  // Q row -> shared memory, SW128 K-major (A operand of the SS QK^T); zero past the chunk / head dim
+            const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(p.q_prefill) +
+                                                              (static_cast<size_t>(my_r) * p.hq + qhead) * p.hd);
+            const uint32_t dst = sQ + X * db::kQBytes + static_cast<uint32_t>(m) * 128u;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint4 v = row_ok && 8 * j < p.hd ? __ldg(src + j) : make_uint4(0u, 0u, 0u, 0u);
+                const uint32_t a = dst + (j >> 3) * (kMBlock * 128u) + ((static_cast<uint32_t>(j & 7) ^ (m & 7)) << 4);
+                asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                             : "memory");
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(bar(X));
+        }
+        // POD_PRECISION_F16PV without the shadow (it is on for these plans with bf16 data): block
+        // A converts V(t) before its P(t) arrival, as in prefill_item_sm
+        auto v_to_f16 = [&](int t) {
+            const int gg = s0.g + t, st = gg % kNS;
+            ptx::mbar_wait(bar(kBarVF + st), (gg / kNS) & 1);
+            v_stage_to_f16<kStage, 128>(sV + st * kStage, q * 32 + lane);
+        };
+        const bool convert = kFmt == 1 && p.p_f16 && !p.vs_pages && X == 0;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int t = 0; t < nt; ++t) {
+            const int n = s0.n[X] + t, b = n & 1;
+            const uint32_t s_addr = lane_base + (X ? db::kSB : db::kSA) + 64 * b;
+            ptx::mbar_wait(bar(kBarS + 2 * X + b), (n >> 1) & 1);
+            ptx::tc_fence_after();
+            float s[kTN];
+            ptx::tmem_ld32(s_addr, *reinterpret_cast<float(*)[32]>(&s[0]));
+            ptx::tmem_ld32(s_addr + 32, *reinterpret_cast<float(*)[32]>(&s[32]));
+            ptx::tmem_wait_ld();
+            const int kb = kt0 + t * kTN;
+            const int lo = max(job.kv_begin - kb, 0);
+            const int hi = row_ok ? min(min(job.kv_end, vis + 1) - kb, kTN) : 0;
+            if (!__all_sync(0xffffffffu, lo == 0 && hi == kTN)) {
+#pragma unroll
+                for (int c = 0; c < kTN; ++c)
+                    if (c < lo || c >= hi) s[c] = -INFINITY;
+            }
+            const float tmax = row_max<kTN>(s);
+            const float m_new = fmaxf(m_run, tmax * p.sl2);
+            const bool need = m_new > m_run + 8.f;  // lazy rescale (see prefill_item)
+            const float m_use = need ? m_new : m_run;
+            const float factor = need ? ptx::ex2(m_run - m_new) : 1.f;
+            l_run *= factor;
+            m_run = m_use;
+            if (t > 0 && __any_sync(0xffffffffu, need)) {  // wait for PV_X(t-1), the newest MMA writing O_X
+                if (t + 1 < nt)  // S_X(t+1) complete => PV_X(t-1) complete
+                    ptx::mbar_wait(bar(kBarS + 2 * X + ((n + 1) & 1)), ((n + 1) >> 1) & 1);
+                else
+                    ptx::mbar_wait(bar(kBarPV + 2 * X + ((n - 1) & 1)), s0.npv[X][(n - 1) & 1] & 1);
+                ptx::tc_fence_after();
+#pragma unroll 1
+                for (int ch = 0; ch < kHeadDim / 32; ++ch) {
+                    float o[32];
+                    ptx::tmem_ld32(o_addr + ch * 32, o);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) o[c] *= factor;
+                    ptx::tmem_st32(o_addr + ch * 32, o);
+                }
+            }
+            const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
+            float lsum;
+            if (kFmt == 1 && p.p_f16)
+                lsum = softmax_p_row<kFmt, 3, kTN>(s, p.sl2, neg_m, s_addr);
+            else if (kFmt == 1 && p.p_split)
+                lsum = softmax_p_row<kFmt, 1, kTN>(s, p.sl2, neg_m, s_addr);
+            else if (p.p_split)
+                lsum = softmax_p_row<kFmt, 2, kTN>(s, p.sl2, neg_m, s_addr);
+            else
+                lsum = softmax_p_row<kFmt, 0, kTN>(s, p.sl2, neg_m, s_addr);
+            l_run += lsum;
+            if (convert) v_to_f16(t);  // V(t) before P(t) goes to the MMA issuer
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(bar(kBarP + 2 * X + b));
+        }
+        // ------------------------------------------------- epilogue --
+        {
+            const int nl = s0.n[X] + nt - 1;
+            ptx::mbar_wait(bar(kBarPV + 2 * X + (nl & 1)), s0.npv[X][nl & 1] & 1);
+            if (nt >= 2) ptx::mbar_wait(bar(kBarPV + 2 * X + ((nl - 1) & 1)), s0.npv[X][(nl - 1) & 1] & 1);
+        }
+        ptx::tc_fence_after();
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+        store_o_rows(o_addr, inv, orow, row_ok, sbase + db::kOffK + static_cast<uint32_t>(warp) * 4096u, lane, p.hd);
+        if (row_ok) *lrow = l_run > 0.f ? (m_run + ptx::lg2(l_run)) * kLn2 : -INFINITY;
+        ptx::tc_fence_before();
+    }
+}
+
+// Shared-memory layout of the two kernel instances: kE = 0 (32- / 64-key single-S engines,
+// six decode warps x 3 ring stages) and kE = 1 (the double-S 64-key engine: Q in smem,
+// six decode warps x 2 ring stages).
+template <int kE>
+struct SmLay {
+    static constexpr int kDW = sm3::kDW, kDS = sm3::kDS;
+    static constexpr uint32_t kOffDec = sm3::kOffDec, kOffBars = sm3::kOffBars, kOffDecBars = sm3::kOffDecBars,
+                              kOffMisc = sm3::kOffMisc, kSmem = sm3::kSmem;
+};
+template <>
+struct SmLay<1> {
+    static constexpr int kDW = sm3::kDW, kDS = 2;
+    static constexpr uint32_t kOffDec = db::kPfBytes;
+    static constexpr uint32_t kOffBars = kOffDec + kDW * kDS * kDecStageBytes;
+    static constexpr uint32_t kOffDecBars = kOffBars + sm3::kNumBars * 8;
+    static constexpr uint32_t kOffMisc = kOffDecBars + kDW * kDS * 8;
+    static constexpr uint32_t kSmem = kOffMisc + 64;
+    static_assert(kSmem <= 232448, "one CTA per SM: <= 227 KB dynamic smem");
+    static_assert(kOffDec % 1024 == 0, "SW128 stages are 1024-aligned");
+};
+
 __device__ __forceinline__ void sm_log_claim(const RunParams& p, int op, int id, int32_t* slot_out) {
     *slot_out = -1;
     if (!p.role_log || id < 0) return;
@@ -922,12 +1217,16 @@ __device__ __forceinline__ void sm_log_claim(const RunParams& p, int op, int id,
 }
 
 // One CTA per SM; both engines bind items from their pools until drained.
-template <int G, int kFmt>
+template <int G, int kFmt, int kE>
 __global__ void __launch_bounds__(sm3::kThreads, 1)
     pod_sm_kernel(const __grid_constant__ RunParams p, const __grid_constant__ CUtensorMap tmk,
                   const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tdk,
                   const __grid_constant__ CUtensorMap tdv) {
     using namespace sm3;
+    using L = SmLay<kE>;
+    constexpr int kDS = L::kDS;
+    constexpr uint32_t kOffDec = L::kOffDec, kOffBars = L::kOffBars, kOffDecBars = L::kOffDecBars,
+                       kOffMisc = L::kOffMisc;
     extern __shared__ __align__(1024) uint8_t smem[];
     // Logical warp roles (0-7 softmax, 8 producer, 9 MMA, 10.. decode).  With
     // POD_SM_SOFTMAX_HIGH the decode group takes the lowest hardware warp ids and the
@@ -997,8 +1296,9 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
             const int id = wuni(misc[2]);
             prev_slot = misc[3];
             if (id < 0) break;
-            if (p.pf_tn64)
-            {
+            if constexpr (kE == 1) {
+                prefill_item_db<kFmt, kOffBars>(p, &tmk, p.vs_pages ? &tmv : &tdv, id, sbase, tmem, ps, warp, lane);
+            } else if (p.pf_tn64) {
                 const int fi = ps.n[0] == 0 ? 0 : 1;  // debug trace: the CTA's first item
                 if (tid == 0) trace_stamp(p, fi, 767, 1);
                 prefill_item_sm64<kFmt>(p, &tmk, p.vs_pages ? &tmv : &tdv, id, sbase, tmem, ps, warp, lane);

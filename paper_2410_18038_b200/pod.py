@@ -226,6 +226,7 @@ class PlanOptions:
     precision: int = _abi.POD_PRECISION_F16PV
     out_dtype: int = _abi.POD_OUT_F32
     prefill_tile_keys: int = 0  # warp-specialised pair engine: 0 = auto, 32 or 64
+    prefill_s_buffers: int = 0  # 64-key pair engine: 0 = auto, 1 = single S (Q in TMEM), 2 = double S (Q in smem)
 
 
 def _task(t) -> CtaTask:
@@ -250,6 +251,7 @@ class Plan:
         o.precision = options.precision
         o.out_dtype = options.out_dtype
         o.prefill_tile_keys = options.prefill_tile_keys
+        o.prefill_s_buffers = options.prefill_s_buffers
         tc = None
         if options.tile_override is not None:
             tc = options.tile_override._c()

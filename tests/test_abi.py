@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     l = _abi.lib()
-    assert l.pod_attn_abi_version() == 1
+    assert l.pod_attn_abi_version() == 2
     for code, name in _abi.STATUS_NAMES.items():
         assert l.pod_status_string(code).decode() == name
 
@@ -63,6 +63,10 @@ def test_plan_info_and_workspace():
     # the pair engine's tile width: 32 keys for this decode-dominant batch, forceable
     assert i.prefill_tile_keys == 32
     assert Plan(b, GpuSpec.b200(), PlanOptions(prefill_tile_keys=64)).info().prefill_tile_keys == 64
+    assert i.prefill_s_buffers == 2  # the 32-key engine double-buffers S
+    for sb in (1, 2):  # the 64-key engine: one S buffer (Q in TMEM) or two (Q in smem, own kernel instance)
+        isb = Plan(b, GpuSpec.b200(), PlanOptions(prefill_tile_keys=64, prefill_s_buffers=sb)).info()
+        assert isb.prefill_s_buffers == sb and isb.smem_bytes + 1024 <= 233472
     # the two-CTA-per-SM POD kernel
     p = Plan(b, GpuSpec.b200(), PlanOptions(policy=_abi.POD_POLICY_COMPLEMENT))
     i = p.info()

@@ -131,10 +131,10 @@ def _check_oracle_sample(wl, out):
     assert eo <= O_TOL and el <= LSE_TOL, ("oracle decode", eo, el)
 
 
-def _run(wl, batch, policy=POD_POLICY_AUTO, keys=0):
+def _run(wl, batch, policy=POD_POLICY_AUTO, keys=0, s_buffers=0):
     from paper_2410_18038_b200.hybrid import PodAttention
 
-    opts = pkg.PlanOptions(policy=policy, prefill_tile_keys=keys)
+    opts = pkg.PlanOptions(policy=policy, prefill_tile_keys=keys, prefill_s_buffers=s_buffers)
     op = PodAttention(batch, options=opts)
     out = op.run(wl.q_prefill, wl.q_decode, wl.k_pool, wl.v_pool, wl.page_indptr, wl.page_indices)
     torch.cuda.synchronize()
@@ -168,9 +168,10 @@ def test_baseline_config_full_size_peaky(name):
 
 
 @pytest.mark.parametrize("name", ["c2_b16", "c4"])
-@pytest.mark.parametrize("kernel", [(POD_POLICY_COMPLEMENT, 0), (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64)])
+@pytest.mark.parametrize("kernel", [(POD_POLICY_COMPLEMENT, 0), (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64, 1),
+                                    (POD_POLICY_WARPSPEC, 64, 2)])
 def test_baseline_config_full_size_every_kernel(name, kernel):
-    """Both POD kernels (and both pair-engine widths) forced at C2 B=16 and C4."""
+    """Both POD kernels (and every pair engine) forced at C2 B=16 and C4."""
     _need_gpu()
     batch = _batch(name)
     wl = build_workload(batch, device="cuda")

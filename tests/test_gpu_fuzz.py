@@ -28,7 +28,8 @@ KERNELS = [
     ("auto", dict(policy=POD_POLICY_AUTO)),
     ("complement", dict(policy=POD_POLICY_COMPLEMENT)),
     ("ws32", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32)),
-    ("ws64", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64)),
+    ("ws64", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64, prefill_s_buffers=1)),
+    ("ws64db", dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64, prefill_s_buffers=2)),
 ]
 
 

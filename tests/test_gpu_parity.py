@@ -72,7 +72,8 @@ def test_matches_oracle(name, mode):
     _check(wl, out)
     # the warp-specialised one-CTA-per-SM kernel, both pair-engine tile widths
     for opts in (pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32),
-                 pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64)):
+                 pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64, prefill_s_buffers=1),
+                 pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64, prefill_s_buffers=2)):
         wl, _, out = _run(batch, mode, options=opts, wl=wl)
         _check(wl, out)
 
@@ -88,7 +89,7 @@ def test_fast_precision_bf16_p_within_loose_bound():
 
 
 @pytest.mark.parametrize("precision", [POD_PRECISION_F16PV, POD_PRECISION_SPLIT])
-@pytest.mark.parametrize("kernel", ["complement", 32, 64])
+@pytest.mark.parametrize("kernel", ["complement", 32, 64, "64db"])
 @pytest.mark.parametrize("q_scale", [1.0, 8.0])
 @pytest.mark.parametrize("name", ["hybrid_gqa4", "page_edges", "gqa8", "mha", "prefill_only"])
 def test_precision_modes_match_oracle(precision, kernel, q_scale, name):
@@ -101,7 +102,10 @@ def test_precision_modes_match_oracle(precision, kernel, q_scale, name):
     hq, hkv, chunk, off, dec = CASES[name]
     batch = make_batch(pkg.ModelShape(hq, hkv, 128, SCALE), chunk=chunk, offset=off, decode_ctx=dec)
     opts = (pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT, precision=precision) if kernel == "complement"
-            else pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=kernel, precision=precision))
+            else pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64, prefill_s_buffers=2,
+                                 precision=precision) if kernel == "64db"
+            else pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=kernel, prefill_s_buffers=1 if kernel == 64 else 0,
+                                 precision=precision))
     wl, _, out = _run(batch, options=opts, q_scale=q_scale)
     _check(wl, out)
     eo, el = compare_prefill(wl, out.o_prefill.cpu().numpy(), out.lse_prefill.cpu().numpy())
@@ -124,14 +128,15 @@ def test_policies_and_reference_tiles(policy):
 
 
 # the POD kernels: two CTAs per SM (COMPLEMENT) and one warp-specialised CTA per SM with
-# its 32-key (double-S) or 64-key (single-S) pair engine
-KERNELS = [POD_POLICY_COMPLEMENT, (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64)]
+# its 32-key (double-S) or 64-key (single-S; double-S with Q in smem) pair engine
+KERNELS = [POD_POLICY_COMPLEMENT, (POD_POLICY_WARPSPEC, 32), (POD_POLICY_WARPSPEC, 64), (POD_POLICY_WARPSPEC, 64, 2)]
 
 
 def _kopts(kernel, **kw):
     """PlanOptions for one entry of KERNELS."""
     if isinstance(kernel, tuple):
-        return pkg.PlanOptions(policy=kernel[0], prefill_tile_keys=kernel[1], **kw)
+        sb = kernel[2] if len(kernel) > 2 else (1 if kernel[1] == 64 else 0)
+        return pkg.PlanOptions(policy=kernel[0], prefill_tile_keys=kernel[1], prefill_s_buffers=sb, **kw)
     return pkg.PlanOptions(policy=kernel, **kw)
 
 

@@ -31,7 +31,8 @@ from tests.common import LSE_TOL, O_TOL, rel_err
 pytestmark = pytest.mark.gpu
 
 KERNELS = [dict(policy=POD_POLICY_COMPLEMENT), dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32),
-           dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64)]
+           dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64, prefill_s_buffers=1),
+           dict(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64, prefill_s_buffers=2)]
 
 
 def _bf16(x: np.ndarray) -> torch.Tensor:

@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for c in c2_b8 c2_b16 c2_b32 c1; do echo "== $c"; bash tools/exp.sh $c 2:0:8 2:0:3; done
-for c in c2_b64 c4; do echo "== $c"; bash tools/exp.sh $c 2:0:8; done
+timeout 2000 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for c in c2_b8 c2_b16 c2_b32 c1 c2_b64; do echo "== $c"; bash tools/exp.sh $c 2:0:8; done
