@@ -78,11 +78,15 @@ def main():
     # ncu summaries + the headline kernel's DRAM traffic
     for rep, (md, title) in NCU.items():
         p = src / f"{rep}.ncu-rep"
-        if p.exists():
+        if (src / f"{rep}.md").exists():  # summarised on the box (the reports stay there)
+            (dst / md).write_text((src / f"{rep}.md").read_text())
+        elif p.exists():
             txt = subprocess.run([sys.executable, "tools/ncu_summary.py", str(p.resolve().relative_to(ROOT)),
                                   "--title", title], capture_output=True, text=True, check=True, cwd=ROOT).stdout
             (dst / md).write_text(txt)
-    if (src / "ev_launches.csv").exists():
+    if (src / "ev_launches.md").exists():
+        (dst / "launches.md").write_text((src / "ev_launches.md").read_text())
+    elif (src / "ev_launches.csv").exists():
         txt = subprocess.run([sys.executable, "tools/ncu_summary.py", "--launches",
                               str((src / "ev_launches.csv").resolve().relative_to(ROOT))], capture_output=True,
                              text=True, check=True, cwd=ROOT).stdout

@@ -18,4 +18,8 @@ timeout 200 python tools/profile_run.py --config c2_b64 --mode fused --iters 3 -
 timeout 600 python tools/serve_bench.py > gpurun_out/ev_serve.log 2>&1
 timeout 600 python -m paper_2410_18038_b200.verify --instances 300 > gpurun_out/ev_verify.log 2>&1; echo "verify rc=$?" >> gpurun_out/ev_verify.log
 timeout 1500 python tools/sweep.py > gpurun_out/ev_sweep_c5.jsonl 2> gpurun_out/ev_sweep.err
+# summaries on the box (gpurun copies back <= 64 MiB): the .ncu-rep files stay behind
+for r in gpurun_out/ev_ncu_*.ncu-rep; do python tools/ncu_summary.py "$r" --title "$(basename "$r" .ncu-rep | sed 's/^ev_ncu_//')" > "${r%.ncu-rep}.md" 2>/dev/null; done
+python tools/ncu_summary.py --launches gpurun_out/ev_launches.csv > gpurun_out/ev_launches.md 2>/dev/null
+mkdir -p /tmp/ncu_reps && mv gpurun_out/ev_ncu_*.ncu-rep /tmp/ncu_reps/ 2>/dev/null
 ls gpurun_out | grep ev_ | wc -l
