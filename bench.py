@@ -439,7 +439,7 @@ def run_pod(args, rank, world, local_rank):
     opts = pkg.PlanOptions(policy=args.policy, tile_mode=args.tile_mode, precision=args.precision,
                            decode_splits=args.decode_splits, split_wave_cap=args.split_wave_cap,
                            out_dtype={"f32": 0, "bf16": 1}[args.out_dtype],
-                           prefill_tile_keys=args.prefill_tile_keys)
+                           prefill_tile_keys=args.prefill_tile_keys, prefill_s_buffers=args.prefill_s_buffers)
     op = PodAttention(batch, options=opts, device=local_rank)
     # the kernel writes straight into the all-gather send buffer (two, for the pipelined e2e)
     gbs = [gather_buffers(batch, world, odt, dev) for _ in range(2)]
@@ -617,6 +617,8 @@ def main():
                     help="element type of the attention outputs (LSE stays fp32); f32 = the reference's")
     ap.add_argument("--decode-splits", type=int, default=0)
     ap.add_argument("--prefill-tile-keys", type=int, default=0, help="warp-specialised pair engine: 0 auto, 32 or 64")
+    ap.add_argument("--prefill-s-buffers", type=int, default=0,
+                    help="64-key pair engine: 0 auto, 1 single S (Q in TMEM), 2 double S (Q in smem)")
     ap.add_argument("--split-wave-cap", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
@@ -732,7 +734,7 @@ def main():
         "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
                  "prefill_splits": info.prefill_splits, "decode_splits": info.decode_splits,
                  "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
-                 "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_tile_keys": info.prefill_tile_keys, "prefill_p": {0: "bf16 hi+lo", 1: "bf16", 2: "fp16 (V -> fp16 in smem)"}[args.precision], "out_dtype": args.out_dtype},
+                 "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_tile_keys": info.prefill_tile_keys, "prefill_s_buffers": info.prefill_s_buffers, "prefill_p": {0: "bf16 hi+lo", 1: "bf16", 2: "fp16 (V -> fp16 in smem)"}[args.precision], "out_dtype": args.out_dtype},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": {7: "pod_sm_kernel (+merge)"}.get(r["info"].policy, "pod_fused_kernel (+merge)"),

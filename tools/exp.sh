@@ -3,8 +3,8 @@
 #   tools/exp.sh CONFIG precision:tile_keys:policy:split_wave_cap:decode_splits ...
 cfg=${1:-c2_b64}; shift
 for v in "$@"; do
-  IFS=: read -r prec tk pol swc ds <<< "$v"
-  line=$(timeout 300 python bench.py --config $cfg --precision $prec --policy ${pol:-8} --split-wave-cap ${swc:-0} --decode-splits ${ds:-0} --prefill-tile-keys ${tk:-0} --no-cpu-baseline --no-serial-search --steps 10 2>/dev/null | tail -1)
+  IFS=: read -r prec tk pol swc ds sb <<< "$v"
+  line=$(timeout 300 python bench.py --config $cfg --precision $prec --policy ${pol:-8} --split-wave-cap ${swc:-0} --decode-splits ${ds:-0} --prefill-tile-keys ${tk:-0} --prefill-s-buffers ${sb:-0} --no-cpu-baseline --no-serial-search --steps 10 2>/dev/null | tail -1)
   python - "$v" "$line" <<'PY'
 import json,sys
 v=sys.argv[1]
