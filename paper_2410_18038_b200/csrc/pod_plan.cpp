@@ -287,10 +287,10 @@ void lower(pod_plan& p) {
         const int32_t keys = p.opts.prefill_tile_keys;
         p.pf_tn64 = warpspec && p.batch.has_prefill && (keys == 64 || (keys == 0 && decode_share(p) < 0.57));
         // two S buffers per block (Q in smem, the decode group at 2 ring stages per warp): fused C2
-        // B=8 (decode share 0.17) 356 -> 332 us, B=16 (0.29) 369 -> 365, but C1 (0.32) 56 -> 59 and
-        // B=32 (0.45) 436 -> 555 -- the smaller decode rings cost more than the prefill gains
+        // B=8 (decode share 0.17) 356 -> 332 us, B=16 (0.29) 357 -> 351, but C1 (0.32) 56.3 -> 58.4
+        // and B=32 (0.45) 436 -> 555 -- the smaller decode rings cost more than the prefill gains
         const int32_t sb = p.opts.prefill_s_buffers;
-        p.pf_db = p.pf_tn64 && (sb == 2 || (sb == 0 && decode_share(p) < 0.25));
+        p.pf_db = p.pf_tn64 && (sb == 2 || (sb == 0 && decode_share(p) < 0.30));
     }
     // Whole waves (warp-specialised kernel): the decode items are claimed in id order
     // (request-major) by one decode group per SM, so a count that is not a multiple of
