@@ -23,7 +23,10 @@ def default_candidates(batch: HybridBatchSpec) -> List[Tuple[str, PlanOptions]]:
     c = [("auto", PlanOptions())]
     if batch.prefill is not None:
         c += [("warpspec/32-key", PlanOptions(policy=_abi.POD_POLICY_WARPSPEC, prefill_tile_keys=32)),
-              ("warpspec/64-key", PlanOptions(policy=_abi.POD_POLICY_WARPSPEC, prefill_tile_keys=64))]
+              ("warpspec/64-key", PlanOptions(policy=_abi.POD_POLICY_WARPSPEC, prefill_tile_keys=64,
+                                              prefill_s_buffers=1)),
+              ("warpspec/64-key/double-S", PlanOptions(policy=_abi.POD_POLICY_WARPSPEC, prefill_tile_keys=64,
+                                                       prefill_s_buffers=2))]
     for cap in (0, 2, 4):
         c.append((f"complement/cap{cap or 'auto'}", PlanOptions(policy=_abi.POD_POLICY_COMPLEMENT, split_wave_cap=cap)))
     return c
