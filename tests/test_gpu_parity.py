@@ -177,14 +177,17 @@ def test_fp16_inputs(policy):
         assert np.abs(out.o_decode[r].cpu().numpy() - o).max() <= O_TOL * np.abs(o).max()
 
 
-def test_nhd_layout():
+@pytest.mark.parametrize("d", [128, 64])
+@pytest.mark.parametrize("policy", KERNELS)
+def test_nhd_layout(policy, d):
+    """NHD pools through every kernel (the fp16 V shadow reads them too), d = 128 and 64."""
     _need_gpu()
-    batch = make_batch(pkg.ModelShape(32, 8, 128, SCALE), chunk=50, offset=70, decode_ctx=[90, 17])
+    batch = make_batch(pkg.ModelShape(32, 8, d, math.sqrt(d)), chunk=50, offset=70, decode_ctx=[90, 17])
     wl = build_workload(batch, device="cuda")
     batch.kv_layout = POD_KV_NHD
     wl.k_pool = wl.k_pool.permute(0, 2, 1, 3).contiguous()
     wl.v_pool = wl.v_pool.permute(0, 2, 1, 3).contiguous()
-    _, _, out = _run(batch, wl=wl)
+    _, _, out = _run(batch, wl=wl, options=_kopts(policy))
     _check(wl, out)
 
 
