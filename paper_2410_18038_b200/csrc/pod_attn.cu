@@ -1933,7 +1933,7 @@ pod_status pod_oproj_run(const void* o, const void* w, int64_t tokens, int64_t k
                          int32_t world, int64_t rows_per_rank, int32_t accumulate, void* stream) {
     if (!o || !w || !y_parts || tokens < 1 || k < 1 || n < 1 || world < 1 || world > oproj::kMaxWorld)
         return POD_ERR_INVALID_ARGUMENT;
-    if (k % oproj::kBK || n % oproj::kBN) {
+    if (k % oproj::kBK || n % 128) {
         set_last_error("pod_oproj_run: K must be a multiple of 64 and N of 128");
         return POD_ERR_UNSUPPORTED;
     }
@@ -1993,12 +1993,22 @@ pod_status pod_oproj_run(const void* o, const void* w, int64_t tokens, int64_t k
         cudaError_t e = cudaGetDevice(&dev);
         if (e != cudaSuccess || dev < 0 || dev >= kMaxDev) return cuda_fail(e, "cudaGetDevice");
         std::call_once(once[dev], [&] {
-            err[dev] = cudaFuncSetAttribute(oproj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, oproj::kSmem);
+            err[dev] = cudaFuncSetAttribute(oproj_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            oproj::Cfg<128>::kSmem);
+            if (err[dev] == cudaSuccess)
+                err[dev] = cudaFuncSetAttribute(oproj_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                oproj::Cfg<256>::kSmem);
         });
         if (err[dev] != cudaSuccess) return cuda_fail(err[dev], "o_proj attributes");
     }
-    const dim3 grid(static_cast<unsigned>(n / oproj::kBN), static_cast<unsigned>((tokens + oproj::kBM - 1) / oproj::kBM));
-    oproj_kernel<<<grid, oproj::kThreads, oproj::kSmem, static_cast<cudaStream_t>(stream)>>>(p, ta, tb);
+    // 128 x 256 tiles when N allows (half the A re-reads per output), else 128 x 128
+    const unsigned gy = static_cast<unsigned>((tokens + oproj::kBM - 1) / oproj::kBM);
+    if (n % 256 == 0)
+        oproj_kernel<256><<<dim3(static_cast<unsigned>(n / 256), gy), oproj::kThreads, oproj::Cfg<256>::kSmem,
+                             static_cast<cudaStream_t>(stream)>>>(p, ta, tb);
+    else
+        oproj_kernel<128><<<dim3(static_cast<unsigned>(n / 128), gy), oproj::kThreads, oproj::Cfg<128>::kSmem,
+                             static_cast<cudaStream_t>(stream)>>>(p, ta, tb);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "o_proj launch");
     return POD_OK;
