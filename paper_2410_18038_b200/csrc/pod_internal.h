@@ -16,7 +16,10 @@ constexpr int kHeadDim = 128;       // the compiled head dim (all BASELINE confi
 constexpr int kMBlock = 128;        // tcgen05 M: packed (row, q-head) rows per prefill block
 constexpr int kKvTile = 64;         // prefill keys per tcgen05 N tile (4 pages of 16)
 constexpr int kDecodeWarps = 4;     // virtual decode CTAs per physical CTA
-constexpr int kSmDecodeWarps = 6;   // decode warps of the warp-specialised kernel (pod_sm.cuh)
+#ifndef POD_SM_DEC_WARPS
+#define POD_SM_DEC_WARPS 6
+#endif
+constexpr int kSmDecodeWarps = POD_SM_DEC_WARPS;   // decode warps of the warp-specialised kernel (pod_sm.cuh)
 constexpr int kPrefillWarps = 4;    // softmax warps (one TMEM lane quadrant each)
 constexpr int kThreads = 192;       // 4 softmax warps + 1 TMA-producer warp + 1 MMA warp
 constexpr int kMaxSms = 1024;       // sm counter slots (sized for %nsmid, not %smid density)
