@@ -596,6 +596,10 @@ def run_pod(args, rank, world, local_rank):
 
     info = op.info
     launches_per_step = 1 + (1 if (info.num_merge_rows_prefill or info.num_merge_rows_decode) else 0)  # one merge launch
+    # + the fp16 V shadow's conversion kernel (pod_plan.cpp: bf16 data, F16PV, a prefill on the
+    # two-CTA kernel or the 64-key pair engine)
+    if (chunk and args.precision == 2 and (info.policy == 3 or (info.policy == 7 and info.prefill_tile_keys == 64))):
+        launches_per_step += 1
     res = dict(t_fused=t_fused, ms_fused=ms_fused, t_serial=t_serial, t_pf=t_pf, t_dec=t_dec, t_e2e=t_e2e,
                t_attn=t_attn, t_append=t_append, append_bytes=append_bytes, best=best, tp_check=tp_check,
                oproj=oproj_res,
@@ -734,7 +738,7 @@ def main():
         "plan": {"prefill_ctas": info.num_prefill_ctas, "decode_ctas": info.num_decode_ctas,
                  "prefill_splits": info.prefill_splits, "decode_splits": info.decode_splits,
                  "ratio": f"{info.prefill_ratio}:{info.decode_ratio}", "smem_per_cta": info.smem_bytes,
-                 "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_tile_keys": info.prefill_tile_keys, "prefill_s_buffers": info.prefill_s_buffers, "prefill_p": {0: "bf16 hi+lo", 1: "bf16", 2: "fp16 (V -> fp16 in smem)"}[args.precision], "out_dtype": args.out_dtype},
+                 "policy": {3: "complement", 7: "warpspec"}.get(info.policy, info.policy), "split_wave_cap": info.config.split_wave_cap, "prefill_tile_keys": info.prefill_tile_keys, "prefill_s_buffers": info.prefill_s_buffers, "prefill_p": {0: "bf16 hi+lo", 1: "bf16", 2: "fp16 (V -> fp16: " + ("one shadow pass per launch)" if r["launches"] > 1 + (1 if (info.num_merge_rows_prefill or info.num_merge_rows_decode) else 0) else "per tile in smem)")}[args.precision], "out_dtype": args.out_dtype},
         "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": {7: "pod_sm_kernel (+merge)"}.get(r["info"].policy, "pod_fused_kernel (+merge)"),
