@@ -18,7 +18,10 @@
 // traffic per row), ping-ponging the tensor core between the blocks' softmax.
 // Two tile widths share the layout: 32-key tiles with double-buffered S
 // (prefill_item_sm, decode-dominant plans) and 64-key tiles with one S buffer per
-// block (prefill_item_sm64, prefill-dominant plans; RunParams::pf_tn64).
+// block (prefill_item_sm64, prefill-dominant plans; RunParams::pf_tn64).  The most
+// prefill-dominant plans (RunParams::pf_db) run a second kernel instance (kE = 1): 64-key
+// tiles with two S buffers per block, Q in shared memory (prefill_item_db, SmLay<1>).
+// Plans with RunParams::vs_pages read V from the per-launch fp16 shadow (no conversion).
 //
 // Role binding is still SM-aware and dynamic: every SM hosts both roles for as
 // long as both pools have work (the placement the POD scheduler aims for,
