@@ -179,8 +179,8 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                        __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
 }
 #ifndef POD_EXP_POLY
-#define POD_EXP_POLY 0  // pairs per 8 whose exp2 runs on the FMA pipe (0 = all on MUFU; 2-4 measured
-                        // 1-3 % slower on B200: the softmax is not MUFU-bound)
+#define POD_EXP_POLY 0  // default pairs per 8 whose exp2 runs on the FMA pipe (0 = all on MUFU; the
+                        // double-S pair engine passes 1 explicitly)
 #endif
 
 template <int kFmt>
@@ -239,7 +239,7 @@ __device__ __forceinline__ void prefill_issue_pv(uint32_t tmem_o, uint32_t tmem_
 //            [0,32), lo in [32,64); hi + lo keeps ~15 mantissa bits
 //   kMode 2: hi + lo rounded to nearest (fp16 inputs)
 //   kMode 3: one P rounded to fp16 (POD_PRECISION_F16PV), columns [0, kN/2)
-template <int kFmt, int kMode, int kN = kKvTile>
+template <int kFmt, int kMode, int kN = kKvTile, int kPoly = POD_EXP_POLY>
 __device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, float neg_m, uint32_t s_addr) {
     const float2 sl2v = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
     float2 lsum2 = make_float2(0.f, 0.f), lsum2b = make_float2(0.f, 0.f);  // two chains
@@ -253,7 +253,7 @@ __device__ __forceinline__ float softmax_p_row(const float (&s)[kN], float sl2, 
             const float p0 = x.x * 0.5f, p1 = x.y * 0.5f;
 #else
             float p0, p1;
-            if (POD_EXP_POLY > 0 && (c / 2) % 8 >= 8 - POD_EXP_POLY) {
+            if (kPoly > 0 && (c / 2) % 8 >= 8 - kPoly) {  // kPoly of every 8 pairs on the FMA pipe
                 const float2 e = ex2_poly2(x);
                 p0 = e.x;
                 p1 = e.y;

@@ -1153,14 +1153,18 @@ __device__ void prefill_item_db(const RunParams& p, const CUtensorMap* tmk, cons
             }
             const float neg_m = m_use == -INFINITY ? 0.f : -m_use;
             float lsum;
+            // one pair in 8 of the exponentials on the FMA pipe (ex2_poly2): with two S buffers
+            // per block the two blocks' softmax phases overlap and share the MUFU (fused C2 B=8
+            // 333 -> 321 us; the single-S and two-CTA engines measured no gain or a loss)
+            constexpr int kPoly = 1;
             if (kFmt == 1 && p.p_f16)
-                lsum = softmax_p_row<kFmt, 3, kTN>(s, p.sl2, neg_m, s_addr);
+                lsum = softmax_p_row<kFmt, 3, kTN, kPoly>(s, p.sl2, neg_m, s_addr);
             else if (kFmt == 1 && p.p_split)
-                lsum = softmax_p_row<kFmt, 1, kTN>(s, p.sl2, neg_m, s_addr);
+                lsum = softmax_p_row<kFmt, 1, kTN, kPoly>(s, p.sl2, neg_m, s_addr);
             else if (p.p_split)
-                lsum = softmax_p_row<kFmt, 2, kTN>(s, p.sl2, neg_m, s_addr);
+                lsum = softmax_p_row<kFmt, 2, kTN, kPoly>(s, p.sl2, neg_m, s_addr);
             else
-                lsum = softmax_p_row<kFmt, 0, kTN>(s, p.sl2, neg_m, s_addr);
+                lsum = softmax_p_row<kFmt, 0, kTN, kPoly>(s, p.sl2, neg_m, s_addr);
             l_run += lsum;
             if (convert) v_to_f16(t);  // V(t) before P(t) goes to the MMA issuer
             ptx::tmem_wait_st();
