@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_reference_cases.py tests/test_gpu_fuzz.py -x -q 2>&1 | tail -2
-for c in c2_b8 c2_b16; do echo "== $c"; bash tools/exp.sh $c 2:0:8 2:0:8 ; done
+for i in 1 2; do bash tools/exp.sh c1 2:64:7::0:1 2:64:7::0:2; done
+bash tools/exp.sh c2_b32 2:64:7::0:1 2:64:7::0:2
