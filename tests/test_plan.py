@@ -303,3 +303,32 @@ def test_decode_split_count_per_request_is_clamped_to_context():
         i = p.info()
         assert i.num_decode_ctas == 8 * (1 + 3 + 4)
         assert i.num_merge_rows_decode == 2 * 32  # requests 1 and 2 merge, request 0 writes directly
+
+
+def test_auto_engine_choice_and_v_shadow_workspace():
+    """AUTO's measured engine rules at the BASELINE shapes (pod_plan.cpp):
+    the 64-key pair engine below a decode share of 0.57, with two S buffers below 0.30, the
+    32-key engine above; the fp16 V shadow (prefill V converted once per launch) for F16PV
+    bf16 plans on the two-CTA kernel and the 64-key engine, sized [pages][Hkv][16][d] fp16."""
+    from paper_2410_18038_b200._abi import POD_PRECISION_SPLIT, POD_POLICY_COMPLEMENT
+    shape = ModelShape(32, 8, 128, math.sqrt(128))
+
+    def c2(nb):
+        return HybridBatchSpec(prefill=PrefillSpec(1024, 16384, 15360), decodes=[DecodeSpec(16384)] * nb,
+                               shape=shape)
+
+    want = {8: (64, 2), 16: (64, 2), 32: (64, 1), 64: (32, 2)}  # decode share 0.17 / 0.29 / 0.45 / 0.62
+    for nb, (keys, sb) in want.items():
+        i = Plan(c2(nb), GpuSpec.b200()).info()
+        assert (i.prefill_tile_keys, i.prefill_s_buffers) == (keys, sb), nb
+    c1 = HybridBatchSpec(prefill=PrefillSpec(512, 2048, 1536), decodes=[DecodeSpec(2048)] * 8, shape=shape)
+    assert (Plan(c1, GpuSpec.b200()).info().prefill_tile_keys, Plan(c1, GpuSpec.b200()).info().prefill_s_buffers) == (64, 1)
+    # the shadow: 16384 keys = 1024 logical pages x 8 KV heads x 16 x 128 x 2 B = 32 MiB of workspace
+    shadow = 1024 * 8 * 16 * 128 * 2
+    ws = {}
+    for name, opts in (("complement", PlanOptions(policy=POD_POLICY_COMPLEMENT)),
+                       ("complement_split", PlanOptions(policy=POD_POLICY_COMPLEMENT, precision=POD_PRECISION_SPLIT)),
+                       ("ws32", PlanOptions(prefill_tile_keys=32)), ("ws64", PlanOptions(prefill_tile_keys=64))):
+        ws[name] = Plan(c2(64), GpuSpec.b200(), opts).workspace_bytes()
+    assert ws["complement"] - ws["complement_split"] >= shadow  # F16PV adds the shadow, SPLIT does not
+    assert ws["ws64"] - ws["ws32"] >= shadow - (1 << 20)        # 64-key plans carry it, 32-key ones do not
