@@ -1,3 +1,12 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-for i in 1 2; do bash tools/exp.sh c1 2:64:7::0:1 2:64:7::0:2; done
-bash tools/exp.sh c2_b32 2:64:7::0:1 2:64:7::0:2
+for pol in 8 3; do timeout 900 python tools/sweep.py --heads 32,32 --chunks 512,2048 --ctx 4096,16384 --batches 32,128 --policy $pol > gpurun_out/mha_sweep_$pol.jsonl 2>&1; done
+python - <<'PY'
+import json
+rows = {}
+for pol in (8, 3):
+    for l in open(f"gpurun_out/mha_sweep_{pol}.jsonl"):
+        if l.startswith("{") and "fused_us" in l:
+            d = json.loads(l); rows.setdefault((d["chunk"], d["ctx"], d["batch"]), {})[pol] = (d["fused_us"], d["policy"])
+for k, v in sorted(rows.items()):
+    print(k, v)
+PY

@@ -31,13 +31,15 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--max-kv-gb", type=float, default=80.0)
     ap.add_argument("--policy", type=int, default=8, help="POD_POLICY_* (8 = AUTO)")
+    ap.add_argument("--heads", default="32,8", help="q heads, kv heads")
     a = ap.parse_args()
     pk = peaks()
-    shape = pkg.ModelShape(32, 8, 128, math.sqrt(128))
+    hq, hkv = map(int, a.heads.split(","))
+    shape = pkg.ModelShape(hq, hkv, 128, math.sqrt(128))
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for ctx in map(int, a.ctx.split(",")):
         for b in map(int, a.batches.split(",")):
-            kv_gb = b * ctx * 8 * 128 * 4 / 1e9
+            kv_gb = b * ctx * hkv * 128 * 4 / 1e9
             if kv_gb > a.max_kv_gb:
                 print(json.dumps({"ctx": ctx, "batch": b, "skipped": f"{kv_gb:.0f} GB of KV"}))
                 continue
