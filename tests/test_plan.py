@@ -332,3 +332,18 @@ def test_auto_engine_choice_and_v_shadow_workspace():
         ws[name] = Plan(c2(64), GpuSpec.b200(), opts).workspace_bytes()
     assert ws["complement"] - ws["complement_split"] >= shadow  # F16PV adds the shadow, SPLIT does not
     assert ws["ws64"] - ws["ws32"] >= shadow - (1 << 20)        # 64-key plans carry it, 32-key ones do not
+
+
+def test_tuned_options_signature_buckets():
+    """tune.TunedOptions memoises per bucketed batch signature: decode contexts and the
+    prefill offset round up to the bucket, so nearby serving-loop shapes share one search."""
+    from paper_2410_18038_b200.tune import TunedOptions, default_candidates
+    shape = ModelShape(32, 8, 128, math.sqrt(128))
+    t = TunedOptions(bucket=256)
+    a = HybridBatchSpec(prefill=PrefillSpec(256, 2048, 1792), decodes=[DecodeSpec(2048)] * 4, shape=shape)
+    b = HybridBatchSpec(prefill=PrefillSpec(256, 1956, 1700), decodes=[DecodeSpec(2000)] * 4, shape=shape)
+    c = HybridBatchSpec(prefill=PrefillSpec(256, 2300, 2044), decodes=[DecodeSpec(2300)] * 4, shape=shape)
+    assert t.signature(a) == t.signature(b) != t.signature(c)
+    names = [n for n, _ in default_candidates(a)]
+    assert names[0] == "auto" and "warpspec/64-key/double-S" in names and len(names) == len(set(names))
+    assert [n for n, _ in default_candidates(HybridBatchSpec(decodes=[DecodeSpec(100)], shape=shape))][0] == "auto"
