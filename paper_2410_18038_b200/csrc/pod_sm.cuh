@@ -1195,9 +1195,15 @@ struct SmLay {
     static constexpr uint32_t kOffDec = sm3::kOffDec, kOffBars = sm3::kOffBars, kOffDecBars = sm3::kOffDecBars,
                               kOffMisc = sm3::kOffMisc, kSmem = sm3::kSmem;
 };
+#ifndef POD_DB_DEC_WARPS
+#define POD_DB_DEC_WARPS 4  // the double-S instance's decode group: warps x ring stages (6 x 2: C2 B=8 322 vs 316 us)
+#endif
+#ifndef POD_DB_DEC_STAGES
+#define POD_DB_DEC_STAGES 3
+#endif
 template <>
 struct SmLay<1> {
-    static constexpr int kDW = sm3::kDW, kDS = 2;
+    static constexpr int kDW = POD_DB_DEC_WARPS, kDS = POD_DB_DEC_STAGES;
     static constexpr uint32_t kOffDec = db::kPfBytes;
     static constexpr uint32_t kOffBars = kOffDec + kDW * kDS * kDecStageBytes;
     static constexpr uint32_t kOffDecBars = kOffBars + sm3::kNumBars * 8;
@@ -1231,7 +1237,7 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
                   const __grid_constant__ CUtensorMap tdv) {
     using namespace sm3;
     using L = SmLay<kE>;
-    constexpr int kDS = L::kDS;
+    constexpr int kDS = L::kDS, kDW = L::kDW;  // (kDW < sm3::kDW leaves the last warps idle)
     constexpr uint32_t kOffDec = L::kOffDec, kOffBars = L::kOffBars, kOffDecBars = L::kOffDecBars,
                        kOffMisc = L::kOffMisc;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -1323,7 +1329,7 @@ __global__ void __launch_bounds__(sm3::kThreads, 1)
         // ============================================= decode engine ===
         const int dw = warp - kDecWarp0;
         int dpos = 0;
-        while (p.num_dctas > 0) {
+        while (p.num_dctas > 0 && dw < kDW) {
             if (dw == 0 && lane == 0) {
                 int id = static_cast<int>(atomicAdd(&p.ctr->cta_assign[1], 1u));
                 if (id >= p.num_dctas) id = -1;
