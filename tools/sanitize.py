@@ -50,6 +50,7 @@ def main():
     cases = [
         (small, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC), ("fused", "serial")),
         (small, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64), ("fused",)),
+        (small, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=64, prefill_s_buffers=2), ("fused", "serial")),
         (small, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=32, decode_splits=3), ("fused",)),
         (small, pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT, split_wave_cap=4, decode_splits=2), ("fused", "serial")),
     ]
@@ -59,8 +60,9 @@ def main():
     run(d64, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC), ("fused",))  # head dim 64, zero-padded
     run(d64, pkg.PlanOptions(policy=POD_POLICY_COMPLEMENT, decode_splits=2), ("fused",))
     many = make_batch(shape, chunk=256, offset=200, decode_ctx=[300, 64, 5])
-    for keys in (32, 64):
-        run(many, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=keys), ("fused",), nsm=3)
+    for keys, sb in ((32, 0), (64, 1), (64, 2)):
+        run(many, pkg.PlanOptions(policy=POD_POLICY_WARPSPEC, prefill_tile_keys=keys, prefill_s_buffers=sb), ("fused",),
+            nsm=3)
     # the o_proj consumer: store and reduce-scatter epilogues (virtual ranks)
     from paper_2410_18038_b200.tp import oproj
     o = (torch.rand(200, 512, device="cuda") - 0.5).to(torch.bfloat16)
